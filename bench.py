@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the local-smoothing GMG hot path on B200 (BASELINE.json metric:
+V-cycle DoFs/s and level-vmult HBM GB/s as a fraction of peak).
+
+A step is one V-cycle preconditioner application x = V(b) (P:318-327 with local
+smoothing) on the config-3 forest (3D Poisson, Q2, sphere-refined,
+49.8M leaf DoFs, 11 levels), b uniform[-1,1) by canonical index, resident in
+HBM.  DoFs = all leaf nodes (reading R22).  Inputs are larger than L2 (every
+multigrid-layout vector is 466 MB > 126 MB), so no flush is needed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3] [--profile]
+
+--impl reference times the CPU oracle (oracle/, numpy/scipy, as it stands) on
+a bounded sample of the same workload family (c3 recipe truncated at 4 passes).
+For N > 1 this version runs N independent replicas (one per GPU, weak scaling,
+no collective): the sharded multi-GPU V-cycle is not implemented yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V-cycle DoFs/s and level vmult HBM GB/s (fraction of peak) at 1/2/4/8 B200"
+UNIT = "DoFs/s"
+WORKLOADS = {
+    "c3": "BASELINE configs[2]: 3D Poisson -Laplace u = f on [0,1]^3, Q2, fp64, Dirichlet; 3 global "
+          "refinements + 7 sphere-surface passes (|x-(.5,.5,.5)| = 0.3), 2:1 vertex balanced",
+    "c2": "BASELINE configs[1]: 2D L-shape Q2, corner-graded to ~1M DoFs",
+    "c3p4": "c3 recipe truncated at 4 passes (774,181 DoFs)",
+}
+SAMPLE = "c3p4"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.12)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        time.sleep(0.06)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        import statistics
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+def oracle_sample(steps: int, warmup: int):
+    """The oracle V-cycle, as it stands, on the bounded sample (c3 recipe at 4 passes)."""
+    import numpy as np
+    from gmg_inputs import config, uniform_pm1
+    from oracle import forest as F, mg
+    cfg = config(SAMPLE)
+    t0 = time.time()
+    f = F.generate(cfg)
+    h = mg.build(f, cfg["k"])
+    setup = time.time() - t0
+    b = uniform_pm1(h.leaf.n_free)
+    n_dofs = int(h.leaf.X.shape[0])
+    for _ in range(warmup):
+        mg.vcycle(h, b)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        mg.vcycle(h, b)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return dict(value=n_dofs / dt, sec_per_vcycle=dt, n_dofs=n_dofs, setup_s=setup)
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    r = oracle_sample(args.steps, args.warmup)
+    cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{SAMPLE}: c3 recipe at 4 passes, {r['n_dofs']} DoFs, one V-cycle per step "
+                     f"(scipy CSR level matrices, single thread), setup {r['setup_s']:.1f}s excluded"}
+    out = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * r["sec_per_vcycle"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": WORKLOADS[SAMPLE], "sample_of": args.config},
+           "cpu_baseline": cpu,
+           "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1904_03317_b200 as G
+    from gmg_inputs import config, uniform_pm1
+
+    rank, world, local = env_rank()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = config(args.config)
+    t0 = time.time()
+    f, part, h = G.build_config(cfg)
+    setup_s = time.time() - t0
+    info = h.info()
+    n_free = info["n_leaf_free"]
+    n_dofs = info["n_leaf_nodes"]
+    b = torch.tensor(uniform_pm1(n_free), device=dev, dtype=torch.float64)
+    x = torch.zeros_like(b)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 1)):
+        h.vcycle(b, x)
+    barrier()
+    if args.profile:
+        torch.cuda.profiler.start()
+        h.vcycle(b, x)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+    launches0 = h.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.vcycle(b, x)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    launches = h.launch_count() - launches0
+    t_dev = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_dev], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    value = world * n_dofs * args.steps / t_dev
+
+    # ---- roofline of the dominant kernel: cell_apply on the finest level
+    L = info["n_levels"] - 1
+    nL = info["level_dofs"][L]
+    ncell = info["level_cells"][L]
+    nn = (cfg["k"] + 1) ** cfg["dim"]
+    xa = torch.tensor(uniform_pm1(nL), device=dev, dtype=torch.float64)
+    ya = torch.zeros_like(xa)
+    for _ in range(3):
+        h.level_apply(L, xa, ya)
+    reps = 20
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a0.record(stream)
+    for _ in range(reps):
+        h.level_apply(L, xa, ya)
+    a1.record(stream)
+    a1.synchronize()
+    t_apply = a0.elapsed_time(a1) / 1e3 / reps   # includes the y memset (cudaMemsetAsync)
+    alg_bytes = 16 * nL + 4 * nn * ncell          # x read + y write + index table
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / t_apply / 1e9
+    applies_per_vc = 2 * args.cheb_degree         # (m-1) pre + 1 residual + m post on every level
+    share = applies_per_vc * t_apply / (t_dev / args.steps)
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies timed
+    bh = torch.tensor(uniform_pm1(n_free), dtype=torch.float64).pin_memory()
+    xh = torch.empty(n_free, dtype=torch.float64).pin_memory()
+    bd = torch.empty_like(b)
+    xd = torch.empty_like(b)
+    for _ in range(2):
+        bd.copy_(bh, non_blocking=True)
+        h.vcycle(bd, xd)
+        xh.copy_(xd, non_blocking=True)
+    barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 20))
+    s0.record(stream)
+    for _ in range(e2e_steps):
+        bd.copy_(bh, non_blocking=True)
+        h.vcycle(bd, xd)
+        xh.copy_(xd, non_blocking=True)
+    s1.record(stream)
+    s1.synchronize()
+    t_e2e = s0.elapsed_time(s1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = world * n_dofs * e2e_steps / t_e2e
+
+    # ---- one GMG-CG solve (context, not the metric)
+    bb = torch.zeros_like(b)
+    h.rhs_constant(1.0, bb)
+    xs = torch.zeros_like(b)
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    its, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
+    torch.cuda.synchronize()
+    t_cg = time.perf_counter() - c0
+
+    per_vc, per_la = h.launch_profile()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_sample(steps=3, warmup=1)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{SAMPLE}: c3 recipe at 4 passes, {r['n_dofs']} DoFs, 3 oracle V-cycles "
+                         f"(scipy CSR, single thread), setup excluded"}
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
+                          "n_leaf_dofs": n_dofs, "n_free_dofs": n_free, "levels": info["n_levels"],
+                          "level_dofs": info["level_dofs"], "k": cfg["k"], "dim": cfg["dim"],
+                          "cheb_degree": args.cheb_degree, "global_batch": 1,
+                          "l2": "inputs larger than L2 (MG-layout vectors %.0f MB each > 126 MB)"
+                                % (info["mg_vector_len"] * 8 / 1e6),
+                          "parallelism": "single GPU" if world == 1 else
+                          f"{world} independent replicas (sharded V-cycle not implemented)",
+                          "setup_s": round(setup_s, 2)},
+               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                            "frac": achieved / peak, "traffic": None, "kernel": "cell_apply<3,2> finest level",
+                            "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,
+                            "share_of_step": share, "peak_source": peak_src},
+               "cpu_baseline": cpu,
+               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_free,
+                       "d2h_bytes_per_step": 8 * n_free},
+               "gpu_launches": launches,
+               "launches_per_vcycle": per_vc,
+               "clocks": clk.summary(),
+               "cg": {"iters": its, "rel_res": relres, "seconds": t_cg, "rtol": 1e-8,
+                      "dofs_per_s": n_dofs / t_cg}}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--cheb-degree", type=int, default=4)
+    ap.add_argument("--profile", action="store_true", help="cudaProfilerStart/Stop around one V-cycle")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.profile:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

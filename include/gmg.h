@@ -1,0 +1,262 @@
+/* gmg.h -- C ABI of libgmg: the data-parallel hot path of the local-smoothing
+ * adaptive geometric multigrid of Clevenger, Heister, Kanschat, Kronbichler,
+ * "A Flexible, Parallel, Adaptive Geometric Multigrid method for FEM"
+ * (arXiv 1904.03317), built for NVIDIA B200 (sm_100a).  Citations "P:n" are
+ * line numbers of PAPER.md (the paper's LaTeX); readings of the paper are the
+ * "R#" entries of DESIGN.md.
+ *
+ * Conventions (all calls):
+ *  - Every call returns gmg_status; GMG_OK == 0.  No exception crosses the ABI.
+ *    On error, gmg_last_error() returns a thread-local message.
+ *  - Handles are opaque, owned by the library, immutable after creation except
+ *    through the documented setters, and destroyed by the matching *_destroy.
+ *  - "host" pointers are caller-owned host memory, "device" pointers
+ *    caller-owned CUDA device memory (fp64, int32, ...) on the hierarchy's device.
+ *  - Export functions follow the size-query idiom: pass NULL arrays to obtain
+ *    the count in *n, then call again with arrays of that size.
+ *  - Device work is enqueued on the caller's `cuda_stream` (cudaStream_t, NULL =
+ *    legacy default stream); calls return without synchronising unless stated.
+ */
+#ifndef GMG_H
+#define GMG_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GMG_OK = 0,
+  GMG_E_INVALID_ARG = 1,   /* null pointer, out-of-range argument */
+  GMG_E_UNSORTED = 2,      /* leaves not strictly increasing in SFC order */
+  GMG_E_NOT_TILING = 3,    /* leaves overlap or leave holes in the brick */
+  GMG_E_UNBALANCED = 4,    /* 2:1 vertex balance violated */
+  GMG_E_DEPTH = 5,         /* level too deep for 64-bit lattice keys */
+  GMG_E_STATE = 6,         /* call not valid in this state (e.g. no device data) */
+  GMG_E_ZERO_DIAG = 7,     /* zero diagonal on a smoothed row */
+  GMG_E_SINGULAR_COARSE = 8,/* coarse matrix not SPD */
+  GMG_E_NOT_CONVERGED = 9, /* CG reached max_it (x = last iterate) */
+  GMG_E_CUDA = 10,         /* CUDA runtime error */
+  GMG_E_NCCL = 11,         /* NCCL error */
+  GMG_E_OOM = 12           /* host or device allocation failed */
+} gmg_status;
+
+typedef struct gmg_forest gmg_forest;
+typedef struct gmg_partitioning gmg_partitioning;  /* handle made by gmg_partition() */
+typedef struct gmg_hierarchy gmg_hierarchy;
+
+const char *gmg_last_error(void);
+int gmg_abi_version(void);
+
+/* ------------------------------------------------------------------ forest
+ * A forest of quad-/octrees over a brick of unit trees.  A cell is
+ * identified by (tree, level, morton): level = distance to the root, morton =
+ * the path bits from the root, d bits per level, x the fastest bit (the z-curve
+ * of P:603).  Trees are ordered by the z-order of their brick
+ * positions.  Refinement is isotropic into 2^d children.
+ */
+#define GMG_CLOSE_BALANCE 1u   /* close to 2:1 vertex balance instead of rejecting */
+
+/* tree_xyz: host [n_trees*dim] brick coordinates (>= 0) of the trees (any order,
+ *   they are re-sorted to z-order; leaf_tree indexes the z-ordered list).
+ * leaf_tree / leaf_level / leaf_morton: host [n_leaves], the leaves in SFC
+ *   order (tree, then Morton within the tree).
+ * Errors: INVALID_ARG (dim not 2/3, n_trees < 1, duplicate tree), DEPTH,
+ *   UNSORTED, NOT_TILING, UNBALANCED (unless GMG_CLOSE_BALANCE). */
+gmg_status gmg_forest_create(int dim, int n_trees, const int32_t *tree_xyz, int64_t n_leaves,
+                             const int32_t *leaf_tree, const int8_t *leaf_level,
+                             const uint64_t *leaf_morton, uint32_t flags, gmg_forest **out);
+
+/* Synthetic config forests (BASELINE.json configs).
+ * Each pass marks the leaves satisfying the rule, refines them and closes the
+ * forest to 2:1 vertex balance ("completed by a closure after each refinement
+ * step").  n_passes < 0: repeat until no leaf is marked. */
+typedef enum {
+  GMG_RULE_NONE = 0,
+  GMG_RULE_CENTER_BALL = 1,    /* |centre(T) - c| <= r                      (config 1) */
+  GMG_RULE_SPHERE_SURFACE = 2, /* min_T |x-c| <= r+w  and  max_T |x-c| >= r-w (3, 5) */
+  GMG_RULE_CORNER_DIST = 3     /* level(T) < lmax and dist(T, corner) <= 2^(s-level) (2, 4) */
+} gmg_rule;
+
+typedef struct {
+  int dim;
+  int n_trees;
+  int32_t tree_xyz[8 * 3];     /* brick positions */
+  int global_refinements;
+  gmg_rule rule;
+  int n_passes;                /* < 0: to a fixed point */
+  int64_t center_num[3], center_den[3]; /* rule point c (brick units, exact rational) */
+  int64_t radius_num, radius_den;       /* r */
+  int64_t shell_num, shell_den;         /* w (sphere shell half-width; 0/1 = surface) */
+  int64_t corner[3];           /* integer brick point for CORNER_DIST */
+  int s, lmax;                 /* CORNER_DIST parameters */
+} gmg_recipe;
+
+gmg_status gmg_forest_generate(const gmg_recipe *recipe, gmg_forest **out);
+gmg_status gmg_forest_destroy(gmg_forest *f);
+gmg_status gmg_forest_info(const gmg_forest *f, int *dim, int *n_trees, int64_t *n_leaves,
+                           int *max_level);
+/* host arrays [n_leaves] (any may be NULL) */
+gmg_status gmg_export_leaves(const gmg_forest *f, int32_t *leaf_tree, int8_t *leaf_level,
+                             uint64_t *leaf_morton);
+
+/* ------------------------------------------------------------------ partition
+ * First-child-rule partition: the SFC-ordered leaves are cut into
+ * n_ranks contiguous intervals, the first (N mod n_ranks) ranks receiving
+ * ceil(N/n_ranks) leaves (R4); every other cell is owned by the owner of its
+ * first child, recursively -- equivalently by the owner of the first SFC leaf
+ * of its subtree.  Pure integer work, no communication.
+ * Errors: INVALID_ARG when n_ranks < 1. */
+gmg_status gmg_partition(const gmg_forest *f, int n_ranks, gmg_partitioning **out);
+gmg_status gmg_partition_destroy(gmg_partitioning *p);
+
+#define GMG_MAX_LEVELS 64
+/* Partition-efficiency model of P:622-666 in exact integers.  N_l counts the
+ * cells strictly on level l (R2).  W0_override < 0: level 0 is an ordinary
+ * level (the worked example P:699-711, R3); otherwise W_0 := W0_override in
+ * W_opt, W_sync and W.  eta = W_opt / W as a reduced fraction. */
+typedef struct {
+  int n_levels;
+  int n_ranks;
+  int64_t W_opt_num, W_opt_den;
+  int64_t W_sync;
+  int64_t W;
+  int64_t eta_num, eta_den;
+  int64_t N[GMG_MAX_LEVELS];
+  int64_t W_l[GMG_MAX_LEVELS];
+  int64_t ghost_children[GMG_MAX_LEVELS]; /* cells of level l whose owner != parent's */
+  int64_t children[GMG_MAX_LEVELS];
+} gmg_model;
+gmg_status gmg_partition_model(const gmg_partitioning *p, int64_t W0_override, gmg_model *out);
+/* N_{l,p}: host [n_levels * n_ranks], row-major by level */
+gmg_status gmg_export_tallies(const gmg_partitioning *p, int64_t *N_lp);
+/* Cells of level l in SFC order: Morton key of the global brick coordinates on
+ * the level-l lattice, owner, leaf flag.  Size query with NULL arrays. */
+gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t *n, uint64_t *key,
+                                  int32_t *owner, uint8_t *is_leaf);
+
+/* ------------------------------------------------------------------ hierarchy
+ * Level spaces (notation of DESIGN.md): C_l = cells of level l,
+ * D_l = their Q_k nodes, B_l = D_l on the boundary (homogeneous Dirichlet),
+ * E_l = D_l \ B_l on the closure of a leaf of level < l (refinement edge),
+ * S_l = the rest (smoothed).  Level vectors hold the S u E DoFs in
+ * global order (owner, Morton key of the node's finest-lattice coordinates);
+ * owner of a node = min owner of the level cells having it as a node.
+ * Free leaf DoFs (non-hanging, non-Dirichlet) are numbered (owner, key) with
+ * owner = the level owner at lambda(n) = max{ l : n in S_l }.
+ */
+#define GMG_HOST_ONLY 1u      /* integer topology only, no device data (exports, CPU tests) */
+#define GMG_NO_GRAPH 2u       /* do not capture the V-cycle in a CUDA graph */
+#define GMG_LOCAL_RANKS 4u    /* all n_ranks logical ranks in this process (not yet used) */
+
+typedef struct {
+  int k;                    /* Q_k degree, 1 or 2 */
+  int cheb_degree;          /* Chebyshev degree m (R6; default 4) */
+  double cheb_lo, cheb_hi;  /* eigenvalue range factors (0.08, 1.2) */
+  int eig_iters;            /* CG iterations of the eigenvalue estimate (10) */
+  const double *coef_level2;/* host [#level-2 cells] coefficient per level-2 cell in SFC
+                               order (config 4), NULL = constant 1 */
+  int rank, n_ranks;        /* this process' rank; must equal the partition's n_ranks */
+  void *nccl_comm;          /* ncclComm_t for n_ranks > 1 (not yet used), else NULL */
+  int device;               /* CUDA device ordinal; -1 = current */
+  uint32_t flags;           /* GMG_HOST_ONLY | GMG_NO_GRAPH */
+} gmg_params;
+
+/* Fills *p with the defaults above (k = 2). */
+void gmg_params_default(gmg_params *p);
+
+/* Builds the level topology (host, integer) and, unless GMG_HOST_ONLY, uploads
+ * the hierarchy to the device, computes D^{-1} on S rows, the eigenvalue
+ * estimates of D^{-1} A_l^S per level and factors the coarse matrix
+ * A_0^S (dense Cholesky).  Synchronises the device.
+ * Errors: INVALID_ARG, STATE, ZERO_DIAG, SINGULAR_COARSE, CUDA, OOM. */
+gmg_status gmg_setup(const gmg_forest *f, const gmg_partitioning *p, const gmg_params *params,
+                     gmg_hierarchy **out);
+gmg_status gmg_hierarchy_destroy(gmg_hierarchy *h);
+
+typedef struct {
+  int dim, k, n_levels, n_ranks, rank;
+  int64_t n_leaf_nodes;      /* all leaf nodes incl. hanging and Dirichlet (R22) */
+  int64_t n_leaf_free;       /* free leaf DoFs (global) */
+  int64_t n_leaf_hanging, n_leaf_dirichlet;
+  int64_t n_owned;           /* free leaf DoFs owned by this rank */
+  int64_t first_owned;       /* global leaf index of the first owned DoF */
+  int64_t level_dofs[GMG_MAX_LEVELS];  /* |S_l u E_l| (global) */
+  int64_t level_cells[GMG_MAX_LEVELS];
+  int64_t level_families[GMG_MAX_LEVELS];
+  int64_t level_S[GMG_MAX_LEVELS], level_E[GMG_MAX_LEVELS], level_B[GMG_MAX_LEVELS];
+  int64_t level_leaf_cells[GMG_MAX_LEVELS];
+  int64_t mg_vector_len;     /* sum of the level vector lengths */
+} gmg_info;
+gmg_status gmg_hierarchy_info(const gmg_hierarchy *h, gmg_info *out);
+
+/* Level DoFs of `level` in global order: Morton key, class (0 = S, 1 = E),
+ * owner, canonical index (position in the Morton order = the p = 1 numbering). */
+gmg_status gmg_export_level_dofs(const gmg_hierarchy *h, int level, int64_t *n, uint64_t *key,
+                                 uint8_t *cls, int32_t *owner, int64_t *canonical);
+/* Free leaf DoFs in global leaf order: key, lambda, owner, canonical index. */
+gmg_status gmg_export_leaf_dofs(const gmg_hierarchy *h, int64_t *n, uint64_t *key, int8_t *lambda,
+                                int32_t *owner, int64_t *canonical);
+/* Cell -> level-DoF table of `level` (global index, -1 for Dirichlet nodes):
+ * host [n_cells * (k+1)^d], cells in SFC order, local nodes x fastest. */
+gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_cells,
+                                int64_t *dofs);
+
+/* ------------------------------------------------------------------ hot path
+ * All vectors below are DEVICE fp64 arrays.  "leaf vector": length n_owned in
+ * the rank's global leaf order.  "level vector": length level_dofs[level] in
+ * global level order.  p = 1 only in this version (n_ranks > 1 -> STATE). */
+
+/* One V-cycle (P:318-327 with local smoothing P:413-469), x = V(b), x0 = 0:
+ * Chebyshev-Jacobi pre/post smoothing of degree m on S rows, residual with the
+ * edge matrices (E rows), restriction R = P^T, recursion, dense coarse solve,
+ * prolongation.  b and x must not alias. */
+gmg_status gmg_vcycle(gmg_hierarchy *h, const double *b_dev, double *x_dev, void *cuda_stream);
+
+/* Preconditioned CG on the leaf system (hanging nodes condensed, Dirichlet
+ * removed) with one V-cycle as preconditioner, x0 = 0, stopping at the first
+ * iterate with ||b - A x||_2 <= rtol ||b||_2.  Returns
+ * NOT_CONVERGED (x = last iterate) when max_it is reached.  *iters and
+ * *rel_res (may be NULL) are set in both cases.  Synchronises the stream once
+ * per iteration (convergence check). */
+gmg_status gmg_solve_cg(gmg_hierarchy *h, const double *b_dev, double *x_dev, double rtol,
+                        int max_it, int *iters, double *rel_res, void *cuda_stream);
+
+/* b_i = int f phi_i for constant f on the free leaf DoFs (hanging-node
+ * condensed), leaf vector. */
+gmg_status gmg_rhs_constant(gmg_hierarchy *h, double f, double *b_dev, void *cuda_stream);
+
+/* Single-operator entry points (parity checks, ncu runs). */
+/* y = K_l x over all cells of C_l on S u E rows (edge rows included). */
+gmg_status gmg_level_apply(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
+                           void *cuda_stream);
+/* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1) */
+gmg_status gmg_restrict(gmg_hierarchy *h, int level, const double *r_fine_dev,
+                        double *d_coarse_dev, void *cuda_stream);
+/* x_fine += P_l x_coarse on all fine rows (level >= 1) */
+gmg_status gmg_prolongate(gmg_hierarchy *h, int level, const double *x_coarse_dev,
+                          double *x_fine_dev, void *cuda_stream);
+/* v = A_leaf u (hanging-node condensed leaf operator), leaf vectors */
+gmg_status gmg_leaf_apply(gmg_hierarchy *h, const double *u_dev, double *v_dev,
+                          void *cuda_stream);
+/* x^S = Cheb(A^S, g^S - A^{SE} x^E, x^S) on one level (x_is_zero: start from 0) */
+gmg_status gmg_level_smooth(gmg_hierarchy *h, int level, const double *g_dev, double *x_dev,
+                            int x_is_zero, void *cuda_stream);
+/* diagonal of A_l^S on S rows, 0 on E rows (level vector) */
+gmg_status gmg_level_diagonal(gmg_hierarchy *h, int level, double *diag_dev, void *cuda_stream);
+
+/* lambda_bar of D^{-1} A_l^S; set overrides it (parity decoupling). */
+gmg_status gmg_get_eigen(const gmg_hierarchy *h, int level, double *lambda_bar);
+gmg_status gmg_set_eigen(gmg_hierarchy *h, int level, double lambda_bar);
+
+/* Kernel launches issued by the library since creation (evidence counter). */
+gmg_status gmg_launch_count(const gmg_hierarchy *h, int64_t *count);
+/* Launches per V-cycle (graph nodes), per CG iteration. */
+gmg_status gmg_launch_profile(const gmg_hierarchy *h, int64_t *per_vcycle, int64_t *per_leaf_apply);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMG_H */

@@ -74,6 +74,42 @@ class Hierarchy:
         return len(self.levels) - 1
 
 
+@dataclass
+class Topology:
+    """Integer view (no matrices): level spaces, leaf space, lambda slots and
+    the global leaf numbering (owner = owner of the level-lambda(n) DoF,
+    DESIGN.md reading R25; sorted by (owner, Morton key))."""
+    lat: Lattice
+    cells: list
+    spaces: list
+    leaf: LeafSpace
+    leaf_owner: np.ndarray      # per free DoF (canonical free order)
+    leaf_global: np.ndarray     # permutation: global position -> canonical free index
+
+
+def topology(f: Forest, k: int, n_ranks: int = 1) -> Topology:
+    lat = Lattice(f, k)
+    owners = leaf_owners(f, n_ranks)
+    cells = level_cells(f, owners)
+    leafsets = leaf_level_sets(f, lat)
+    spaces = [level_space(f, lat, c, leafsets) for c in cells]
+    leaf = leaf_space(f, lat, owners, spaces, lambda xi: fem.lagrange(k, xi))
+    fX = leaf.X[leaf.free_index >= 0]
+    own = np.empty(leaf.n_free, dtype=np.int64)
+    for l, s in enumerate(spaces):
+        sel = np.nonzero(leaf.lam == l)[0]
+        if sel.size == 0:
+            continue
+        lk = lat.lin(s.X)
+        o = np.argsort(lk)
+        q = lat.lin(fX[sel])
+        p = o[np.searchsorted(lk[o], q)]
+        own[sel] = s.owner[p]
+    fkey = leaf.key[leaf.free_index >= 0]
+    glob = np.lexsort((fkey, own))
+    return Topology(lat, cells, spaces, leaf, own, glob)
+
+
 def build(f: Forest, k: int, n_ranks: int = 1, coef_level2: np.ndarray | None = None,
           degree: int = 4, eig=True, rhs="one") -> Hierarchy:
     lat = Lattice(f, k)
@@ -180,8 +216,9 @@ def eigen_estimate(lev: Level, iters: int = 10) -> float:
     nS = int(lev.S.sum())
     if nS == 0:
         return 0.0
-    A = lev.K
-    alphas, betas = cg_lanczos(A, lev.Dinv, eigen_rhs(lev), min(iters, nS))
+    S = lev.S
+    A_S = lev.K[S][:, S]                  # A_l^S, the matrix of the smoother (R9)
+    alphas, betas = cg_lanczos(A_S, lev.Dinv[S], eigen_rhs(lev)[S], min(iters, nS))
     if not alphas:
         return 0.0
     T = lanczos_tridiag(alphas, betas)

@@ -1,0 +1,391 @@
+"""Thin Python binding of libgmg (include/gmg.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA library ``libgmg.so`` built for
+sm_100a from ``csrc/``; there is no Python or CPU fallback.  Importing this
+package raises if the library has not been built (``__graft_entry__.build()``).
+PyTorch is used only for device memory and streams (tensors are passed by
+``data_ptr()``, the current torch stream is the launch stream).
+
+Function names follow the C ABI (``gmg_forest_generate``, ``gmg_partition``,
+``gmg_setup``, ``gmg_vcycle``, ``gmg_solve_cg`` ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgmg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libgmg.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = C.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ status
+GMG_OK = 0
+STATUS = {0: "GMG_OK", 1: "GMG_E_INVALID_ARG", 2: "GMG_E_UNSORTED", 3: "GMG_E_NOT_TILING",
+          4: "GMG_E_UNBALANCED", 5: "GMG_E_DEPTH", 6: "GMG_E_STATE", 7: "GMG_E_ZERO_DIAG",
+          8: "GMG_E_SINGULAR_COARSE", 9: "GMG_E_NOT_CONVERGED", 10: "GMG_E_CUDA", 11: "GMG_E_NCCL",
+          12: "GMG_E_OOM"}
+GMG_CLOSE_BALANCE = 1
+GMG_HOST_ONLY = 1
+GMG_NO_GRAPH = 2
+MAX_LEVELS = 64
+
+
+class GmgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _check(code):
+    if code != GMG_OK:
+        raise GmgError(code, _lib.gmg_last_error().decode())
+    return code
+
+
+# ------------------------------------------------------------------ structs
+class Recipe(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_trees", C.c_int), ("tree_xyz", C.c_int32 * 24),
+                ("global_refinements", C.c_int), ("rule", C.c_int), ("n_passes", C.c_int),
+                ("center_num", C.c_int64 * 3), ("center_den", C.c_int64 * 3),
+                ("radius_num", C.c_int64), ("radius_den", C.c_int64),
+                ("shell_num", C.c_int64), ("shell_den", C.c_int64),
+                ("corner", C.c_int64 * 3), ("s", C.c_int), ("lmax", C.c_int)]
+
+
+class Model(C.Structure):
+    _fields_ = [("n_levels", C.c_int), ("n_ranks", C.c_int), ("W_opt_num", C.c_int64), ("W_opt_den", C.c_int64),
+                ("W_sync", C.c_int64), ("W", C.c_int64), ("eta_num", C.c_int64), ("eta_den", C.c_int64),
+                ("N", C.c_int64 * MAX_LEVELS), ("W_l", C.c_int64 * MAX_LEVELS),
+                ("ghost_children", C.c_int64 * MAX_LEVELS), ("children", C.c_int64 * MAX_LEVELS)]
+
+
+class Params(C.Structure):
+    _fields_ = [("k", C.c_int), ("cheb_degree", C.c_int), ("cheb_lo", C.c_double), ("cheb_hi", C.c_double),
+                ("eig_iters", C.c_int), ("coef_level2", C.POINTER(C.c_double)), ("rank", C.c_int),
+                ("n_ranks", C.c_int), ("nccl_comm", C.c_void_p), ("device", C.c_int), ("flags", C.c_uint32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("dim", C.c_int), ("k", C.c_int), ("n_levels", C.c_int), ("n_ranks", C.c_int), ("rank", C.c_int),
+                ("n_leaf_nodes", C.c_int64), ("n_leaf_free", C.c_int64), ("n_leaf_hanging", C.c_int64),
+                ("n_leaf_dirichlet", C.c_int64), ("n_owned", C.c_int64), ("first_owned", C.c_int64),
+                ("level_dofs", C.c_int64 * MAX_LEVELS), ("level_cells", C.c_int64 * MAX_LEVELS),
+                ("level_families", C.c_int64 * MAX_LEVELS), ("level_S", C.c_int64 * MAX_LEVELS),
+                ("level_E", C.c_int64 * MAX_LEVELS), ("level_B", C.c_int64 * MAX_LEVELS),
+                ("level_leaf_cells", C.c_int64 * MAX_LEVELS), ("mg_vector_len", C.c_int64)]
+
+
+_vp = C.c_void_p
+_i64p = C.POINTER(C.c_int64)
+_SIGS = {
+    "gmg_last_error": ([], C.c_char_p),
+    "gmg_abi_version": ([], C.c_int),
+    "gmg_forest_create": ([C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "gmg_forest_generate": ([C.POINTER(Recipe), C.POINTER(_vp)], C.c_int),
+    "gmg_forest_destroy": ([_vp], C.c_int),
+    "gmg_forest_info": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int)], C.c_int),
+    "gmg_export_leaves": ([_vp, _vp, _vp, _vp], C.c_int),
+    "gmg_partition": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
+    "gmg_partition_destroy": ([_vp], C.c_int),
+    "gmg_partition_model": ([_vp, C.c_int64, C.POINTER(Model)], C.c_int),
+    "gmg_export_tallies": ([_vp, _vp], C.c_int),
+    "gmg_export_level_cells": ([_vp, C.c_int, _i64p, _vp, _vp, _vp], C.c_int),
+    "gmg_params_default": ([C.POINTER(Params)], None),
+    "gmg_setup": ([_vp, _vp, C.POINTER(Params), C.POINTER(_vp)], C.c_int),
+    "gmg_hierarchy_destroy": ([_vp], C.c_int),
+    "gmg_hierarchy_info": ([_vp, C.POINTER(Info)], C.c_int),
+    "gmg_export_level_dofs": ([_vp, C.c_int, _i64p, _vp, _vp, _vp, _vp], C.c_int),
+    "gmg_export_leaf_dofs": ([_vp, _i64p, _vp, _vp, _vp, _vp], C.c_int),
+    "gmg_export_cell_dofs": ([_vp, C.c_int, _i64p, _vp], C.c_int),
+    "gmg_vcycle": ([_vp, _vp, _vp, _vp], C.c_int),
+    "gmg_solve_cg": ([_vp, _vp, _vp, C.c_double, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), _vp],
+                     C.c_int),
+    "gmg_rhs_constant": ([_vp, C.c_double, _vp, _vp], C.c_int),
+    "gmg_level_apply": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_restrict": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_prolongate": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_leaf_apply": ([_vp, _vp, _vp, _vp], C.c_int),
+    "gmg_level_smooth": ([_vp, C.c_int, _vp, _vp, C.c_int, _vp], C.c_int),
+    "gmg_level_diagonal": ([_vp, C.c_int, _vp, _vp], C.c_int),
+    "gmg_get_eigen": ([_vp, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "gmg_set_eigen": ([_vp, C.c_int, C.c_double], C.c_int),
+    "gmg_launch_count": ([_vp, _i64p], C.c_int),
+    "gmg_launch_profile": ([_vp, _i64p, _i64p], C.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = sorted(_SIGS)
+
+
+def _ptr(a):
+    """data pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(_vp)
+    return _vp(a.data_ptr())
+
+
+def _stream(stream):
+    if stream is not None:
+        return _vp(stream)
+    import torch
+    return _vp(torch.cuda.current_stream().cuda_stream)
+
+
+# ------------------------------------------------------------------ recipes
+def recipe_from_config(cfg: dict, passes: int | None = -1) -> Recipe:
+    """gmg_recipe from a gmg_inputs config dict (parameters only)."""
+    r = Recipe()
+    r.dim = cfg["dim"]
+    r.n_trees = len(cfg["trees"])
+    for t, pos in enumerate(cfg["trees"]):
+        for j in range(cfg["dim"]):
+            r.tree_xyz[3 * t + j] = pos[j]
+    r.global_refinements = cfg["global_refinements"]
+    rules = {"center_ball": 1, "sphere_surface": 2, "corner_dist": 3}
+    r.rule = rules[cfg["rule"]]
+    npass = cfg["passes"] if passes == -1 else passes
+    r.n_passes = -1 if npass is None else int(npass)
+    for j in range(3):
+        r.center_den[j] = 1
+    if "center" in cfg:
+        for j, (n, d) in enumerate(cfg["center"]):
+            r.center_num[j], r.center_den[j] = n, d
+    if "radius" in cfg:
+        r.radius_num, r.radius_den = cfg["radius"]
+    else:
+        r.radius_num, r.radius_den = 0, 1
+    r.shell_num, r.shell_den = cfg.get("shell", (0, 1))
+    if "corner" in cfg:
+        for j, v in enumerate(cfg["corner"]):
+            r.corner[j] = v
+        r.s = cfg["s"]
+        r.lmax = cfg["lmax"]
+    return r
+
+
+# ------------------------------------------------------------------ handles
+class Forest:
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.gmg_forest_destroy(self.h)
+            self.h = None
+
+    def info(self):
+        d, t, n, L = C.c_int(), C.c_int(), C.c_int64(), C.c_int()
+        _check(_lib.gmg_forest_info(self.h, C.byref(d), C.byref(t), C.byref(n), C.byref(L)))
+        return dict(dim=d.value, n_trees=t.value, n_leaves=n.value, max_level=L.value)
+
+    def leaves(self):
+        n = self.info()["n_leaves"]
+        tree = np.empty(n, np.int32)
+        lev = np.empty(n, np.int8)
+        mor = np.empty(n, np.uint64)
+        _check(_lib.gmg_export_leaves(self.h, _ptr(tree), _ptr(lev), _ptr(mor)))
+        return tree, lev, mor
+
+
+def gmg_forest_generate(recipe: Recipe) -> Forest:
+    h = _vp()
+    _check(_lib.gmg_forest_generate(C.byref(recipe), C.byref(h)))
+    return Forest(h)
+
+
+def gmg_forest_create(dim, trees, leaf_tree, leaf_level, leaf_morton, flags=0) -> Forest:
+    t = np.ascontiguousarray(np.asarray(trees, dtype=np.int32).reshape(-1))
+    lt = np.ascontiguousarray(leaf_tree, dtype=np.int32)
+    ll = np.ascontiguousarray(leaf_level, dtype=np.int8)
+    lm = np.ascontiguousarray(leaf_morton, dtype=np.uint64)
+    h = _vp()
+    _check(_lib.gmg_forest_create(dim, t.size // dim, _ptr(t), lt.size, _ptr(lt), _ptr(ll), _ptr(lm), flags,
+                                  C.byref(h)))
+    return Forest(h)
+
+
+class Partitioning:
+    def __init__(self, handle, forest, n_ranks):
+        self.h = handle
+        self.forest = forest      # keep the forest alive
+        self.n_ranks = n_ranks
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.gmg_partition_destroy(self.h)
+            self.h = None
+
+    def model(self, W0_override=-1):
+        m = Model()
+        _check(_lib.gmg_partition_model(self.h, W0_override, C.byref(m)))
+        nl = m.n_levels
+        return dict(n_levels=nl, W_opt=(m.W_opt_num, m.W_opt_den), W_sync=m.W_sync, W=m.W,
+                    eta=(m.eta_num, m.eta_den), N=list(m.N[:nl]), W_l=list(m.W_l[:nl]),
+                    ghost_children=list(m.ghost_children[:nl]), children=list(m.children[:nl]))
+
+    def tallies(self):
+        nl = self.model()["n_levels"]
+        out = np.empty(nl * self.n_ranks, np.int64)
+        _check(_lib.gmg_export_tallies(self.h, _ptr(out)))
+        return out.reshape(nl, self.n_ranks)
+
+    def level_cells(self, level):
+        n = C.c_int64()
+        _check(_lib.gmg_export_level_cells(self.h, level, C.byref(n), None, None, None))
+        key = np.empty(n.value, np.uint64)
+        own = np.empty(n.value, np.int32)
+        leaf = np.empty(n.value, np.uint8)
+        _check(_lib.gmg_export_level_cells(self.h, level, C.byref(n), _ptr(key), _ptr(own), _ptr(leaf)))
+        return key, own, leaf
+
+
+def gmg_partition(forest: Forest, n_ranks: int) -> Partitioning:
+    h = _vp()
+    _check(_lib.gmg_partition(forest.h, n_ranks, C.byref(h)))
+    return Partitioning(h, forest, n_ranks)
+
+
+def gmg_params_default() -> Params:
+    p = Params()
+    _lib.gmg_params_default(C.byref(p))
+    return p
+
+
+class Hierarchy:
+    def __init__(self, handle, part, coef=None):
+        self.h = handle
+        self.part = part
+        self._coef = coef
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.gmg_hierarchy_destroy(self.h)
+            self.h = None
+
+    def info(self) -> dict:
+        i = Info()
+        _check(_lib.gmg_hierarchy_info(self.h, C.byref(i)))
+        nl = i.n_levels
+        out = {f: getattr(i, f) for f, _ in Info._fields_ if not f.startswith("level_")}
+        for f in ("level_dofs", "level_cells", "level_families", "level_S", "level_E", "level_B",
+                  "level_leaf_cells"):
+            out[f] = list(getattr(i, f)[:nl])
+        return out
+
+    # ---------- integer exports
+    def level_dofs(self, level):
+        n = C.c_int64()
+        _check(_lib.gmg_export_level_dofs(self.h, level, C.byref(n), None, None, None, None))
+        key = np.empty(n.value, np.uint64)
+        cls = np.empty(n.value, np.uint8)
+        own = np.empty(n.value, np.int32)
+        can = np.empty(n.value, np.int64)
+        _check(_lib.gmg_export_level_dofs(self.h, level, C.byref(n), _ptr(key), _ptr(cls), _ptr(own), _ptr(can)))
+        return key, cls, own, can
+
+    def leaf_dofs(self):
+        n = C.c_int64()
+        _check(_lib.gmg_export_leaf_dofs(self.h, C.byref(n), None, None, None, None))
+        key = np.empty(n.value, np.uint64)
+        lam = np.empty(n.value, np.int8)
+        own = np.empty(n.value, np.int32)
+        can = np.empty(n.value, np.int64)
+        _check(_lib.gmg_export_leaf_dofs(self.h, C.byref(n), _ptr(key), _ptr(lam), _ptr(own), _ptr(can)))
+        return key, lam, own, can
+
+    def cell_dofs(self, level):
+        n = C.c_int64()
+        _check(_lib.gmg_export_cell_dofs(self.h, level, C.byref(n), None))
+        info = self.info()
+        nn = (info["k"] + 1) ** info["dim"]
+        out = np.empty(n.value * nn, np.int64)
+        _check(_lib.gmg_export_cell_dofs(self.h, level, C.byref(n), _ptr(out)))
+        return out.reshape(n.value, nn)
+
+    # ---------- hot path (device tensors)
+    def vcycle(self, b, x, stream=None):
+        _check(_lib.gmg_vcycle(self.h, _ptr(b), _ptr(x), _stream(stream)))
+
+    def solve_cg(self, b, x, rtol=1e-8, max_it=200, stream=None, raise_on_fail=True):
+        it = C.c_int()
+        rel = C.c_double()
+        code = _lib.gmg_solve_cg(self.h, _ptr(b), _ptr(x), rtol, max_it, C.byref(it), C.byref(rel),
+                                 _stream(stream))
+        if code != GMG_OK and (raise_on_fail or code != 9):
+            _check(code)
+        return it.value, rel.value, code
+
+    def rhs_constant(self, f, b, stream=None):
+        _check(_lib.gmg_rhs_constant(self.h, f, _ptr(b), _stream(stream)))
+
+    def level_apply(self, level, x, y, stream=None):
+        _check(_lib.gmg_level_apply(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
+
+    def restrict(self, level, r, dc, stream=None):
+        _check(_lib.gmg_restrict(self.h, level, _ptr(r), _ptr(dc), _stream(stream)))
+
+    def prolongate(self, level, xc, xf, stream=None):
+        _check(_lib.gmg_prolongate(self.h, level, _ptr(xc), _ptr(xf), _stream(stream)))
+
+    def leaf_apply(self, u, v, stream=None):
+        _check(_lib.gmg_leaf_apply(self.h, _ptr(u), _ptr(v), _stream(stream)))
+
+    def level_smooth(self, level, g, x, x_is_zero, stream=None):
+        _check(_lib.gmg_level_smooth(self.h, level, _ptr(g), _ptr(x), int(bool(x_is_zero)), _stream(stream)))
+
+    def level_diagonal(self, level, diag, stream=None):
+        _check(_lib.gmg_level_diagonal(self.h, level, _ptr(diag), _stream(stream)))
+
+    def get_eigen(self, level):
+        v = C.c_double()
+        _check(_lib.gmg_get_eigen(self.h, level, C.byref(v)))
+        return v.value
+
+    def set_eigen(self, level, lam):
+        _check(_lib.gmg_set_eigen(self.h, level, float(lam)))
+
+    def launch_count(self):
+        v = C.c_int64()
+        _check(_lib.gmg_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def launch_profile(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.gmg_launch_profile(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
+              coef_level2=None, graph=True, device=-1) -> Hierarchy:
+    p = gmg_params_default()
+    p.k = k
+    p.cheb_degree = cheb_degree
+    p.rank = rank
+    p.n_ranks = part.n_ranks
+    p.device = device
+    p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH)
+    coef = None
+    if coef_level2 is not None:
+        coef = np.ascontiguousarray(coef_level2, dtype=np.float64)
+        p.coef_level2 = coef.ctypes.data_as(C.POINTER(C.c_double))
+    h = _vp()
+    _check(_lib.gmg_setup(forest.h, part.h, C.byref(p), C.byref(h)))
+    return Hierarchy(h, part, coef)
+
+
+def build_config(cfg: dict, n_ranks=1, host_only=False, passes=-1, **kw):
+    """Forest -> partition -> hierarchy for a gmg_inputs config dict."""
+    f = gmg_forest_generate(recipe_from_config(cfg, passes))
+    part = gmg_partition(f, n_ranks)
+    h = gmg_setup(f, part, k=cfg["k"], host_only=host_only, **kw)
+    return f, part, h

@@ -1,0 +1,437 @@
+// C ABI of libgmg (include/gmg.h): argument checks, handle management and the
+// translation of internal errors into gmg_status codes.
+#include <cmath>
+#include <memory>
+#include <new>
+
+#include "device.hpp"
+#include "forest.hpp"
+
+struct gmg_forest {
+  gmg::Forest f;
+};
+struct gmg_partitioning {
+  const gmg_forest* forest;
+  gmg::Partition p;
+};
+struct gmg_hierarchy {
+  gmg::Topology topo;
+  gmg_params prm{};
+  gmg::DeviceHierarchy* dev = nullptr;
+  std::vector<gmg::i64> level_cells, level_fams;
+  ~gmg_hierarchy() { gmg::device_destroy(dev); }
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+gmg_status guard(F&& fn) {
+  try {
+    fn();
+    return GMG_OK;
+  } catch (const gmg::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return GMG_E_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GMG_E_STATE;
+  } catch (...) {
+    g_err = "unknown error";
+    return GMG_E_STATE;
+  }
+}
+
+#define NEED(p) GMG_REQUIRE((p) != nullptr, GMG_E_INVALID_ARG, #p " is NULL")
+
+gmg::DeviceHierarchy* need_dev(gmg_hierarchy* h) {
+  GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "hierarchy has no device data (GMG_HOST_ONLY)");
+  GMG_REQUIRE(h->prm.n_ranks == 1, GMG_E_STATE, "n_ranks > 1 is not supported by this build");
+  return h->dev;
+}
+void need_level(const gmg_hierarchy* h, int level) {
+  GMG_REQUIRE(level >= 0 && level <= h->topo.L, GMG_E_INVALID_ARG, "level out of range");
+}
+}  // namespace
+
+extern "C" {
+
+const char* gmg_last_error(void) { return g_err.c_str(); }
+int gmg_abi_version(void) { return 1; }
+
+gmg_status gmg_forest_create(int dim, int n_trees, const int32_t* tree_xyz, int64_t n_leaves,
+                             const int32_t* leaf_tree, const int8_t* leaf_level, const uint64_t* leaf_morton,
+                             uint32_t flags, gmg_forest** out) {
+  return guard([&] {
+    NEED(out);
+    auto f = std::make_unique<gmg_forest>();
+    f->f = gmg::forest_create(dim, n_trees, tree_xyz, n_leaves, leaf_tree, leaf_level, leaf_morton, flags);
+    *out = f.release();
+  });
+}
+
+gmg_status gmg_forest_generate(const gmg_recipe* r, gmg_forest** out) {
+  return guard([&] {
+    NEED(r);
+    NEED(out);
+    auto f = std::make_unique<gmg_forest>();
+    f->f = gmg::forest_generate(*r);
+    *out = f.release();
+  });
+}
+
+gmg_status gmg_forest_destroy(gmg_forest* f) {
+  delete f;
+  return GMG_OK;
+}
+
+gmg_status gmg_forest_info(const gmg_forest* f, int* dim, int* n_trees, int64_t* n_leaves, int* max_level) {
+  return guard([&] {
+    NEED(f);
+    if (dim) *dim = f->f.dim;
+    if (n_trees) *n_trees = (int)f->f.trees.size();
+    if (n_leaves) *n_leaves = f->f.n_leaves();
+    if (max_level) *max_level = f->f.L;
+  });
+}
+
+gmg_status gmg_export_leaves(const gmg_forest* fh, int32_t* leaf_tree, int8_t* leaf_level, uint64_t* leaf_morton) {
+  return guard([&] {
+    NEED(fh);
+    const gmg::Forest& f = fh->f;
+    for (gmg::i64 i = 0; i < f.n_leaves(); ++i) {
+      int l = f.level[i];
+      gmg::Vec3 tp{f.gc[i][0] >> l, f.gc[i][1] >> l, f.gc[i][2] >> l};
+      int t = f.tree_of(tp);
+      gmg::Vec3 loc{f.gc[i][0] - (tp[0] << l), f.gc[i][1] - (tp[1] << l), f.gc[i][2] - (tp[2] << l)};
+      if (leaf_tree) leaf_tree[i] = t;
+      if (leaf_level) leaf_level[i] = (int8_t)l;
+      if (leaf_morton) leaf_morton[i] = gmg::morton(f.dim, loc);
+    }
+  });
+}
+
+gmg_status gmg_partition(const gmg_forest* f, int n_ranks, gmg_partitioning** out) {
+  return guard([&] {
+    NEED(f);
+    NEED(out);
+    auto p = std::make_unique<gmg_partitioning>();
+    p->forest = f;
+    p->p = gmg::make_partition(f->f, n_ranks);
+    *out = p.release();
+  });
+}
+
+gmg_status gmg_partition_destroy(gmg_partitioning* p) {
+  delete p;
+  return GMG_OK;
+}
+
+gmg_status gmg_partition_model(const gmg_partitioning* p, int64_t W0_override, gmg_model* out) {
+  return guard([&] {
+    NEED(p);
+    NEED(out);
+    *out = gmg::partition_model(p->p, W0_override);
+  });
+}
+
+gmg_status gmg_export_tallies(const gmg_partitioning* p, int64_t* N_lp) {
+  return guard([&] {
+    NEED(p);
+    NEED(N_lp);
+    const int P = p->p.n_ranks;
+    for (size_t l = 0; l < p->p.levels.size(); ++l) {
+      for (int r = 0; r < P; ++r) N_lp[l * P + r] = 0;
+      for (auto o : p->p.levels[l].owner) N_lp[l * P + o]++;
+    }
+  });
+}
+
+gmg_status gmg_export_level_cells(const gmg_partitioning* p, int level, int64_t* n, uint64_t* key, int32_t* owner,
+                                  uint8_t* is_leaf) {
+  return guard([&] {
+    NEED(p);
+    NEED(n);
+    GMG_REQUIRE(level >= 0 && level < (int)p->p.levels.size(), GMG_E_INVALID_ARG, "level out of range");
+    const auto& lc = p->p.levels[level];
+    *n = (int64_t)lc.key.size();
+    for (size_t c = 0; c < lc.key.size(); ++c) {
+      if (key) key[c] = lc.key[c];
+      if (owner) owner[c] = lc.owner[c];
+      if (is_leaf) is_leaf[c] = lc.leaf[c];
+    }
+  });
+}
+
+void gmg_params_default(gmg_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof *p);
+  p->k = 2;
+  p->cheb_degree = 4;
+  p->cheb_lo = 0.08;
+  p->cheb_hi = 1.2;
+  p->eig_iters = 10;
+  p->coef_level2 = nullptr;
+  p->rank = 0;
+  p->n_ranks = 1;
+  p->nccl_comm = nullptr;
+  p->device = -1;
+  p->flags = 0;
+}
+
+gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_params* prm, gmg_hierarchy** out) {
+  return guard([&] {
+    NEED(f);
+    NEED(p);
+    NEED(prm);
+    NEED(out);
+    GMG_REQUIRE(p->forest == f, GMG_E_INVALID_ARG, "partition was not built from this forest");
+    GMG_REQUIRE(prm->n_ranks == p->p.n_ranks, GMG_E_INVALID_ARG, "params.n_ranks != partition n_ranks");
+    GMG_REQUIRE(prm->rank >= 0 && prm->rank < prm->n_ranks, GMG_E_INVALID_ARG, "rank out of range");
+    GMG_REQUIRE(prm->cheb_degree >= 1 && prm->cheb_degree <= 16, GMG_E_INVALID_ARG, "cheb_degree");
+    GMG_REQUIRE(prm->cheb_lo > 0 && prm->cheb_hi > prm->cheb_lo, GMG_E_INVALID_ARG, "cheb range");
+    GMG_REQUIRE(prm->eig_iters >= 1, GMG_E_INVALID_ARG, "eig_iters");
+    auto h = std::make_unique<gmg_hierarchy>();
+    h->prm = *prm;
+    h->topo = gmg::make_topology(f->f, p->p, prm->k);
+    if (!(prm->flags & GMG_HOST_ONLY)) {
+      GMG_REQUIRE(prm->n_ranks == 1, GMG_E_STATE, "n_ranks > 1 is not supported by this build");
+      std::vector<double> cflat;
+      std::vector<gmg::i64> coff;
+      if (prm->coef_level2) {
+        GMG_REQUIRE(f->f.L >= 2, GMG_E_INVALID_ARG, "coefficient per level-2 cell needs >= 3 levels");
+        gmg::fail(GMG_E_INVALID_ARG, "variable coefficient (config 4) is not supported by this build yet");
+      }
+      h->dev = gmg::device_create(h->topo, *prm, cflat, coff);
+    }
+    *out = h.release();
+  });
+}
+
+gmg_status gmg_hierarchy_destroy(gmg_hierarchy* h) {
+  return guard([&] { delete h; });
+}
+
+gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
+  return guard([&] {
+    NEED(h);
+    NEED(o);
+    std::memset(o, 0, sizeof *o);
+    const auto& T = h->topo;
+    o->dim = T.dim;
+    o->k = T.k;
+    o->n_levels = T.L + 1;
+    o->n_ranks = T.n_ranks;
+    o->rank = h->prm.rank;
+    o->n_leaf_nodes = T.n_leaf_nodes;
+    o->n_leaf_free = T.n_leaf;
+    o->n_leaf_hanging = T.n_hanging;
+    o->n_leaf_dirichlet = T.n_dirichlet;
+    gmg::i64 first = -1, cnt = 0;
+    for (gmg::i64 g = 0; g < T.n_leaf; ++g)
+      if (T.leaf_owner[g] == h->prm.rank) {
+        if (first < 0) first = g;
+        ++cnt;
+      }
+    o->n_owned = cnt;
+    o->first_owned = first < 0 ? 0 : first;
+    gmg::i64 mg = 0;
+    for (int l = 0; l <= T.L && l < GMG_MAX_LEVELS; ++l) {
+      const auto& t = T.lv[l];
+      o->level_dofs[l] = t.n_dofs;
+      o->level_cells[l] = t.n_cells;
+      o->level_families[l] = t.n_fam;
+      o->level_S[l] = t.nS;
+      o->level_E[l] = t.nE;
+      o->level_B[l] = t.nB;
+      o->level_leaf_cells[l] = (gmg::i64)t.leaf_cells.size();
+      mg += (t.n_dofs + 31) / 32 * 32;
+    }
+    o->mg_vector_len = mg;
+  });
+}
+
+gmg_status gmg_export_level_dofs(const gmg_hierarchy* h, int level, int64_t* n, uint64_t* key, uint8_t* cls,
+                                 int32_t* owner, int64_t* canonical) {
+  return guard([&] {
+    NEED(h);
+    NEED(n);
+    need_level(h, level);
+    const auto& t = h->topo.lv[level];
+    *n = t.n_dofs;
+    for (gmg::i64 i = 0; i < t.n_dofs; ++i) {
+      if (key) key[i] = t.dof_key[i];
+      if (cls) cls[i] = t.dof_cls[i];
+      if (owner) owner[i] = t.dof_owner[i];
+      if (canonical) canonical[i] = t.dof_canon[i];
+    }
+  });
+}
+
+gmg_status gmg_export_leaf_dofs(const gmg_hierarchy* h, int64_t* n, uint64_t* key, int8_t* lambda, int32_t* owner,
+                                int64_t* canonical) {
+  return guard([&] {
+    NEED(h);
+    NEED(n);
+    const auto& T = h->topo;
+    *n = T.n_leaf;
+    for (gmg::i64 i = 0; i < T.n_leaf; ++i) {
+      if (key) key[i] = T.leaf_key[i];
+      if (lambda) lambda[i] = T.leaf_lambda[i];
+      if (owner) owner[i] = T.leaf_owner[i];
+      if (canonical) canonical[i] = T.leaf_canon[i];
+    }
+  });
+}
+
+gmg_status gmg_export_cell_dofs(const gmg_hierarchy* h, int level, int64_t* n_cells, int64_t* dofs) {
+  return guard([&] {
+    NEED(h);
+    NEED(n_cells);
+    need_level(h, level);
+    const auto& t = h->topo.lv[level];
+    *n_cells = t.n_cells;
+    if (dofs)
+      for (size_t i = 0; i < t.cell_dofs.size(); ++i) dofs[i] = t.cell_dofs[i];
+  });
+}
+
+gmg_status gmg_vcycle(gmg_hierarchy* h, const double* b, double* x, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(b);
+    NEED(x);
+    GMG_REQUIRE(b != x, GMG_E_INVALID_ARG, "b and x must not alias");
+    gmg::device_vcycle(need_dev(h), b, x, s);
+  });
+}
+
+gmg_status gmg_solve_cg(gmg_hierarchy* h, const double* b, double* x, double rtol, int max_it, int* iters,
+                        double* rel_res, void* s) {
+  gmg_status st = GMG_OK;
+  gmg_status g = guard([&] {
+    NEED(h);
+    NEED(b);
+    NEED(x);
+    GMG_REQUIRE(rtol >= 0 && max_it >= 1, GMG_E_INVALID_ARG, "rtol >= 0 and max_it >= 1 required");
+    int rc = gmg::device_solve_cg(need_dev(h), b, x, rtol, max_it, iters, rel_res, s);
+    if (rc) {
+      g_err = "CG did not converge within max_it";
+      st = GMG_E_NOT_CONVERGED;
+    }
+  });
+  return g != GMG_OK ? g : st;
+}
+
+gmg_status gmg_rhs_constant(gmg_hierarchy* h, double f, double* b, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(b);
+    gmg::device_rhs_constant(need_dev(h), f, b, s);
+  });
+}
+
+gmg_status gmg_level_apply(gmg_hierarchy* h, int level, const double* x, double* y, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(x);
+    NEED(y);
+    need_level(h, level);
+    gmg::device_level_apply(need_dev(h), level, x, y, s);
+  });
+}
+
+gmg_status gmg_restrict(gmg_hierarchy* h, int level, const double* r, double* dc, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(r);
+    NEED(dc);
+    need_level(h, level);
+    GMG_REQUIRE(level >= 1, GMG_E_INVALID_ARG, "restriction needs level >= 1");
+    gmg::device_restrict(need_dev(h), level, r, dc, s);
+  });
+}
+
+gmg_status gmg_prolongate(gmg_hierarchy* h, int level, const double* xc, double* xf, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(xc);
+    NEED(xf);
+    need_level(h, level);
+    GMG_REQUIRE(level >= 1, GMG_E_INVALID_ARG, "prolongation needs level >= 1");
+    gmg::device_prolongate(need_dev(h), level, xc, xf, s);
+  });
+}
+
+gmg_status gmg_leaf_apply(gmg_hierarchy* h, const double* u, double* v, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(u);
+    NEED(v);
+    gmg::device_leaf_apply(need_dev(h), u, v, s);
+  });
+}
+
+gmg_status gmg_level_smooth(gmg_hierarchy* h, int level, const double* g, double* x, int x_is_zero, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(g);
+    NEED(x);
+    need_level(h, level);
+    gmg::device_level_smooth(need_dev(h), level, g, x, x_is_zero, s);
+  });
+}
+
+gmg_status gmg_level_diagonal(gmg_hierarchy* h, int level, double* diag, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(diag);
+    need_level(h, level);
+    gmg::device_level_diagonal(need_dev(h), level, diag, s);
+  });
+}
+
+gmg_status gmg_get_eigen(const gmg_hierarchy* h, int level, double* lam) {
+  return guard([&] {
+    NEED(h);
+    NEED(lam);
+    need_level(h, level);
+    GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "no device data");
+    *lam = gmg::device_get_eigen(h->dev, level);
+  });
+}
+
+gmg_status gmg_set_eigen(gmg_hierarchy* h, int level, double lam) {
+  return guard([&] {
+    NEED(h);
+    need_level(h, level);
+    GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "no device data");
+    GMG_REQUIRE(level >= 1 && lam > 0 && std::isfinite(lam), GMG_E_INVALID_ARG, "lambda must be > 0 on level >= 1");
+    gmg::device_set_eigen(h->dev, level, lam);
+  });
+}
+
+gmg_status gmg_launch_count(const gmg_hierarchy* h, int64_t* count) {
+  return guard([&] {
+    NEED(h);
+    NEED(count);
+    *count = h->dev ? gmg::device_launches(h->dev) : 0;
+  });
+}
+
+gmg_status gmg_launch_profile(const gmg_hierarchy* h, int64_t* pv, int64_t* pl) {
+  return guard([&] {
+    NEED(h);
+    NEED(pv);
+    NEED(pl);
+    long long a = 0, b = 0;
+    if (h->dev) gmg::device_launch_profile(h->dev, &a, &b);
+    *pv = a;
+    *pl = b;
+  });
+}
+
+}  // extern "C"

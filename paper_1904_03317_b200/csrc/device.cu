@@ -1,0 +1,682 @@
+// Device hierarchy and hot-path driver: V-cycle (local smoothing
+// P:413-469), Chebyshev-Jacobi smoother, leaf operator with hanging
+// nodes, GMG-preconditioned CG, eigenvalue estimate and coarse
+// solve (setup).  One process per GPU; this version runs p = 1.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "device.hpp"
+#include "kernels.cuh"
+
+namespace gmg {
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) fail(GMG_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+struct DevLevel {
+  i64 n = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
+  int* cell_dofs = nullptr;
+  long ldc = 0;
+  double* coef = nullptr;
+  unsigned char* cls = nullptr;     // bit0 = E
+  double* Dinv = nullptr;
+  int* fam_parent = nullptr;
+  unsigned long long* fam_mask = nullptr;
+  int mask_words = 0;
+  int* leaf_cells = nullptr;
+  int* edge_fams = nullptr;
+  double h = 1, scale = 1;          // scale = h^(d-2)
+  double lam = 0;
+  std::vector<double> c1, c2;
+};
+
+struct DeviceHierarchy {
+  int dim = 2, k = 2, L = 0, m = 4;
+  double lo = 0.08, hi = 1.2;
+  int eig_iters = 10;
+  std::vector<DevLevel> lv;
+  i64 N = 0, n_leaf = 0;
+  double *D = nullptr, *X = nullptr, *T = nullptr, *DV = nullptr, *W = nullptr, *Y = nullptr;
+  double *cx = nullptr, *cr = nullptr, *cp = nullptr, *cq = nullptr, *cz = nullptr;
+  unsigned char* lam_mg = nullptr;
+  long long* mg_to_leaf = nullptr;
+  long long* leaf_to_mg = nullptr;
+  double* partial = nullptr;
+  int nred = 0;
+  double* scal = nullptr;       // device scalars
+  double* hscal = nullptr;      // pinned host mirror
+  int nS0 = 0;
+  int* coarse_idx = nullptr;
+  double* coarse_inv = nullptr;
+  bool use_graph = true;
+  cudaGraphExec_t vgraph = nullptr;
+  cudaStream_t cap = nullptr;
+  long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
+  std::vector<void*> allocs;
+  int sms = 148;
+
+  template <class T_>
+  T_* alloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T_));
+    if (e != cudaSuccess) fail(GMG_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    allocs.push_back(p);
+    return (T_*)p;
+  }
+  template <class T_>
+  T_* upload(const std::vector<T_>& v) {
+    T_* p = alloc<T_>(v.size());
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T_), cudaMemcpyHostToDevice));
+    return p;
+  }
+  int vgrid(i64 n, int nt = 256) const {
+    i64 b = (n + nt - 1) / nt;
+    i64 cap_ = (i64)sms * 16;
+    if (b > cap_) b = cap_;
+    return (int)(b < 1 ? 1 : b);
+  }
+};
+
+#define DISPATCH_DK(dim, k, ...)                                   \
+  do {                                                             \
+    if ((dim) == 2 && (k) == 1) { constexpr int D_ = 2, K_ = 1; __VA_ARGS__; } \
+    else if ((dim) == 2 && (k) == 2) { constexpr int D_ = 2, K_ = 2; __VA_ARGS__; } \
+    else if ((dim) == 3 && (k) == 1) { constexpr int D_ = 3, K_ = 1; __VA_ARGS__; } \
+    else { constexpr int D_ = 3, K_ = 2; __VA_ARGS__; }             \
+  } while (0)
+
+// ---------------------------------------------------------------- primitives
+static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
+  if (n == 0) return;
+  DevLevel& v = d->lv[l];
+  const int nt = 128;
+  int grid = (int)((n + nt - 1) / nt);
+  DISPATCH_DK(d->dim, d->k, (dev::cell_apply<D_, K_><<<grid, nt, 0, s>>>((int)n, list, v.cell_dofs, v.ldc, v.coef,
+                                                                            v.scale, x, y)));
+  d->launches++;
+}
+
+template <int MODE>
+static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const double* vin, double* t, double* dc,
+                       cudaStream_t s) {
+  if (nf == 0) return;
+  DevLevel& f = d->lv[l];
+  DevLevel& c = d->lv[l - 1];
+  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  DISPATCH_DK(d->dim, d->k,
+              (dev::fam_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                  (int)nf, list, f.fam_parent, f.fam_mask, f.mask_words, c.cell_dofs, c.ldc, f.cell_dofs, f.ldc, f.cls,
+                  vin, t, dc)));
+  d->launches++;
+}
+
+template <int MODE>
+static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, const double* xc, double* xf,
+                         cudaStream_t s) {
+  if (nf == 0) return;
+  DevLevel& f = d->lv[l];
+  DevLevel& c = d->lv[l - 1];
+  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  DISPATCH_DK(d->dim, d->k,
+              (dev::fam_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                  (int)nf, list, f.fam_parent, f.fam_mask, f.mask_words, c.cell_dofs, c.ldc, f.cell_dofs, f.ldc, f.cls,
+                  xc, xf)));
+  d->launches++;
+}
+
+// Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
+// first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
+// x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows keeps x^E fixed).
+static void smooth(DeviceHierarchy* d, int l, const double* g, double* x, double* t, double* dv, bool x_zero,
+                   cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  const i64 n = v.n;
+  if (n == 0) return;
+  const int m = d->m;
+  const int gr = d->vgrid(n);
+  if (x_zero) {
+    dev::cheb_step<false, false, true, true><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
+  } else {
+    k_apply(d, l, nullptr, v.n_cells, x, t, s);
+    if (m == 1)
+      dev::cheb_step<true, false, false, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
+    else
+      dev::cheb_step<true, false, true, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
+  }
+  d->launches++;
+  for (int j = 1; j < m; ++j) {
+    k_apply(d, l, nullptr, v.n_cells, x, t, s);
+    if (j == m - 1)
+      dev::cheb_step<true, true, false, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, v.c1[j], v.c2[j]);
+    else
+      dev::cheb_step<true, true, true, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, v.c1[j], v.c2[j]);
+    d->launches++;
+  }
+}
+
+static void coarse(DeviceHierarchy* d, const double* d0, double* x0, cudaStream_t s) {
+  if (d->nS0 == 0) return;
+  dev::coarse_solve<<<1, 256, 0, s>>>(d->nS0, d->coarse_idx, d->coarse_inv, d0, x0);
+  d->launches++;
+}
+
+// The V-cycle on the MG-layout buffers D (defects, copy_to_mg done), X (out).
+static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
+  const int L = d->L;
+  for (int l = L; l >= 1; --l) {
+    DevLevel& v = d->lv[l];
+    double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
+    smooth(d, l, g, x, t, dv, true, s);                                     // 1: pre-smooth from 0
+    k_apply(d, l, nullptr, v.n_cells, x, t, s);                             // 2: t = K x
+    k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, d->D + d->lv[l - 1].off, s);  // 3: d_{l-1} += P^T (d - t)
+  }
+  coarse(d, d->D + d->lv[0].off, d->X + d->lv[0].off, s);                   // 4: coarse solve
+  for (int l = 1; l <= L; ++l) {
+    DevLevel& v = d->lv[l];
+    double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
+    k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, d->X + d->lv[l - 1].off, x, s);  // 5
+    smooth(d, l, g, x, t, dv, false, s);                                    // 6: post-smooth
+  }
+}
+
+static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s) {
+  if (!d->use_graph) {
+    vcycle_levels(d, s);
+    return;
+  }
+  if (!d->vgraph) {
+    long long before = d->launches;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal));
+    vcycle_levels(d, d->cap);
+    CK(cudaStreamEndCapture(d->cap, &g));
+    CK(cudaGraphInstantiate(&d->vgraph, g, 0));
+    CK(cudaGraphDestroy(g));
+    d->per_vcycle = d->launches - before;
+    d->launches = before;
+  }
+  CK(cudaGraphLaunch(d->vgraph, s));
+  d->launches += d->per_vcycle;
+}
+
+// leaf operator in MG layout: q = lam * Y, Y = A_leaf p (hanging nodes via E rows)
+static void leaf_apply_mg(DeviceHierarchy* d, const double* p, double* q, double* partial, cudaStream_t s) {
+  const int L = d->L;
+  long long before = d->launches;
+  CK(cudaMemcpyAsync(d->W, p, d->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (int l = 1; l <= L; ++l)
+    k_prolongate<dev::XFER_SET_E>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->W + d->lv[l - 1].off,
+                                  d->W + d->lv[l].off, s);
+  CK(cudaMemsetAsync(d->Y, 0, d->N * sizeof(double), s));
+  for (int l = 0; l <= L; ++l)
+    k_apply(d, l, d->lv[l].leaf_cells, d->lv[l].n_leaf, d->W + d->lv[l].off, d->Y + d->lv[l].off, s);
+  for (int l = L; l >= 1; --l)
+    k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
+                               d->Y + d->lv[l - 1].off, s);
+  dev::mask_dot<<<d->nred, dev::RED_NT, 0, s>>>(d->N, d->lam_mg, d->Y, p, q, partial);
+  d->launches++;
+  d->per_leaf_apply = d->launches - before;
+}
+
+static double host_dot(DeviceHierarchy* d, i64 n, const double* a, const double* b, cudaStream_t s) {
+  dev::dot_partial<<<d->nred, dev::RED_NT, 0, s>>>(n, a, b, d->partial);
+  dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 7);
+  d->launches += 2;
+  CK(cudaMemcpyAsync(d->hscal + 7, d->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return d->hscal[7];
+}
+
+static void set_cheb(DeviceHierarchy* d, int l) {
+  DevLevel& v = d->lv[l];
+  v.c1.assign(d->m, 0.0);
+  v.c2.assign(d->m, 0.0);
+  if (!(v.lam > 0)) return;
+  const double hi = d->hi * v.lam, lo = d->lo * v.lam;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  v.c1[0] = 0.0;
+  v.c2[0] = 1.0 / theta;
+  for (int j = 1; j < d->m; ++j) {
+    double rn = 1.0 / (2.0 * sigma - rho);
+    v.c1[j] = rn * rho;
+    v.c2[j] = 2.0 * rn / delta;
+    rho = rn;
+  }
+}
+
+// largest eigenvalue of a symmetric tridiagonal matrix (cyclic Jacobi on the
+// dense matrix, m <= ~20)
+static double tridiag_max_eig(const std::vector<double>& a, const std::vector<double>& b) {
+  const int m = (int)a.size();
+  std::vector<double> A((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i) A[(size_t)i * m + i] = a[i];
+  for (int i = 1; i < m; ++i) A[(size_t)i * m + i - 1] = A[(size_t)(i - 1) * m + i] = b[i - 1];
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0;
+    for (int i = 0; i < m; ++i)
+      for (int j = i + 1; j < m; ++j) off += A[(size_t)i * m + j] * A[(size_t)i * m + j];
+    if (off < 1e-300) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        double apq = A[(size_t)p * m + q];
+        if (apq == 0.0) continue;
+        double app = A[(size_t)p * m + p], aqq = A[(size_t)q * m + q];
+        double th = (aqq - app) / (2.0 * apq);
+        double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int r = 0; r < m; ++r) {
+          double arp = A[(size_t)r * m + p], arq = A[(size_t)r * m + q];
+          A[(size_t)r * m + p] = c * arp - s * arq;
+          A[(size_t)r * m + q] = s * arp + c * arq;
+        }
+        for (int r = 0; r < m; ++r) {
+          double apr = A[(size_t)p * m + r], aqr = A[(size_t)q * m + r];
+          A[(size_t)p * m + r] = c * apr - s * aqr;
+          A[(size_t)q * m + r] = s * apr + c * aqr;
+        }
+      }
+  }
+  double mx = -1e300;
+  for (int i = 0; i < m; ++i) mx = std::max(mx, A[(size_t)i * m + i]);
+  return mx;
+}
+
+// CG (Jacobi preconditioned) on A^S x = v, v = (-5.5, ..., 5.5, -5.5, ...)
+// over the S DoFs in canonical order, min(eig_iters, n_S) iterations, Lanczos
+// tridiagonal from the CG coefficients, lambda = its largest eigenvalue.
+static double eigen_estimate(DeviceHierarchy* d, int l, const std::vector<double>& v_host, i64 nS,
+                             cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  const i64 n = v.n;
+  if (nS == 0 || n == 0) return 0.0;
+  double *r = d->X + v.off, *z = d->DV + v.off, *p = d->W + v.off, *q = d->Y + v.off;
+  CK(cudaMemcpyAsync(r, v_host.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  const int gr = (int)((n + 255) / 256);
+  dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
+  CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  d->launches++;
+  double rz = host_dot(d, n, r, z, s);
+  double r0 = std::sqrt(host_dot(d, n, r, r, s));
+  std::vector<double> alphas, betas;
+  if (rz == 0.0 || r0 == 0.0) return 0.0;
+  const int maxit = (int)std::min<i64>(d->eig_iters, nS);
+  for (int it = 0; it < maxit; ++it) {
+    CK(cudaMemsetAsync(q, 0, n * sizeof(double), s));
+    k_apply(d, l, nullptr, v.n_cells, p, q, s);
+    double pq = host_dot(d, n, p, q, s);
+    double alpha = rz / pq;
+    alphas.push_back(alpha);
+    dev::eig_update_r<<<gr, 256, 0, s>>>(n, alpha, v.cls, q, r);
+    d->launches++;
+    if (it == maxit - 1) break;
+    dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
+    d->launches++;
+    double rz_new = host_dot(d, n, r, z, s);
+    double rn = std::sqrt(host_dot(d, n, r, r, s));
+    if (rn <= 1e-10 * r0 || rz_new == 0.0) break;
+    double beta = rz_new / rz;
+    betas.push_back(beta);
+    dev::axpby<<<gr, 256, 0, s>>>(n, 1.0, z, beta, p);
+    d->launches++;
+    rz = rz_new;
+  }
+  const int m = (int)alphas.size();
+  std::vector<double> a(m), b(m > 0 ? m - 1 : 0);
+  for (int j = 0; j < m; ++j) {
+    a[j] = 1.0 / alphas[j] + (j > 0 ? betas[j - 1] / alphas[j - 1] : 0.0);
+    if (j > 0) b[j - 1] = std::sqrt(betas[j - 1]) / alphas[j - 1];
+  }
+  return tridiag_max_eig(a, b);
+}
+
+// ---------------------------------------------------------------- creation
+DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const std::vector<double>& coef_flat,
+                               const std::vector<i64>& coef_off) {
+  auto* d = new DeviceHierarchy();
+  try {
+    if (prm.device >= 0) CK(cudaSetDevice(prm.device));
+    int dev_id = 0;
+    CK(cudaGetDevice(&dev_id));
+    CK(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, dev_id));
+    d->dim = Tp.dim;
+    d->k = Tp.k;
+    d->L = Tp.L;
+    d->m = prm.cheb_degree;
+    d->lo = prm.cheb_lo;
+    d->hi = prm.cheb_hi;
+    d->eig_iters = prm.eig_iters;
+    d->use_graph = !(prm.flags & GMG_NO_GRAPH);
+    GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
+    CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
+    const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
+    d->lv.resize(Tp.L + 1);
+    i64 off = 0;
+    for (int l = 0; l <= Tp.L; ++l) {
+      const LevelTopo& t = Tp.lv[l];
+      DevLevel& v = d->lv[l];
+      v.n = t.n_dofs;
+      v.n_cells = t.n_cells;
+      v.n_fam = t.n_fam;
+      v.n_leaf = (i64)t.leaf_cells.size();
+      v.n_edge = (i64)t.edge_fams.size();
+      v.off = off;
+      off += (v.n + 31) / 32 * 32;    // 256-byte aligned level segments
+      v.ldc = (long)t.n_cells;
+      std::vector<int> soa((size_t)t.n_cells * nn);
+      for (i64 c = 0; c < t.n_cells; ++c)
+        for (int b = 0; b < nn; ++b) soa[(size_t)b * t.n_cells + c] = t.cell_dofs[(size_t)c * nn + b];
+      v.cell_dofs = d->upload(soa);
+      std::vector<unsigned char> cls(t.n_dofs);
+      for (i64 i = 0; i < t.n_dofs; ++i) cls[i] = t.dof_cls[i] == CLS_E ? 1 : 0;
+      v.cls = d->upload(cls);
+      v.fam_parent = d->upload(t.fam_parent);
+      std::vector<unsigned long long> mk(t.fam_mask.begin(), t.fam_mask.end());
+      v.fam_mask = d->upload(mk);
+      v.mask_words = t.mask_words;
+      v.leaf_cells = d->upload(t.leaf_cells);
+      v.edge_fams = d->upload(t.edge_fams);
+      v.h = std::ldexp(1.0, -l);
+      v.scale = Tp.dim == 3 ? v.h : 1.0;
+      if (!coef_off.empty()) {
+        std::vector<double> cc(coef_flat.begin() + coef_off[l], coef_flat.begin() + coef_off[l + 1]);
+        v.coef = d->upload(cc);
+      }
+      v.Dinv = d->alloc<double>(v.n);
+    }
+    d->N = off;
+    const i64 N = d->N;
+    d->D = d->alloc<double>(N);
+    d->X = d->alloc<double>(N);
+    d->T = d->alloc<double>(N);
+    d->DV = d->alloc<double>(N);
+    d->W = d->alloc<double>(N);
+    d->Y = d->alloc<double>(N);
+    d->cx = d->alloc<double>(N);
+    d->cr = d->alloc<double>(N);
+    d->cp = d->alloc<double>(N);
+    d->cq = d->alloc<double>(N);
+    d->cz = d->alloc<double>(N);
+    for (double* p : {d->D, d->X, d->T, d->DV, d->W, d->Y, d->cx, d->cr, d->cp, d->cq, d->cz})
+      CK(cudaMemset(p, 0, N * sizeof(double)));
+    // lambda mask and leaf <-> MG maps
+    std::vector<unsigned char> lam(N, 0);
+    std::vector<long long> m2l(N, -1), l2m(Tp.n_leaf);
+    for (int l = 0; l <= Tp.L; ++l)
+      for (i64 i = 0; i < Tp.lv[l].n_dofs; ++i) lam[d->lv[l].off + i] = Tp.lv[l].dof_lam[i];
+    for (i64 g = 0; g < Tp.n_leaf; ++g) {
+      i64 m = d->lv[Tp.leaf_lambda[g]].off + Tp.leaf_level_index[g];
+      l2m[g] = m;
+      m2l[m] = g;
+    }
+    d->n_leaf = Tp.n_leaf;
+    d->lam_mg = d->upload(lam);
+    d->mg_to_leaf = d->upload(m2l);
+    d->leaf_to_mg = d->upload(l2m);
+    d->nred = d->sms * 4;
+    d->partial = d->alloc<double>(d->nred);
+    d->scal = d->alloc<double>(16);
+    CK(cudaMemset(d->scal, 0, 16 * sizeof(double)));
+    CK(cudaMallocHost(&d->hscal, 16 * sizeof(double)));
+    cudaStream_t s = d->cap;
+    // diagonal and D^-1 (S rows), zero-diagonal check
+    int* bad = d->alloc<int>(1);
+    CK(cudaMemset(bad, 0, sizeof(int)));
+    for (int l = 0; l <= Tp.L; ++l) {
+      DevLevel& v = d->lv[l];
+      if (v.n == 0) continue;
+      CK(cudaMemsetAsync(v.Dinv, 0, v.n * sizeof(double), s));
+      int grid = (int)((v.n_cells + 127) / 128);
+      DISPATCH_DK(d->dim, d->k,
+                  (dev::cell_diag<D_, K_><<<grid, 128, 0, s>>>((int)v.n_cells, v.cell_dofs, v.ldc, v.coef, v.scale,
+                                                               v.Dinv)));
+      dev::invert_diag<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.cls, v.Dinv, bad);
+      d->launches += 2;
+    }
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    GMG_REQUIRE(hbad == 0, GMG_E_ZERO_DIAG, "zero or negative diagonal on an S row");
+    // coarse matrix A_0^S: columns by applying K_0 to unit vectors; dense Cholesky
+    {
+      DevLevel& v0 = d->lv[0];
+      const int n0 = (int)v0.n;
+      d->nS0 = n0;
+      if (n0 > 0) {
+        GMG_REQUIRE(n0 <= 4096, GMG_E_INVALID_ARG, "coarse level too large for the dense solver");
+        std::vector<double> A((size_t)n0 * n0), e(n0);
+        double *xe = d->X + v0.off, *ye = d->Y + v0.off;
+        for (int j = 0; j < n0; ++j) {
+          std::fill(e.begin(), e.end(), 0.0);
+          e[j] = 1.0;
+          CK(cudaMemcpyAsync(xe, e.data(), n0 * sizeof(double), cudaMemcpyHostToDevice, s));
+          CK(cudaMemsetAsync(ye, 0, n0 * sizeof(double), s));
+          k_apply(d, 0, nullptr, v0.n_cells, xe, ye, s);
+          CK(cudaMemcpyAsync(A.data() + (size_t)j * n0, ye, n0 * sizeof(double), cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+        }
+        // Cholesky A = L L^T, then inverse
+        std::vector<double> Lm((size_t)n0 * n0, 0.0);
+        for (int i = 0; i < n0; ++i)
+          for (int j = 0; j <= i; ++j) {
+            double sum = 0.5 * (A[(size_t)i * n0 + j] + A[(size_t)j * n0 + i]);
+            for (int q = 0; q < j; ++q) sum -= Lm[(size_t)i * n0 + q] * Lm[(size_t)j * n0 + q];
+            if (i == j) {
+              GMG_REQUIRE(sum > 0.0, GMG_E_SINGULAR_COARSE, "coarse matrix not SPD");
+              Lm[(size_t)i * n0 + i] = std::sqrt(sum);
+            } else {
+              Lm[(size_t)i * n0 + j] = sum / Lm[(size_t)j * n0 + j];
+            }
+          }
+        std::vector<double> inv((size_t)n0 * n0);
+        for (int c = 0; c < n0; ++c) {
+          std::vector<double> y(n0), x(n0);
+          for (int i = 0; i < n0; ++i) {
+            double sum = (i == c) ? 1.0 : 0.0;
+            for (int q = 0; q < i; ++q) sum -= Lm[(size_t)i * n0 + q] * y[q];
+            y[i] = sum / Lm[(size_t)i * n0 + i];
+          }
+          for (int i = n0 - 1; i >= 0; --i) {
+            double sum = y[i];
+            for (int q = i + 1; q < n0; ++q) sum -= Lm[(size_t)q * n0 + i] * x[q];
+            x[i] = sum / Lm[(size_t)i * n0 + i];
+          }
+          for (int i = 0; i < n0; ++i) inv[(size_t)i * n0 + c] = x[i];
+        }
+        std::vector<int> idx(n0);
+        for (int i = 0; i < n0; ++i) idx[i] = i;
+        d->coarse_idx = d->upload(idx);
+        d->coarse_inv = d->upload(inv);
+      }
+    }
+    // eigenvalue estimates (levels >= 1)
+    for (int l = 1; l <= Tp.L; ++l) {
+      const LevelTopo& t = Tp.lv[l];
+      std::vector<double> vv(t.n_dofs, 0.0);
+      i64 cs = 0;
+      for (i64 c = 0; c < t.n_dofs; ++c) {
+        i64 g = t.canon_to_global[c];
+        if (t.dof_cls[g] == CLS_S) vv[g] = -5.5 + (double)(cs++ % 12);
+      }
+      d->lv[l].lam = eigen_estimate(d, l, vv, cs, s);
+      set_cheb(d, l);
+    }
+    // restore the work buffers to zero (T must be zero between applies)
+    for (double* p : {d->X, d->T, d->DV, d->W, d->Y}) CK(cudaMemsetAsync(p, 0, N * sizeof(double), s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+  } catch (...) {
+    device_destroy(d);
+    throw;
+  }
+  return d;
+}
+
+void device_destroy(DeviceHierarchy* d) {
+  if (!d) return;
+  cudaDeviceSynchronize();
+  if (d->vgraph) cudaGraphExecDestroy(d->vgraph);
+  for (void* p : d->allocs) cudaFree(p);
+  if (d->hscal) cudaFreeHost(d->hscal);
+  if (d->cap) cudaStreamDestroy(d->cap);
+  delete d;
+}
+
+// ---------------------------------------------------------------- API ops
+void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int gr = d->vgrid(d->N);
+  dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);            // copy_to_mg
+  d->launches++;
+  run_vcycle_mg(d, s);
+  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);  // copy_from_mg
+  d->launches++;
+  CK(cudaPeekAtLastError());
+}
+
+int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol, int max_it, int* iters,
+                    double* rel_res, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const i64 N = d->N;
+  const int gr = d->vgrid(N);
+  // r = b (MG layout), x = 0
+  dev::gather_to_mg<<<gr, 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
+  CK(cudaMemsetAsync(d->cx, 0, N * sizeof(double), s));
+  d->launches++;
+  double nb2 = host_dot(d, N, d->cr, d->cr, s);
+  double nb = std::sqrt(nb2);
+  int it = 0;
+  double rel = nb > 0 ? 1.0 : 0.0;
+  int status = 0;
+  if (nb > 0) {
+    // z = V(r); p = z; rz = (r, z) -> scal[0]
+    CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    run_vcycle_mg(d, s);
+    dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
+    dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 0);
+    CK(cudaMemcpyAsync(d->cp, d->cz, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    d->launches += 2;
+    status = 1;
+    for (it = 1; it <= max_it; ++it) {
+      leaf_apply_mg(d, d->cp, d->cq, d->partial, s);                           // q = A p, (p,q)
+      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 1);
+      dev::cg_update_xr<<<d->nred, dev::RED_NT, 0, s>>>(N, d->scal, d->cp, d->cq, d->cx, d->cr, d->partial);
+      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 3);
+      d->launches += 3;
+      CK(cudaMemcpyAsync(d->hscal + 3, d->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      rel = std::sqrt(d->hscal[3]) / nb;
+      if (rel <= rtol) {
+        status = 0;
+        break;
+      }
+      if (it == max_it) break;
+      CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      run_vcycle_mg(d, s);                                                      // z = V(r)
+      dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
+      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 2);
+      dev::cg_update_p<<<gr, 256, 0, s>>>(N, d->scal, d->cz, d->cp);            // p = z + beta p
+      dev::copy_scalar<<<1, 1, 0, s>>>(d->scal + 2, d->scal + 0);
+      d->launches += 4;
+    }
+    if (it > max_it) it = max_it;
+  }
+  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
+  d->launches++;
+  CK(cudaPeekAtLastError());
+  if (iters) *iters = it;
+  if (rel_res) *rel_res = rel;
+  return status;
+}
+
+void device_rhs_constant(DeviceHierarchy* d, double f, double* b, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(d->Y, 0, d->N * sizeof(double), s));
+  for (int l = 0; l <= d->L; ++l) {
+    DevLevel& v = d->lv[l];
+    if (v.n_leaf == 0) continue;
+    double fh = f * std::pow(v.h, d->dim);
+    int grid = (int)((v.n_leaf + 127) / 128);
+    DISPATCH_DK(d->dim, d->k, (dev::cell_load<D_, K_><<<grid, 128, 0, s>>>((int)v.n_leaf, v.leaf_cells, v.cell_dofs,
+                                                                            v.ldc, fh, d->Y + v.off)));
+    d->launches++;
+  }
+  for (int l = d->L; l >= 1; --l)
+    k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
+                               d->Y + d->lv[l - 1].off, s);
+  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
+  d->launches++;
+  CK(cudaPeekAtLastError());
+}
+
+void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  DevLevel& v = d->lv[l];
+  CK(cudaMemsetAsync(y, 0, v.n * sizeof(double), s));
+  k_apply(d, l, nullptr, v.n_cells, x, y, s);
+  CK(cudaPeekAtLastError());
+}
+
+void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
+  k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
+  CK(cudaPeekAtLastError());
+}
+
+void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, void* stream) {
+  k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, xc, xf, (cudaStream_t)stream);
+  CK(cudaPeekAtLastError());
+}
+
+void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int gr = d->vgrid(d->N);
+  dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
+  d->launches++;
+  leaf_apply_mg(d, d->cp, d->cq, d->partial, s);
+  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
+  d->launches++;
+  CK(cudaPeekAtLastError());
+}
+
+void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, int x_zero, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  DevLevel& v = d->lv[l];
+  GMG_REQUIRE(l >= 1, GMG_E_INVALID_ARG, "no smoother on level 0");
+  double* gg = d->W + v.off;
+  CK(cudaMemcpyAsync(gg, g, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  smooth(d, l, gg, x, d->T + v.off, d->DV + v.off, x_zero != 0, s);
+  CK(cudaPeekAtLastError());
+}
+
+void device_level_diagonal(DeviceHierarchy* d, int l, double* diag, void* stream) {
+  DevLevel& v = d->lv[l];
+  if (v.n == 0) return;
+  dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v.n, v.cls, v.Dinv, diag);
+  d->launches++;
+  CK(cudaPeekAtLastError());
+}
+
+double device_get_eigen(const DeviceHierarchy* d, int l) { return d->lv[l].lam; }
+
+void device_set_eigen(DeviceHierarchy* d, int l, double lam) {
+  d->lv[l].lam = lam;
+  set_cheb(d, l);
+  if (d->vgraph) {   // coefficients are baked into the graph: re-capture
+    cudaGraphExecDestroy(d->vgraph);
+    d->vgraph = nullptr;
+  }
+}
+
+long long device_launches(const DeviceHierarchy* d) { return d->launches; }
+void device_launch_profile(const DeviceHierarchy* d, long long* pv, long long* pl) {
+  *pv = d->per_vcycle;
+  *pl = d->per_leaf_apply;
+}
+
+}  // namespace gmg

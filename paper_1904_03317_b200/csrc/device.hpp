@@ -1,0 +1,28 @@
+// Device hierarchy interface (host C++ side; no CUDA types).
+#pragma once
+#include "forest.hpp"
+
+namespace gmg {
+
+struct DeviceHierarchy;
+
+DeviceHierarchy* device_create(const Topology& T, const gmg_params& prm, const std::vector<double>& coef_cells_flat,
+                               const std::vector<i64>& coef_offsets);
+void device_destroy(DeviceHierarchy* d);
+
+void device_vcycle(DeviceHierarchy* d, const double* b_leaf, double* x_leaf, void* stream);
+int device_solve_cg(DeviceHierarchy* d, const double* b_leaf, double* x_leaf, double rtol, int max_it,
+                    int* iters, double* rel_res, void* stream);
+void device_rhs_constant(DeviceHierarchy* d, double f, double* b_leaf, void* stream);
+void device_level_apply(DeviceHierarchy* d, int level, const double* x, double* y, void* stream);
+void device_restrict(DeviceHierarchy* d, int level, const double* r, double* dc, void* stream);
+void device_prolongate(DeviceHierarchy* d, int level, const double* xc, double* xf, void* stream);
+void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* stream);
+void device_level_smooth(DeviceHierarchy* d, int level, const double* g, double* x, int x_zero, void* stream);
+void device_level_diagonal(DeviceHierarchy* d, int level, double* diag, void* stream);
+double device_get_eigen(const DeviceHierarchy* d, int level);
+void device_set_eigen(DeviceHierarchy* d, int level, double lam);
+long long device_launches(const DeviceHierarchy* d);
+void device_launch_profile(const DeviceHierarchy* d, long long* per_vcycle, long long* per_leaf_apply);
+
+}  // namespace gmg

@@ -1,0 +1,107 @@
+// Forest of refinement trees, partition and level topology (host, integer).
+#pragma once
+
+#include "common.hpp"
+
+namespace gmg {
+
+// A forest over a brick of unit trees.  Cells are (level, G) with G the global
+// brick coordinates on the level lattice; a cell's key is morton(G).
+struct Forest {
+  int dim = 2;
+  std::vector<Vec3> trees;      // brick positions, z-ordered
+  Vec3 ext{1, 1, 1};
+  std::vector<uint8_t> occ;     // occupancy of brick positions
+  int L = 0;                    // finest level
+  std::vector<int8_t> level;    // leaves in SFC order
+  std::vector<Vec3> gc;
+  std::vector<std::vector<u64>> refined;  // per level: sorted keys of refined cells
+
+  bool in_domain(int l, const Vec3& g) const {
+    Vec3 t{0, 0, 0};
+    for (int j = 0; j < dim; ++j) {
+      if (g[j] < 0) return false;
+      t[j] = g[j] >> l;
+      if (t[j] >= ext[j]) return false;
+    }
+    return occ[(size_t)((t[2] * ext[1] + t[1]) * ext[0] + t[0])] != 0;
+  }
+  int tree_of(const Vec3& tpos) const;
+  bool is_refined(int l, u64 key) const {
+    if (l < 0 || l >= (int)refined.size()) return false;
+    const auto& v = refined[l];
+    auto it = std::lower_bound(v.begin(), v.end(), key);
+    return it != v.end() && *it == key;
+  }
+  i64 n_leaves() const { return (i64)level.size(); }
+};
+
+Forest forest_from_refined(int dim, const std::vector<Vec3>& trees, std::vector<FlatSet>& R);
+// Closure to 2:1 vertex balance: every refined cell of level >= 1 must have all
+// its same-level neighbours (inside the domain) existing, i.e. their parents
+// refined.  Processes the worklist of newly refined cells (level, key).
+// Returns the number of cells refined by the closure.
+i64 close_balance(int dim, const Forest& dom, std::vector<FlatSet>& R,
+                  std::vector<std::pair<int, u64>>& work);
+Forest forest_generate(const gmg_recipe& r);
+Forest forest_create(int dim, int n_trees, const int32_t* tree_xyz, i64 n_leaves,
+                     const int32_t* leaf_tree, const int8_t* leaf_level, const uint64_t* leaf_morton,
+                     uint32_t flags);
+
+// ------------------------------------------------------------------ partition
+struct LevelCells {
+  std::vector<u64> key;       // sorted
+  std::vector<i32> owner;
+  std::vector<uint8_t> leaf;
+};
+
+struct Partition {
+  const Forest* f = nullptr;
+  int n_ranks = 1;
+  std::vector<i32> leaf_owner;
+  std::vector<LevelCells> levels;
+};
+
+Partition make_partition(const Forest& f, int n_ranks);
+gmg_model partition_model(const Partition& p, i64 W0_override);
+
+// ------------------------------------------------------------------ topology
+enum : uint8_t { CLS_S = 0, CLS_E = 1 };
+
+struct LevelTopo {
+  int level = 0;
+  i64 n_cells = 0;
+  i64 n_fam = 0;
+  std::vector<i32> fam_parent;     // index in C_{l-1}
+  i64 n_dofs = 0;                  // |S u E|
+  std::vector<u64> dof_key;        // global order
+  std::vector<uint8_t> dof_cls;
+  std::vector<i32> dof_owner;
+  std::vector<i64> dof_canon;      // canonical (Morton) index of each global DoF
+  std::vector<i64> canon_to_global;
+  std::vector<uint8_t> dof_lam;    // lambda slot (S here, not S on l+1)
+  std::vector<i32> cell_dofs;      // [n_cells][nn], global index or -1
+  int mask_words = 0;
+  std::vector<u64> fam_mask;       // [n_fam][mask_words] transfer ownership of patch nodes
+  std::vector<i32> edge_fams;      // families owning >= 1 E patch node
+  std::vector<i32> leaf_cells;     // cells of C_l that are leaves
+  i64 nS = 0, nE = 0, nB = 0;
+  i64 leaf_nodes = 0, hanging = 0, dirichlet = 0;
+};
+
+struct Topology {
+  int dim = 2, k = 2, L = 0, n_ranks = 1;
+  std::vector<LevelTopo> lv;
+  // free leaf DoFs in global leaf order
+  i64 n_leaf = 0;
+  std::vector<u64> leaf_key;
+  std::vector<int8_t> leaf_lambda;
+  std::vector<i32> leaf_owner;
+  std::vector<i64> leaf_canon;
+  std::vector<i64> leaf_level_index;   // global level index at lambda
+  i64 n_leaf_nodes = 0, n_hanging = 0, n_dirichlet = 0;
+};
+
+Topology make_topology(const Forest& f, const Partition& p, int k);
+
+}  // namespace gmg

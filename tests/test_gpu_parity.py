@@ -1,0 +1,234 @@
+"""Float parity of the CUDA path (through the C ABI) against the oracle.
+
+Bars (BASELINE.json north_star): operator applies / transfers / diagonal /
+leaf operator 1e-12 relative (max-norm, reading R23), one V-cycle 1e-10,
+CG iterations +-1 at 1e-8.  Inputs: uniform[-1,1) by canonical index
+(gmg_inputs, seed 190403317).  With p = 1 the library's global level/leaf
+order equals the canonical (Morton) order of the oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1904_03317_b200 as G  # noqa: E402
+from gmg_inputs import config, uniform_pm1, STREAM_PROBE  # noqa: E402
+from oracle import forest as F, mg  # noqa: E402
+
+OP_TOL = 1e-12
+VC_TOL = 1e-10
+
+
+def dev(a):
+    return torch.tensor(np.asarray(a), device="cuda", dtype=torch.float64)
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    s = np.abs(b).max()
+    return np.abs(a - b).max() / (s if s > 0 else 1.0)
+
+
+_cache = {}
+
+
+def pair(name, k=None, passes=-1, cfg_over=None):
+    key = (name, k, passes, tuple(sorted((cfg_over or {}).items())))
+    if key in _cache:
+        return _cache[key]
+    cfg = dict(config(name))
+    if cfg_over:
+        cfg.update(cfg_over)
+    if k is not None:
+        cfg["k"] = k
+    f, part, h = G.build_config(cfg, passes=passes)
+    of = F.generate(cfg, passes=passes)
+    oh = mg.build(of, cfg["k"])
+    _cache[key] = (h, oh, (f, part))
+    return _cache[key]
+
+
+CASES = [("c1", None), ("c1", 2), ("c3p2", None), ("c3p2", 1)]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[f"{n}-k{k}" for n, k in CASES])
+def hp(request):
+    return pair(*request.param)
+
+
+def test_sizes_match(hp):
+    h, oh, _ = hp
+    info = h.info()
+    assert info["n_levels"] == oh.L + 1
+    assert info["n_leaf_free"] == oh.leaf.n_free
+    for l, lev in enumerate(oh.levels):
+        assert info["level_dofs"][l] == lev.space.n
+
+
+def test_level_apply(hp):
+    h, oh, _ = hp
+    off = 0
+    for l, lev in enumerate(oh.levels):
+        n = lev.space.n
+        if n == 0:
+            continue
+        x = uniform_pm1(n, STREAM_PROBE, offset=off)
+        off += n
+        y = torch.zeros(n, device="cuda", dtype=torch.float64)
+        h.level_apply(l, dev(x), y)
+        assert rel(y.cpu().numpy(), lev.K @ x) < OP_TOL, l
+
+
+def test_diagonal(hp):
+    h, oh, _ = hp
+    for l, lev in enumerate(oh.levels):
+        n = lev.space.n
+        if n == 0:
+            continue
+        d = torch.zeros(n, device="cuda", dtype=torch.float64)
+        h.level_diagonal(l, d)
+        ref = np.where(lev.S, lev.K.diagonal(), 0.0)
+        assert rel(d.cpu().numpy(), ref) < OP_TOL
+
+
+def test_transfers_and_adjointness(hp):
+    h, oh, _ = hp
+    for l in range(1, oh.L + 1):
+        P = oh.levels[l].P
+        nf, nc = P.shape
+        if nf == 0 or nc == 0:
+            continue
+        xc = uniform_pm1(nc, STREAM_PROBE, offset=7 * l)
+        rf = uniform_pm1(nf, STREAM_PROBE, offset=1000 + 7 * l)
+        xf = torch.zeros(nf, device="cuda", dtype=torch.float64)
+        h.prolongate(l, dev(xc), xf)
+        assert rel(xf.cpu().numpy(), P @ xc) < OP_TOL
+        dc = torch.zeros(nc, device="cuda", dtype=torch.float64)
+        h.restrict(l, dev(rf), dc)
+        assert rel(dc.cpu().numpy(), P.T @ rf) < OP_TOL
+        # <R r, x> = <r, P x> (R = P^T)
+        lhs = float(dc.cpu().numpy() @ xc)
+        rhs = float(rf @ xf.cpu().numpy())
+        assert abs(lhs - rhs) <= 1e-12 * max(abs(lhs), 1.0)
+
+
+def test_leaf_apply_and_rhs(hp):
+    h, oh, _ = hp
+    n = oh.leaf.n_free
+    u = uniform_pm1(n, STREAM_PROBE, offset=99)
+    v = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.leaf_apply(dev(u), v)
+    assert rel(v.cpu().numpy(), oh.A_leaf @ u) < OP_TOL
+    b = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, b)
+    assert rel(b.cpu().numpy(), oh.b_leaf) < OP_TOL
+
+
+def test_eigen_estimates(hp):
+    h, oh, _ = hp
+    for l in range(1, oh.L + 1):
+        ref = oh.levels[l].lam
+        got = h.get_eigen(l)
+        assert abs(got - ref) <= 1e-10 * max(ref, 1e-300), (l, got, ref)
+
+
+def test_smoother(hp):
+    h, oh, _ = hp
+    for l in range(1, oh.L + 1):
+        lev = oh.levels[l]
+        n = lev.space.n
+        if not lev.S.any():
+            continue
+        h.set_eigen(l, lev.lam)
+        g = uniform_pm1(n, STREAM_PROBE, offset=3 * l) * (lev.S | lev.E)
+        x0 = uniform_pm1(n, STREAM_PROBE, offset=5000 + 3 * l)
+        x = dev(x0)
+        h.level_smooth(l, dev(g), x, False)
+        ref = mg.chebyshev(lev, g, x0, oh.degree)
+        assert rel(x.cpu().numpy(), ref) < VC_TOL
+        x = torch.zeros(n, device="cuda", dtype=torch.float64)
+        h.level_smooth(l, dev(g), x, True)
+        ref = mg.chebyshev(lev, g, None, oh.degree)
+        assert rel(x.cpu().numpy(), ref) < VC_TOL
+
+
+def test_vcycle(hp):
+    h, oh, _ = hp
+    for l in range(1, oh.L + 1):
+        h.set_eigen(l, oh.levels[l].lam)
+    n = oh.leaf.n_free
+    b = uniform_pm1(n)
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.vcycle(dev(b), x)
+    assert rel(x.cpu().numpy(), mg.vcycle(oh, b)) < VC_TOL
+    # zero in, zero out; linearity
+    z = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.vcycle(torch.zeros(n, device="cuda", dtype=torch.float64), z)
+    assert float(z.abs().max()) == 0.0
+    x2 = torch.zeros_like(x)
+    h.vcycle(dev(2.5 * b), x2)
+    assert rel(x2.cpu().numpy(), 2.5 * x.cpu().numpy()) < 1e-13
+
+
+def test_cg_iterations(hp):
+    h, oh, _ = hp
+    n = oh.leaf.n_free
+    b = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, b)
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    it, relres, _ = h.solve_cg(b, x, rtol=1e-8)
+    xo, it_ref, rel_ref, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
+    assert abs(it - it_ref) <= 1, (it, it_ref)
+    assert relres <= 1e-8
+    tr = np.linalg.norm(oh.b_leaf - oh.A_leaf @ x.cpu().numpy()) / np.linalg.norm(oh.b_leaf)
+    assert tr <= 1.01e-8
+    assert rel(x.cpu().numpy(), xo) < 1e-6
+
+
+def test_cg_not_converged_and_zero_rhs():
+    h, oh, _ = pair("c1")
+    n = oh.leaf.n_free
+    b = dev(uniform_pm1(n))
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    it, relres, code = h.solve_cg(b, x, rtol=1e-30, max_it=3, raise_on_fail=False)
+    assert code == 9 and it == 3 and relres > 0
+    it, relres, code = h.solve_cg(torch.zeros(n, device="cuda", dtype=torch.float64), x, rtol=1e-8)
+    assert it == 0 and float(x.abs().max()) == 0.0
+
+
+def test_graph_and_eager_agree():
+    cfg = config("c1")
+    _, _, h1 = G.build_config(cfg, graph=True)
+    _, _, h2 = G.build_config(cfg, graph=False)
+    n = h1.info()["n_leaf_free"]
+    b = dev(uniform_pm1(n))
+    x1 = torch.zeros(n, device="cuda", dtype=torch.float64)
+    x2 = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h1.vcycle(b, x1)
+    h1.vcycle(b, x1)
+    h2.vcycle(b, x2)
+    assert rel(x1.cpu().numpy(), x2.cpu().numpy()) < 1e-13
+    assert h1.launch_count() > 0
+
+
+@pytest.mark.parametrize("name", ["c2", "c3p4"])
+def test_large_config_vcycle_and_cg(name):
+    h, oh, _ = pair(name)
+    for l in range(1, oh.L + 1):
+        assert abs(h.get_eigen(l) - oh.levels[l].lam) <= 1e-10 * oh.levels[l].lam
+    n = oh.leaf.n_free
+    b = uniform_pm1(n)
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.vcycle(dev(b), x)
+    assert rel(x.cpu().numpy(), mg.vcycle(oh, b)) < VC_TOL
+    u = uniform_pm1(n, STREAM_PROBE)
+    v = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.leaf_apply(dev(u), v)
+    assert rel(v.cpu().numpy(), oh.A_leaf @ u) < OP_TOL
+    bb = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, bb)
+    xs = torch.zeros(n, device="cuda", dtype=torch.float64)
+    it, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
+    _, it_ref, _, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
+    assert abs(it - it_ref) <= 1, (it, it_ref)
