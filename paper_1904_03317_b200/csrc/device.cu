@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.hpp"
 #include "kernels.cuh"
@@ -19,15 +20,15 @@ namespace gmg {
   } while (0)
 
 struct DevLevel {
-  i64 n = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
-  int* cell_dofs = nullptr;
+  i64 n = 0, n_pad = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
+  int* cell_dofs = nullptr;         // SoA [(k+1)^d][n_cells]
   long ldc = 0;
   double* coef = nullptr;
   unsigned char* cls = nullptr;     // bit0 = E
-  double* Dinv = nullptr;
+  double* Dinv = nullptr;           // n_pad entries, 0 on E rows and in the padding
   int* fam_parent = nullptr;
-  unsigned long long* fam_mask = nullptr;
-  int mask_words = 0;
+  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam]
+  int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
   double h = 1, scale = 1;          // scale = h^(d-2)
@@ -54,6 +55,8 @@ struct DeviceHierarchy {
   int* coarse_idx = nullptr;
   double* coarse_inv = nullptr;
   bool use_graph = true;
+  bool xfer_warp = true;        // warp-per-family transfers (GMG_XFER=thread: thread per family)
+  bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
@@ -92,13 +95,30 @@ struct DeviceHierarchy {
   } while (0)
 
 // ---------------------------------------------------------------- primitives
+// y += K_l x over a cell list (leaf cells) or, list == nullptr, over all of C_l.
+// Full levels >= 1 run family-blocked (y must be zero on entry: patch-interior
+// nodes are stored, not added); level 0 and cell lists run thread-per-cell.
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
-  const int nt = 128;
-  int grid = (int)((n + nt - 1) / nt);
-  DISPATCH_DK(d->dim, d->k, (dev::cell_apply<D_, K_><<<grid, nt, 0, s>>>((int)n, list, v.cell_dofs, v.ldc, v.coef,
-                                                                            v.scale, x, y)));
+  if (list == nullptr && l > 0 && v.n_fam > 0 && v.coef == nullptr && d->tensor_apply) {
+    const int row = (int)(d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) + (d->k + 1) * (d->k + 1) * (d->k + 1)
+                                      : (2 * d->k + 1) * (2 * d->k + 1) + (d->k + 1) * (d->k + 1));
+    int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
+    DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+                                  (int)v.n_fam, v.xfer, row, v.scale, x, y)));
+  } else if (list == nullptr && l > 0 && v.n_fam > 0) {
+    DISPATCH_DK(d->dim, d->k, {
+      constexpr int FPB = dev::FamCfg<D_, K_>::FPB;
+      int grid = (int)((v.n_fam + FPB - 1) / FPB);
+      dev::fam_apply<D_, K_><<<grid, FPB * (1 << D_), 0, s>>>((int)v.n_fam, v.fam_dofs, v.coef, v.scale, x, y);
+    });
+  } else {
+    const int nt = 128;
+    int grid = (int)((n + nt - 1) / nt);
+    DISPATCH_DK(d->dim, d->k, (dev::cell_apply<D_, K_><<<grid, nt, 0, s>>>((int)n, list, v.cell_dofs, v.ldc, v.coef,
+                                                                              v.scale, x, y)));
+  }
   d->launches++;
 }
 
@@ -108,11 +128,17 @@ static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
   DevLevel& c = d->lv[l - 1];
-  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  if (d->xfer_warp) {
+    int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+    DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                                  (int)nf, list, f.xfer, f.cls, vin, t, dc)));
+    d->launches++;
+    return;
+  }
+  int grid = (int)((nf + dev::XFER_NT - 1) / dev::XFER_NT);
   DISPATCH_DK(d->dim, d->k,
-              (dev::fam_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
-                  (int)nf, list, f.fam_parent, f.fam_mask, f.mask_words, c.cell_dofs, c.ldc, f.cell_dofs, f.ldc, f.cls,
-                  vin, t, dc)));
+              (dev::fam_restrict<D_, K_, MODE><<<grid, dev::XFER_NT, 0, s>>>(
+                  (int)nf, (int)f.n_fam, list, f.fam_parent, f.fam_dofs, c.cell_dofs, c.ldc, f.cls, vin, t, dc)));
   d->launches++;
 }
 
@@ -122,11 +148,26 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
   DevLevel& c = d->lv[l - 1];
-  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  if (d->xfer_warp) {
+    int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+    DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                                  (int)nf, list, f.xfer, f.cls, xc, xf)));
+    d->launches++;
+    return;
+  }
+  int grid = (int)((nf + dev::XFER_NT - 1) / dev::XFER_NT);
   DISPATCH_DK(d->dim, d->k,
-              (dev::fam_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
-                  (int)nf, list, f.fam_parent, f.fam_mask, f.mask_words, c.cell_dofs, c.ldc, f.cell_dofs, f.ldc, f.cls,
-                  xc, xf)));
+              (dev::fam_prolongate<D_, K_, MODE><<<grid, dev::XFER_NT, 0, s>>>(
+                  (int)nf, (int)f.n_fam, list, f.fam_parent, f.fam_dofs, c.cell_dofs, c.ldc, f.cls, xc, xf)));
+  d->launches++;
+}
+
+template <bool RT, bool RDV, bool WDV, bool XZ>
+static void k_cheb(DeviceHierarchy* d, DevLevel& v, const double* g, double* t, double* dv, double* x, double c1,
+                   double c2, cudaStream_t s) {
+  // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
+  dev::cheb_step<RT, RDV, WDV, XZ><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
+      (const double2*)g, (const double2*)v.Dinv, (double2*)t, (double2*)dv, (double2*)x, c1, c2);
   d->launches++;
 }
 
@@ -136,27 +177,19 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
 static void smooth(DeviceHierarchy* d, int l, const double* g, double* x, double* t, double* dv, bool x_zero,
                    cudaStream_t s) {
   DevLevel& v = d->lv[l];
-  const i64 n = v.n;
-  if (n == 0) return;
+  if (v.n == 0) return;
   const int m = d->m;
-  const int gr = d->vgrid(n);
   if (x_zero) {
-    dev::cheb_step<false, false, true, true><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
+    k_cheb<false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else {
     k_apply(d, l, nullptr, v.n_cells, x, t, s);
-    if (m == 1)
-      dev::cheb_step<true, false, false, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
-    else
-      dev::cheb_step<true, false, true, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, 0.0, v.c2[0]);
+    if (m == 1) k_cheb<true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    else k_cheb<true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   }
-  d->launches++;
   for (int j = 1; j < m; ++j) {
     k_apply(d, l, nullptr, v.n_cells, x, t, s);
-    if (j == m - 1)
-      dev::cheb_step<true, true, false, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, v.c1[j], v.c2[j]);
-    else
-      dev::cheb_step<true, true, true, false><<<gr, 256, 0, s>>>(n, g, v.Dinv, t, dv, x, v.c1[j], v.c2[j]);
-    d->launches++;
+    if (j == m - 1) k_cheb<true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
+    else k_cheb<true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
   }
 }
 
@@ -353,6 +386,8 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
     d->hi = prm.cheb_hi;
     d->eig_iters = prm.eig_iters;
     d->use_graph = !(prm.flags & GMG_NO_GRAPH);
+    if (const char* e = std::getenv("GMG_XFER")) d->xfer_warp = std::string(e) != "thread";
+    if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
     const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
@@ -362,12 +397,13 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
       const LevelTopo& t = Tp.lv[l];
       DevLevel& v = d->lv[l];
       v.n = t.n_dofs;
+      v.n_pad = (v.n + dev::VEC_PAD - 1) / dev::VEC_PAD * dev::VEC_PAD;   // zero padding
       v.n_cells = t.n_cells;
       v.n_fam = t.n_fam;
       v.n_leaf = (i64)t.leaf_cells.size();
       v.n_edge = (i64)t.edge_fams.size();
       v.off = off;
-      off += (v.n + 31) / 32 * 32;    // 256-byte aligned level segments
+      off += v.n_pad;
       v.ldc = (long)t.n_cells;
       std::vector<int> soa((size_t)t.n_cells * nn);
       for (i64 c = 0; c < t.n_cells; ++c)
@@ -377,9 +413,24 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
       for (i64 i = 0; i < t.n_dofs; ++i) cls[i] = t.dof_cls[i] == CLS_E ? 1 : 0;
       v.cls = d->upload(cls);
       v.fam_parent = d->upload(t.fam_parent);
-      std::vector<unsigned long long> mk(t.fam_mask.begin(), t.fam_mask.end());
-      v.fam_mask = d->upload(mk);
-      v.mask_words = t.mask_words;
+      {
+        // patch table AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
+        const size_t np = t.n_fam ? t.fam_dofs.size() / (size_t)t.n_fam : 0;
+        std::vector<int> fs(t.fam_dofs.size());
+        for (size_t f = 0; f < (size_t)t.n_fam; ++f)
+          for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.fam_dofs[f * np + a];
+        v.fam_dofs = d->upload(fs);
+        if (l > 0 && t.n_fam > 0) {
+          const size_t row = np + nn;
+          const LevelTopo& tc = Tp.lv[l - 1];
+          std::vector<int> xf((size_t)t.n_fam * row);
+          for (size_t f = 0; f < (size_t)t.n_fam; ++f) {
+            for (size_t a = 0; a < np; ++a) xf[f * row + a] = t.fam_dofs[f * np + a];
+            for (int j = 0; j < nn; ++j) xf[f * row + np + j] = tc.cell_dofs[(size_t)t.fam_parent[f] * nn + j];
+          }
+          v.xfer = d->upload(xf);
+        }
+      }
       v.leaf_cells = d->upload(t.leaf_cells);
       v.edge_fams = d->upload(t.edge_fams);
       v.h = std::ldexp(1.0, -l);
@@ -388,7 +439,8 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
         std::vector<double> cc(coef_flat.begin() + coef_off[l], coef_flat.begin() + coef_off[l + 1]);
         v.coef = d->upload(cc);
       }
-      v.Dinv = d->alloc<double>(v.n);
+      v.Dinv = d->alloc<double>(v.n_pad);
+      CK(cudaMemset(v.Dinv, 0, v.n_pad * sizeof(double)));
     }
     d->N = off;
     const i64 N = d->N;
@@ -648,9 +700,15 @@ void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, 
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   GMG_REQUIRE(l >= 1, GMG_E_INVALID_ARG, "no smoother on level 0");
+  // padded internal copies (the vector kernels stream the padded segment)
   double* gg = d->W + v.off;
+  double* xx = d->Y + v.off;
   CK(cudaMemcpyAsync(gg, g, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  smooth(d, l, gg, x, d->T + v.off, d->DV + v.off, x_zero != 0, s);
+  if (!x_zero) CK(cudaMemcpyAsync(xx, x, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  smooth(d, l, gg, xx, d->T + v.off, d->DV + v.off, x_zero != 0, s);
+  CK(cudaMemcpyAsync(x, xx, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(gg, 0, v.n_pad * sizeof(double), s));
+  CK(cudaMemsetAsync(xx, 0, v.n_pad * sizeof(double), s));
   CK(cudaPeekAtLastError());
 }
 

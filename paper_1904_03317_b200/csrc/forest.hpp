@@ -81,8 +81,9 @@ struct LevelTopo {
   std::vector<i64> canon_to_global;
   std::vector<uint8_t> dof_lam;    // lambda slot (S here, not S on l+1)
   std::vector<i32> cell_dofs;      // [n_cells][nn], global index or -1
-  int mask_words = 0;
-  std::vector<u64> fam_mask;       // [n_fam][mask_words] transfer ownership of patch nodes
+  // [n_fam][(2k+1)^d] family patch -> level DoF: v >= 0 owned (transfers) by
+  // this family, -1 Dirichlet, v <= -2 DoF -2-v owned by an earlier family
+  std::vector<i32> fam_dofs;
   std::vector<i32> edge_fams;      // families owning >= 1 E patch node
   std::vector<i32> leaf_cells;     // cells of C_l that are leaves
   i64 nS = 0, nE = 0, nB = 0;

@@ -281,18 +281,22 @@ Topology make_topology(const Forest& f, const Partition& p, int k) {
         i64 o = l == 0 ? c * nn + b : (c / nch) * np + pt.cell_to_patch[c % nch][b];
         t.cell_dofs[(size_t)c * nn + b] = (i32)glob_of_node[node_of_occ[o]];
       }
-    // ---------------- transfer ownership masks (first family containing the node)
+    // ---------------- family patch table with transfer ownership (the first
+    // family containing a fine node owns it for restriction / prolongation)
     if (l > 0) {
-      t.mask_words = (np + 63) / 64;
-      t.fam_mask.assign((size_t)t.n_fam * t.mask_words, 0);
+      t.fam_dofs.resize((size_t)t.n_fam * np);
       std::vector<uint8_t> edge(t.n_fam, 0);
-      for (i64 r = 0; r < nnodes; ++r) {
-        if (nfl[r] & F_B) continue;
-        i64 o = nfirst[r];
-        i64 fi = o / np;
-        int a = (int)(o % np);
-        t.fam_mask[(size_t)fi * t.mask_words + a / 64] |= 1ull << (a % 64);
-        if (nfl[r] & F_EREG) edge[fi] = 1;
+      for (i64 o = 0; o < n_occ; ++o) {
+        const i64 r = node_of_occ[o];
+        const i64 g = glob_of_node[r];
+        if (g < 0) {
+          t.fam_dofs[o] = -1;
+        } else if (nfirst[r] == o) {
+          t.fam_dofs[o] = (i32)g;
+          if (nfl[r] & F_EREG) edge[o / np] = 1;
+        } else {
+          t.fam_dofs[o] = (i32)(-2 - g);
+        }
       }
       for (i64 fi = 0; fi < t.n_fam; ++fi)
         if (edge[fi]) t.edge_fams.push_back((i32)fi);
