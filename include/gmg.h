@@ -232,6 +232,11 @@ gmg_status gmg_rhs_constant(gmg_hierarchy *h, double f, double *b_dev, void *cud
 /* y = K_l x over all cells of C_l on S u E rows (edge rows included). */
 gmg_status gmg_level_apply(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
                            void *cuda_stream);
+/* The level-operator kernel alone (no memset): y must be zero on entry, y = K_l x
+ * on exit.  For timing the kernel in isolation (repeated calls on the same y
+ * give a meaningless y but the same work per launch). */
+gmg_status gmg_level_apply_kernel(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
+                                  void *cuda_stream);
 /* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1) */
 gmg_status gmg_restrict(gmg_hierarchy *h, int level, const double *r_fine_dev,
                         double *d_coarse_dev, void *cuda_stream);

@@ -107,6 +107,7 @@ _SIGS = {
                      C.c_int),
     "gmg_rhs_constant": ([_vp, C.c_double, _vp, _vp], C.c_int),
     "gmg_level_apply": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_level_apply_kernel": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_restrict": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_prolongate": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_leaf_apply": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -330,6 +331,9 @@ class Hierarchy:
 
     def level_apply(self, level, x, y, stream=None):
         _check(_lib.gmg_level_apply(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
+
+    def level_apply_kernel(self, level, x, y, stream=None):
+        _check(_lib.gmg_level_apply_kernel(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
 
     def restrict(self, level, r, dc, stream=None):
         _check(_lib.gmg_restrict(self.h, level, _ptr(r), _ptr(dc), _stream(stream)))

@@ -344,6 +344,16 @@ gmg_status gmg_level_apply(gmg_hierarchy* h, int level, const double* x, double*
   });
 }
 
+gmg_status gmg_level_apply_kernel(gmg_hierarchy* h, int level, const double* x, double* y, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(x);
+    NEED(y);
+    need_level(h, level);
+    gmg::device_level_apply_kernel(need_dev(h), level, x, y, s);
+  });
+}
+
 gmg_status gmg_restrict(gmg_hierarchy* h, int level, const double* r, double* dc, void* s) {
   return guard([&] {
     NEED(h);

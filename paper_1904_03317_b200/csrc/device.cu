@@ -675,6 +675,12 @@ void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, v
   CK(cudaPeekAtLastError());
 }
 
+void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
+  DevLevel& v = d->lv[l];
+  k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
+  CK(cudaPeekAtLastError());
+}
+
 void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
   k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());

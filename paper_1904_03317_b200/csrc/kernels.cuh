@@ -275,25 +275,21 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, double scale, 
                  double* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
   __shared__ double s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
-  __shared__ int sidx[TENSOR_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int f = blockIdx.x * TENSOR_WARPS + w;
   if (f >= nfam) return;
   const int* rp = xfer + (long)f * row;
-  for (int a = lane; a < NP; a += 32) {
-    const int i = decode_dof(__ldg(rp + a));
-    sidx[w][a] = i;
-    s0[w][a] = i >= 0 ? __ldg(x + i) : 0.0;
-  }
-  __syncwarp();
   double out[NP1];
   int ob = 0, os = 0;   // output line: base and stride in the patch
   if constexpr (D == 3) {
     constexpr int S2 = NP1 * NP1;
-    if (lane < NL) {     // z lines: lane = (px, py)
+    if (lane < NL) {     // z lines: lane = (px, py), gathered straight into registers
+      int gi[NP1];
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
       double u[NP1];
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) u[z] = s0[w][z * S2 + lane];
+      for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : 0.0;
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         double t1 = 0.0, t2 = 0.0;
@@ -352,11 +348,14 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, double scale, 
       }
     }
   } else {
-    if (lane < NL) {     // x lines: lane = py
+    if (lane < NL) {     // x lines: lane = py, gathered straight into registers
       const int b = lane * NP1;
       double u[NP1];
 #pragma unroll
-      for (int q = 0; q < NP1; ++q) u[q] = s0[w][b + q];
+      for (int q = 0; q < NP1; ++q) {
+        const int gi = decode_dof(__ldg(rp + b + q));
+        u[q] = gi >= 0 ? __ldg(x + gi) : 0.0;
+      }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
         double a = 0.0, bb = 0.0;
@@ -395,7 +394,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, double scale, 
 #pragma unroll
     for (int q = 0; q < NP1; ++q) {
       const int a = ob + q * os;
-      const int i = sidx[w][a];
+      const int i = decode_dof(__ldg(rp + a));
       if (i < 0) continue;
       int ad[3] = {a % NP1, (a / NP1) % NP1, D == 3 ? a / (NP1 * NP1) : 1};
       bool interior = ad[0] > 0 && ad[0] < 2 * K && ad[1] > 0 && ad[1] < 2 * K && (D == 2 || (ad[2] > 0 && ad[2] < 2 * K));
