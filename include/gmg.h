@@ -149,7 +149,27 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
  */
 #define GMG_HOST_ONLY 1u      /* integer topology only, no device data (exports, CPU tests) */
 #define GMG_NO_GRAPH 2u       /* do not capture the V-cycle in a CUDA graph */
-#define GMG_LOCAL_RANKS 4u    /* all n_ranks logical ranks in this process (not yet used) */
+#define GMG_LOCAL_RANKS 4u    /* all n_ranks ranks live in this process (one host thread and
+                                 stream each, same GPU); params.nccl_comm is a gmg_local_world */
+
+/* ------------------------------------------------------------------ communicators
+ * Multi-rank runs (one rank per GPU, "processor" = MPI rank): each rank
+ * calls every collective entry point (gmg_setup, gmg_vcycle, gmg_solve_cg,
+ * gmg_leaf_apply, gmg_rhs_constant) with its own leaf vectors (the DoFs it
+ * owns, n_owned = gmg_info.n_owned).  Ghost exchanges use grouped
+ * ncclSend/ncclRecv over NVLink, CG dots one ncclAllReduce.  libnccl.so.2 is
+ * loaded at run time (GMG_NCCL_LIB overrides the path).
+ * gmg_nccl_get_unique_id: rank 0 creates the id (128 bytes, host), the caller
+ * broadcasts it; gmg_nccl_comm_init: every rank, collective. */
+gmg_status gmg_nccl_get_unique_id(char id[128]);
+gmg_status gmg_nccl_comm_init(const char id[128], int n_ranks, int rank, void **comm);
+gmg_status gmg_nccl_comm_destroy(void *comm);
+/* Test transport: n ranks as host threads of one process on one GPU.  Each
+ * thread calls the collective entry points for its rank concurrently; the
+ * exchanges are host barriers plus stream-ordered device copies (no kernel
+ * waits on another). */
+gmg_status gmg_local_world_create(int n_ranks, void **world);
+gmg_status gmg_local_world_destroy(void *world);
 
 typedef struct {
   int k;                    /* Q_k degree, 1 or 2 */
@@ -199,6 +219,13 @@ gmg_status gmg_export_level_dofs(const gmg_hierarchy *h, int level, int64_t *n, 
 /* Free leaf DoFs in global leaf order: key, lambda, owner, canonical index. */
 gmg_status gmg_export_leaf_dofs(const gmg_hierarchy *h, int64_t *n, uint64_t *key, int8_t *lambda,
                                 int32_t *owner, int64_t *canonical);
+/* Rank-local layout of `level` for this hierarchy's rank: owned DoFs are the
+ * global range [first_owned, first_owned + n_owned); ghosts (sorted global
+ * indices, host [n_ghost]) are the DoFs owned elsewhere that this rank's
+ * families (children of the refined cells it owns, first-child rule) or the
+ * parents of its next-finer families touch.  ghosts may be NULL. */
+gmg_status gmg_export_rank_level(const gmg_hierarchy *h, int level, int64_t *first_owned, int64_t *n_owned,
+                                 int64_t *n_ghost, int64_t *ghosts);
 /* Cell -> level-DoF table of `level` (global index, -1 for Dirichlet nodes):
  * host [n_cells * (k+1)^d], cells in SFC order, local nodes x fastest. */
 gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_cells,

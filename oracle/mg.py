@@ -92,7 +92,7 @@ def topology(f: Forest, k: int, n_ranks: int = 1) -> Topology:
     owners = leaf_owners(f, n_ranks)
     cells = level_cells(f, owners)
     leafsets = leaf_level_sets(f, lat)
-    spaces = [level_space(f, lat, c, leafsets) for c in cells]
+    spaces = [level_space(f, lat, c, leafsets, cells[l - 1] if l else None) for l, c in enumerate(cells)]
     leaf = leaf_space(f, lat, owners, spaces, lambda xi: fem.lagrange(k, xi))
     fX = leaf.X[leaf.free_index >= 0]
     own = np.empty(leaf.n_free, dtype=np.int64)
@@ -116,7 +116,7 @@ def build(f: Forest, k: int, n_ranks: int = 1, coef_level2: np.ndarray | None = 
     owners = leaf_owners(f, n_ranks)
     cells = level_cells(f, owners)
     leafsets = leaf_level_sets(f, lat)
-    spaces = [level_space(f, lat, c, leafsets) for c in cells]
+    spaces = [level_space(f, lat, c, leafsets, cells[l - 1] if l else None) for l, c in enumerate(cells)]
     coef = None
     if coef_level2 is not None:
         coef = fem.Coefficient(np.asarray(coef_level2, dtype=np.float64), cells[2].gc, lat.R)

@@ -138,7 +138,22 @@ def leaf_level_sets(f: Forest, lat: Lattice) -> dict[int, np.ndarray]:
     return {int(l): np.sort(_cell_lin(f.gc[f.level == l], Rc)) for l in np.unique(f.level)}
 
 
-def level_space(f: Forest, lat: Lattice, cells: LevelCells, leafsets=None) -> LevelSpace:
+def parent_owner(cells: LevelCells, parents: LevelCells) -> np.ndarray:
+    """Owner of the parent of every cell (the rank that computes its family)."""
+    R = int(max(cells.gc.max(initial=0), parents.gc.max(initial=0))) + 3
+    pk = _cell_lin(parents.gc, R)
+    ck = _cell_lin(cells.gc >> 1, R)
+    o = np.argsort(pk)
+    idx = o[np.searchsorted(pk[o], ck)]
+    assert np.all(pk[idx] == ck)
+    return parents.owner[idx]
+
+
+def level_space(f: Forest, lat: Lattice, cells: LevelCells, leafsets=None,
+                parents: LevelCells | None = None) -> LevelSpace:
+    """DoF owner (R25): level 0 -> rank 0 (coarse handoff); level l >= 1
+    -> min over the cells having the node of the owner of their parent (the rank
+    that computes the family)."""
     l = cells.level
     if leafsets is None:
         leafsets = leaf_level_sets(f, lat)
@@ -171,9 +186,11 @@ def level_space(f: Forest, lat: Lattice, cells: LevelCells, leafsets=None) -> Le
     kept_ids = np.nonzero(keep)[0][order]
     canon[kept_ids] = np.arange(kept_ids.size)
     cell_dofs = canon[inv].reshape(nc, nn)
-    # owner = min owner of the cells having the node
     own_u = np.full(uk.size, np.iinfo(np.int64).max, dtype=np.int64)
-    np.minimum.at(own_u, inv, np.repeat(cells.owner, nn))
+    if l == 0 or parents is None:
+        own_u[:] = 0
+    else:
+        np.minimum.at(own_u, inv, np.repeat(parent_owner(cells, parents), nn))
     owner = own_u[kept_ids]
     return LevelSpace(l, cells, X, key, cls, owner, cell_dofs, int(bnd.sum()))
 

@@ -117,7 +117,14 @@ _SIGS = {
     "gmg_set_eigen": ([_vp, C.c_int, C.c_double], C.c_int),
     "gmg_launch_count": ([_vp, _i64p], C.c_int),
     "gmg_launch_profile": ([_vp, _i64p, _i64p], C.c_int),
+    "gmg_export_rank_level": ([_vp, C.c_int, _i64p, _i64p, _i64p, _vp], C.c_int),
+    "gmg_nccl_get_unique_id": ([C.c_char_p], C.c_int),
+    "gmg_nccl_comm_init": ([C.c_char_p, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
+    "gmg_nccl_comm_destroy": ([_vp], C.c_int),
+    "gmg_local_world_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
+    "gmg_local_world_destroy": ([_vp], C.c_int),
 }
+GMG_LOCAL_RANKS = 4
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -304,6 +311,14 @@ class Hierarchy:
         _check(_lib.gmg_export_leaf_dofs(self.h, C.byref(n), _ptr(key), _ptr(lam), _ptr(own), _ptr(can)))
         return key, lam, own, can
 
+    def rank_level(self, level):
+        """(first_owned, n_owned, ghost global indices) of this rank on `level`."""
+        fo, no, ng = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib.gmg_export_rank_level(self.h, level, C.byref(fo), C.byref(no), C.byref(ng), None))
+        gh = np.empty(ng.value, np.int64)
+        _check(_lib.gmg_export_rank_level(self.h, level, C.byref(fo), C.byref(no), C.byref(ng), _ptr(gh)))
+        return fo.value, no.value, gh
+
     def cell_dofs(self, level):
         n = C.c_int64()
         _check(_lib.gmg_export_cell_dofs(self.h, level, C.byref(n), None))
@@ -369,8 +384,40 @@ class Hierarchy:
         return a.value, b.value
 
 
+class LocalWorld:
+    """n ranks as host threads of one process (test transport, gmg_local_world)."""
+
+    def __init__(self, n):
+        self.h = _vp()
+        _check(_lib.gmg_local_world_create(n, C.byref(self.h)))
+        self.n = n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.gmg_local_world_destroy(self.h)
+            self.h = None
+
+
+def gmg_nccl_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.gmg_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    def __init__(self, uid: bytes, n_ranks: int, rank: int):
+        self.h = _vp()
+        _check(_lib.gmg_nccl_comm_init(C.create_string_buffer(uid, 128), n_ranks, rank, C.byref(self.h)))
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            _lib.gmg_nccl_comm_destroy(self.h)
+            self.h = None
+
+
 def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
-              coef_level2=None, graph=True, device=-1) -> Hierarchy:
+              coef_level2=None, graph=True, device=-1, comm=None) -> Hierarchy:
+    """comm: None (one rank), a LocalWorld (ranks as threads) or an NcclComm."""
     p = gmg_params_default()
     p.k = k
     p.cheb_degree = cheb_degree
@@ -378,6 +425,11 @@ def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_deg
     p.n_ranks = part.n_ranks
     p.device = device
     p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH)
+    if isinstance(comm, LocalWorld):
+        p.flags |= GMG_LOCAL_RANKS
+        p.nccl_comm = comm.h
+    elif comm is not None:
+        p.nccl_comm = comm.h
     coef = None
     if coef_level2 is not None:
         coef = np.ascontiguousarray(coef_level2, dtype=np.float64)

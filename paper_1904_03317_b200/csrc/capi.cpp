@@ -4,6 +4,7 @@
 #include <memory>
 #include <new>
 
+#include "comm.hpp"
 #include "device.hpp"
 #include "forest.hpp"
 
@@ -16,9 +17,9 @@ struct gmg_partitioning {
 };
 struct gmg_hierarchy {
   gmg::Topology topo;
+  gmg::LocalTopo local;
   gmg_params prm{};
   gmg::DeviceHierarchy* dev = nullptr;
-  std::vector<gmg::i64> level_cells, level_fams;
   ~gmg_hierarchy() { gmg::device_destroy(dev); }
 };
 
@@ -49,7 +50,6 @@ gmg_status guard(F&& fn) {
 
 gmg::DeviceHierarchy* need_dev(gmg_hierarchy* h) {
   GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "hierarchy has no device data (GMG_HOST_ONLY)");
-  GMG_REQUIRE(h->prm.n_ranks == 1, GMG_E_STATE, "n_ranks > 1 is not supported by this build");
   return h->dev;
 }
 void need_level(const gmg_hierarchy* h, int level) {
@@ -197,15 +197,27 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
     auto h = std::make_unique<gmg_hierarchy>();
     h->prm = *prm;
     h->topo = gmg::make_topology(f->f, p->p, prm->k);
+    h->local = gmg::make_local(f->f, p->p, h->topo, prm->rank);
     if (!(prm->flags & GMG_HOST_ONLY)) {
-      GMG_REQUIRE(prm->n_ranks == 1, GMG_E_STATE, "n_ranks > 1 is not supported by this build");
-      std::vector<double> cflat;
-      std::vector<gmg::i64> coff;
       if (prm->coef_level2) {
         GMG_REQUIRE(f->f.L >= 2, GMG_E_INVALID_ARG, "coefficient per level-2 cell needs >= 3 levels");
         gmg::fail(GMG_E_INVALID_ARG, "variable coefficient (config 4) is not supported by this build yet");
       }
-      h->dev = gmg::device_create(h->topo, *prm, cflat, coff);
+      std::unique_ptr<gmg::Comm> comm;
+      if (prm->n_ranks > 1) {
+        GMG_REQUIRE(prm->nccl_comm != nullptr, GMG_E_INVALID_ARG, "n_ranks > 1 needs a communicator");
+        if (prm->flags & GMG_LOCAL_RANKS) {
+          auto* w = static_cast<gmg::LocalWorld*>(prm->nccl_comm);
+          GMG_REQUIRE(w->n == prm->n_ranks, GMG_E_INVALID_ARG, "local world size != n_ranks");
+          comm = std::make_unique<gmg::ThreadComm>(w, prm->rank);
+        } else {
+          auto c = std::make_unique<gmg::NcclComm>(prm->nccl_comm);
+          GMG_REQUIRE(c->size() == prm->n_ranks && c->rank() == prm->rank, GMG_E_INVALID_ARG,
+                      "NCCL communicator rank/size != params");
+          comm = std::move(c);
+        }
+      }
+      h->dev = gmg::device_create(h->local, *prm, std::move(comm), h->topo.lv[0].n_dofs);
     }
     *out = h.release();
   });
@@ -230,14 +242,8 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
     o->n_leaf_free = T.n_leaf;
     o->n_leaf_hanging = T.n_hanging;
     o->n_leaf_dirichlet = T.n_dirichlet;
-    gmg::i64 first = -1, cnt = 0;
-    for (gmg::i64 g = 0; g < T.n_leaf; ++g)
-      if (T.leaf_owner[g] == h->prm.rank) {
-        if (first < 0) first = g;
-        ++cnt;
-      }
-    o->n_owned = cnt;
-    o->first_owned = first < 0 ? 0 : first;
+    o->n_owned = h->local.n_leaf_owned;
+    o->first_owned = h->local.leaf_first;
     gmg::i64 mg = 0;
     for (int l = 0; l <= T.L && l < GMG_MAX_LEVELS; ++l) {
       const auto& t = T.lv[l];
@@ -285,6 +291,52 @@ gmg_status gmg_export_leaf_dofs(const gmg_hierarchy* h, int64_t* n, uint64_t* ke
       if (canonical) canonical[i] = T.leaf_canon[i];
     }
   });
+}
+
+gmg_status gmg_export_rank_level(const gmg_hierarchy* h, int level, int64_t* first_owned, int64_t* n_owned,
+                                 int64_t* n_ghost, int64_t* ghosts) {
+  return guard([&] {
+    NEED(h);
+    need_level(h, level);
+    const auto& v = h->local.lv[level];
+    if (first_owned) *first_owned = v.first_owned;
+    if (n_owned) *n_owned = v.n_owned;
+    if (n_ghost) *n_ghost = v.n_ghost;
+    if (ghosts)
+      for (gmg::i64 i = 0; i < v.n_ghost; ++i) ghosts[i] = v.ghost_global[i];
+  });
+}
+
+gmg_status gmg_nccl_get_unique_id(char id[128]) {
+  return guard([&] {
+    NEED(id);
+    gmg::nccl_unique_id(id);
+  });
+}
+
+gmg_status gmg_nccl_comm_init(const char id[128], int n_ranks, int rank, void** comm) {
+  return guard([&] {
+    NEED(id);
+    NEED(comm);
+    GMG_REQUIRE(n_ranks >= 1 && rank >= 0 && rank < n_ranks, GMG_E_INVALID_ARG, "rank / n_ranks");
+    *comm = gmg::nccl_comm_init(id, n_ranks, rank);
+  });
+}
+
+gmg_status gmg_nccl_comm_destroy(void* comm) {
+  return guard([&] { gmg::nccl_comm_destroy(comm); });
+}
+
+gmg_status gmg_local_world_create(int n_ranks, void** world) {
+  return guard([&] {
+    NEED(world);
+    GMG_REQUIRE(n_ranks >= 1 && n_ranks <= 64, GMG_E_INVALID_ARG, "n_ranks");
+    *world = new gmg::LocalWorld(n_ranks);
+  });
+}
+
+gmg_status gmg_local_world_destroy(void* world) {
+  return guard([&] { delete static_cast<gmg::LocalWorld*>(world); });
 }
 
 gmg_status gmg_export_cell_dofs(const gmg_hierarchy* h, int level, int64_t* n_cells, int64_t* dofs) {

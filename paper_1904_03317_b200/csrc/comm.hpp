@@ -1,0 +1,85 @@
+// Inter-rank communication of the level exchanges (ghost import / export-add)
+// and CG reductions ("communication ... only involves neighboring
+// processors", P:836-845 transfer ghosts).  Two transports with one interface:
+//  * NcclComm   one process per GPU, grouped ncclSend/ncclRecv + ncclAllReduce
+//               (libnccl loaded at run time: the same libnccl.so.2 torch uses)
+//  * ThreadComm all ranks in one process (one host thread + stream per rank,
+//               same device): host barriers + event-ordered D2D copies; kernels
+//               never wait on each other.  Used to test the multi-rank logic on
+//               one GPU.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
+#include "common.hpp"
+
+namespace gmg {
+
+struct Comm {
+  virtual ~Comm() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  // Exchange one contiguous chunk per peer: to peers[i] send sendbuf[soff[i], soff[i+1]),
+  // from peers[i] receive into recvbuf[roff[i], roff[i+1]).  Stream-ordered.
+  virtual void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
+                        double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) = 0;
+  // in-place sum over ranks of n doubles (device memory), stream-ordered
+  virtual void allreduce(double* buf, int n, cudaStream_t s) = 0;
+  virtual bool capturable() const = 0;   // may be captured in a CUDA graph
+};
+
+// ---------------------------------------------------------------- threads
+struct LocalWorld {
+  explicit LocalWorld(int n);
+  ~LocalWorld();
+  int n;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  void barrier();
+  struct Slot {
+    const double* sendbuf = nullptr;
+    const std::vector<int>* peers = nullptr;
+    const std::vector<i64>* soff = nullptr;
+    cudaEvent_t packed = nullptr, copied = nullptr;
+    double* red = nullptr;      // pinned host scratch for reductions
+    int device = 0;
+  };
+  std::vector<Slot> slot;
+};
+
+struct ThreadComm : Comm {
+  ThreadComm(LocalWorld* w, int r) : w(w), r(r) {}
+  LocalWorld* w;
+  int r;
+  int rank() const override { return r; }
+  int size() const override { return w->n; }
+  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
+                const std::vector<i64>& roff, cudaStream_t s) override;
+  void allreduce(double* buf, int n, cudaStream_t s) override;
+  bool capturable() const override { return false; }
+};
+
+// ---------------------------------------------------------------- NCCL
+struct NcclComm : Comm {
+  explicit NcclComm(void* comm);
+  void* comm;
+  int r = 0, n = 1;
+  int rank() const override { return r; }
+  int size() const override { return n; }
+  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
+                const std::vector<i64>& roff, cudaStream_t s) override;
+  void allreduce(double* buf, int n, cudaStream_t s) override;
+  bool capturable() const override { return true; }
+};
+
+// NCCL bootstrap helpers (dlopen'ed libnccl)
+void nccl_unique_id(char out[128]);
+void* nccl_comm_init(const char id[128], int nranks, int rank);
+void nccl_comm_destroy(void* comm);
+
+}  // namespace gmg

@@ -1,13 +1,19 @@
 // Device hierarchy and hot-path driver: V-cycle (local smoothing
 // P:413-469), Chebyshev-Jacobi smoother, leaf operator with hanging
 // nodes, GMG-preconditioned CG, eigenvalue estimate and coarse
-// solve (setup).  One process per GPU; this version runs p = 1.
+// solve (setup).  One rank per GPU (or per host thread on one GPU in the
+// local-ranks test mode); rank-local level vectors = owned DoFs + ghosts with
+// one ghost import before and one export-add after every operator that needs
+// it.  Every exchange is called by every rank in the same
+// order, independently of local sizes.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 
+#include "comm.hpp"
 #include "device.hpp"
 #include "kernels.cuh"
 
@@ -20,20 +26,27 @@ namespace gmg {
   } while (0)
 
 struct DevLevel {
-  i64 n = 0, n_pad = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
+  i64 n = 0, n_owned = 0, n_pad = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
   int* cell_dofs = nullptr;         // SoA [(k+1)^d][n_cells]
   long ldc = 0;
   double* coef = nullptr;
   unsigned char* cls = nullptr;     // bit0 = E
-  double* Dinv = nullptr;           // n_pad entries, 0 on E rows and in the padding
-  int* fam_parent = nullptr;
-  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam]
+  double* Dinv = nullptr;           // n_pad entries, 0 on E rows, ghosts and padding
+  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
   double h = 1, scale = 1;          // scale = h^(d-2)
   double lam = 0;
   std::vector<double> c1, c2;
+  // exchange plan
+  std::vector<int> peers;
+  std::vector<i64> send_off, recv_off;
+  int* send_idx = nullptr;
+  int* recv_idx = nullptr;
+  i64 n_send = 0, n_recv = 0;
+  i64 nS_global = 0;
+  std::vector<double> eig_v;
 };
 
 struct DeviceHierarchy {
@@ -41,9 +54,10 @@ struct DeviceHierarchy {
   double lo = 0.08, hi = 1.2;
   int eig_iters = 10;
   std::vector<DevLevel> lv;
-  i64 N = 0, n_leaf = 0;
+  i64 N = 0, n_leaf = 0, n0_global = 0;
   double *D = nullptr, *X = nullptr, *T = nullptr, *DV = nullptr, *W = nullptr, *Y = nullptr;
   double *cx = nullptr, *cr = nullptr, *cp = nullptr, *cq = nullptr, *cz = nullptr;
+  double *sbuf = nullptr, *rbuf = nullptr;
   unsigned char* lam_mg = nullptr;
   long long* mg_to_leaf = nullptr;
   long long* leaf_to_mg = nullptr;
@@ -51,9 +65,9 @@ struct DeviceHierarchy {
   int nred = 0;
   double* scal = nullptr;       // device scalars
   double* hscal = nullptr;      // pinned host mirror
-  int nS0 = 0;
-  int* coarse_idx = nullptr;
+  int nS0 = 0;                  // level-0 DoFs owned here (all on rank 0)
   double* coarse_inv = nullptr;
+  int* coarse_idx = nullptr;
   bool use_graph = true;
   bool xfer_warp = true;        // warp-per-family transfers (GMG_XFER=thread: thread per family)
   bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
@@ -62,6 +76,7 @@ struct DeviceHierarchy {
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
   std::vector<void*> allocs;
   int sms = 148;
+  std::unique_ptr<Comm> comm;
 
   template <class T_>
   T_* alloc(size_t n) {
@@ -94,19 +109,53 @@ struct DeviceHierarchy {
     else { constexpr int D_ = 3, K_ = 2; __VA_ARGS__; }             \
   } while (0)
 
+// ---------------------------------------------------------------- exchanges
+// ghosts <- owners (copy)
+static void import_ghosts(DeviceHierarchy* d, int l, double* vec, cudaStream_t s) {
+  if (!d->comm) return;
+  DevLevel& v = d->lv[l];
+  if (v.n_send) {
+    dev::pack<<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, d->sbuf);
+    d->launches++;
+  }
+  d->comm->exchange(v.peers, d->sbuf, v.send_off, d->rbuf, v.recv_off, s);
+  if (v.n_recv) {
+    dev::unpack_set<<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, d->rbuf, vec);
+    d->launches++;
+  }
+}
+// owners += ghosts; ghosts := 0
+static void export_add(DeviceHierarchy* d, int l, double* vec, cudaStream_t s) {
+  if (!d->comm) return;
+  DevLevel& v = d->lv[l];
+  if (v.n_recv) {
+    dev::pack_zero<<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, d->sbuf);
+    d->launches++;
+  }
+  d->comm->exchange(v.peers, d->sbuf, v.recv_off, d->rbuf, v.send_off, s);
+  if (v.n_send) {
+    dev::unpack_add<<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, d->rbuf, vec);
+    d->launches++;
+  }
+}
+static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
+  if (d->comm) d->comm->allreduce(buf, n, s);
+}
+
 // ---------------------------------------------------------------- primitives
-// y += K_l x over a cell list (leaf cells) or, list == nullptr, over all of C_l.
-// Full levels >= 1 run family-blocked (y must be zero on entry: patch-interior
-// nodes are stored, not added); level 0 and cell lists run thread-per-cell.
+// y += K_l x over a cell list (leaf cells) or, list == nullptr, over all local
+// cells.  Full levels >= 1 run family-blocked (y must be zero on entry:
+// patch-interior nodes are stored, not added); level 0 and cell lists run
+// thread-per-cell.
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
   if (list == nullptr && l > 0 && v.n_fam > 0 && v.coef == nullptr && d->tensor_apply) {
-    const int row = (int)(d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) + (d->k + 1) * (d->k + 1) * (d->k + 1)
-                                      : (2 * d->k + 1) * (2 * d->k + 1) + (d->k + 1) * (d->k + 1));
+    const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
+    const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
     int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
     DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
-                                  (int)v.n_fam, v.xfer, row, v.scale, x, y)));
+                                  (int)v.n_fam, v.xfer, np + nn, v.scale, x, y)));
   } else if (list == nullptr && l > 0 && v.n_fam > 0) {
     DISPATCH_DK(d->dim, d->k, {
       constexpr int FPB = dev::FamCfg<D_, K_>::FPB;
@@ -122,23 +171,21 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const dou
   d->launches++;
 }
 
+// t = K_l x on owned rows: ghost import of x, local family apply, export-add of t
+static void apply_full(DeviceHierarchy* d, int l, double* x, double* t, cudaStream_t s) {
+  import_ghosts(d, l, x, s);
+  k_apply(d, l, nullptr, d->lv[l].n_cells, x, t, s);
+  export_add(d, l, t, s);
+}
+
 template <int MODE>
 static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const double* vin, double* t, double* dc,
                        cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  DevLevel& c = d->lv[l - 1];
-  if (d->xfer_warp) {
-    int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
-    DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
-                                  (int)nf, list, f.xfer, f.cls, vin, t, dc)));
-    d->launches++;
-    return;
-  }
-  int grid = (int)((nf + dev::XFER_NT - 1) / dev::XFER_NT);
-  DISPATCH_DK(d->dim, d->k,
-              (dev::fam_restrict<D_, K_, MODE><<<grid, dev::XFER_NT, 0, s>>>(
-                  (int)nf, (int)f.n_fam, list, f.fam_parent, f.fam_dofs, c.cell_dofs, c.ldc, f.cls, vin, t, dc)));
+  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                                (int)nf, list, f.xfer, f.cls, vin, t, dc)));
   d->launches++;
 }
 
@@ -147,24 +194,16 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
                          cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  DevLevel& c = d->lv[l - 1];
-  if (d->xfer_warp) {
-    int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
-    DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
-                                  (int)nf, list, f.xfer, f.cls, xc, xf)));
-    d->launches++;
-    return;
-  }
-  int grid = (int)((nf + dev::XFER_NT - 1) / dev::XFER_NT);
-  DISPATCH_DK(d->dim, d->k,
-              (dev::fam_prolongate<D_, K_, MODE><<<grid, dev::XFER_NT, 0, s>>>(
-                  (int)nf, (int)f.n_fam, list, f.fam_parent, f.fam_dofs, c.cell_dofs, c.ldc, f.cls, xc, xf)));
+  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+                                (int)nf, list, f.xfer, f.cls, xc, xf)));
   d->launches++;
 }
 
 template <bool RT, bool RDV, bool WDV, bool XZ>
 static void k_cheb(DeviceHierarchy* d, DevLevel& v, const double* g, double* t, double* dv, double* x, double c1,
                    double c2, cudaStream_t s) {
+  if (v.n_pad == 0) return;
   // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
   dev::cheb_step<RT, RDV, WDV, XZ><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
       (const double2*)g, (const double2*)v.Dinv, (double2*)t, (double2*)dv, (double2*)x, c1, c2);
@@ -173,21 +212,20 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const double* g, double* t, 
 
 // Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
 // first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
-// x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows keeps x^E fixed).
+// x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows and ghosts keeps those entries fixed).
 static void smooth(DeviceHierarchy* d, int l, const double* g, double* x, double* t, double* dv, bool x_zero,
                    cudaStream_t s) {
   DevLevel& v = d->lv[l];
-  if (v.n == 0) return;
   const int m = d->m;
   if (x_zero) {
     k_cheb<false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else {
-    k_apply(d, l, nullptr, v.n_cells, x, t, s);
+    apply_full(d, l, x, t, s);
     if (m == 1) k_cheb<true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
     else k_cheb<true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   }
   for (int j = 1; j < m; ++j) {
-    k_apply(d, l, nullptr, v.n_cells, x, t, s);
+    apply_full(d, l, x, t, s);
     if (j == m - 1) k_cheb<true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
     else k_cheb<true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
   }
@@ -205,15 +243,19 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
   for (int l = L; l >= 1; --l) {
     DevLevel& v = d->lv[l];
     double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
+    double* gc = d->D + d->lv[l - 1].off;
     smooth(d, l, g, x, t, dv, true, s);                                     // 1: pre-smooth from 0
-    k_apply(d, l, nullptr, v.n_cells, x, t, s);                             // 2: t = K x
-    k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, d->D + d->lv[l - 1].off, s);  // 3: d_{l-1} += P^T (d - t)
+    apply_full(d, l, x, t, s);                                              // 2: t = K x
+    k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
+    export_add(d, l - 1, gc, s);
   }
-  coarse(d, d->D + d->lv[0].off, d->X + d->lv[0].off, s);                   // 4: coarse solve
+  coarse(d, d->D + d->lv[0].off, d->X + d->lv[0].off, s);                   // 4: coarse solve (rank 0)
   for (int l = 1; l <= L; ++l) {
     DevLevel& v = d->lv[l];
     double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
-    k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, d->X + d->lv[l - 1].off, x, s);  // 5
+    double* xc = d->X + d->lv[l - 1].off;
+    import_ghosts(d, l - 1, xc, s);
+    k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, xc, x, s);         // 5: x += P x_{l-1}
     smooth(d, l, g, x, t, dv, false, s);                                    // 6: post-smooth
   }
 }
@@ -243,24 +285,35 @@ static void leaf_apply_mg(DeviceHierarchy* d, const double* p, double* q, double
   const int L = d->L;
   long long before = d->launches;
   CK(cudaMemcpyAsync(d->W, p, d->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  for (int l = 1; l <= L; ++l)
+  for (int l = 1; l <= L; ++l) {
+    import_ghosts(d, l - 1, d->W + d->lv[l - 1].off, s);
     k_prolongate<dev::XFER_SET_E>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->W + d->lv[l - 1].off,
                                   d->W + d->lv[l].off, s);
+  }
+  import_ghosts(d, L, d->W + d->lv[L].off, s);
   CK(cudaMemsetAsync(d->Y, 0, d->N * sizeof(double), s));
   for (int l = 0; l <= L; ++l)
     k_apply(d, l, d->lv[l].leaf_cells, d->lv[l].n_leaf, d->W + d->lv[l].off, d->Y + d->lv[l].off, s);
-  for (int l = L; l >= 1; --l)
+  for (int l = L; l >= 1; --l) {
+    export_add(d, l, d->Y + d->lv[l].off, s);
     k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
                                d->Y + d->lv[l - 1].off, s);
+  }
+  export_add(d, 0, d->Y + d->lv[0].off, s);
   dev::mask_dot<<<d->nred, dev::RED_NT, 0, s>>>(d->N, d->lam_mg, d->Y, p, q, partial);
   d->launches++;
   d->per_leaf_apply = d->launches - before;
 }
 
 static double host_dot(DeviceHierarchy* d, i64 n, const double* a, const double* b, cudaStream_t s) {
-  dev::dot_partial<<<d->nred, dev::RED_NT, 0, s>>>(n, a, b, d->partial);
-  dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 7);
-  d->launches += 2;
+  if (n > 0) {
+    dev::dot_partial<<<d->nred, dev::RED_NT, 0, s>>>(n, a, b, d->partial);
+    dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 7);
+    d->launches += 2;
+  } else {
+    CK(cudaMemsetAsync(d->scal + 7, 0, sizeof(double), s));
+  }
+  allreduce(d, d->scal + 7, 1, s);
   CK(cudaMemcpyAsync(d->hscal + 7, d->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return d->hscal[7];
@@ -324,40 +377,48 @@ static double tridiag_max_eig(const std::vector<double>& a, const std::vector<do
 // CG (Jacobi preconditioned) on A^S x = v, v = (-5.5, ..., 5.5, -5.5, ...)
 // over the S DoFs in canonical order, min(eig_iters, n_S) iterations, Lanczos
 // tridiagonal from the CG coefficients, lambda = its largest eigenvalue.
-static double eigen_estimate(DeviceHierarchy* d, int l, const std::vector<double>& v_host, i64 nS,
-                             cudaStream_t s) {
+// Collective over ranks (global dots, same control flow everywhere).
+static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
   DevLevel& v = d->lv[l];
   const i64 n = v.n;
-  if (nS == 0 || n == 0) return 0.0;
+  if (v.nS_global == 0) return 0.0;
   double *r = d->X + v.off, *z = d->DV + v.off, *p = d->W + v.off, *q = d->Y + v.off;
-  CK(cudaMemcpyAsync(r, v_host.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
   const int gr = (int)((n + 255) / 256);
-  dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
-  CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  d->launches++;
+  if (n > 0) {
+    CK(cudaMemcpyAsync(r, v.eig_v.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+    dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
+    CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    d->launches++;
+  }
   double rz = host_dot(d, n, r, z, s);
   double r0 = std::sqrt(host_dot(d, n, r, r, s));
   std::vector<double> alphas, betas;
   if (rz == 0.0 || r0 == 0.0) return 0.0;
-  const int maxit = (int)std::min<i64>(d->eig_iters, nS);
+  const int maxit = (int)std::min<i64>(d->eig_iters, v.nS_global);
   for (int it = 0; it < maxit; ++it) {
-    CK(cudaMemsetAsync(q, 0, n * sizeof(double), s));
-    k_apply(d, l, nullptr, v.n_cells, p, q, s);
+    if (n > 0) CK(cudaMemsetAsync(q, 0, n * sizeof(double), s));
+    apply_full(d, l, p, q, s);
     double pq = host_dot(d, n, p, q, s);
     double alpha = rz / pq;
     alphas.push_back(alpha);
-    dev::eig_update_r<<<gr, 256, 0, s>>>(n, alpha, v.cls, q, r);
-    d->launches++;
+    if (n > 0) {
+      dev::eig_update_r<<<gr, 256, 0, s>>>(n, alpha, v.cls, q, r);
+      d->launches++;
+    }
     if (it == maxit - 1) break;
-    dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
-    d->launches++;
+    if (n > 0) {
+      dev::eig_z<<<gr, 256, 0, s>>>(n, v.Dinv, r, z);
+      d->launches++;
+    }
     double rz_new = host_dot(d, n, r, z, s);
     double rn = std::sqrt(host_dot(d, n, r, r, s));
     if (rn <= 1e-10 * r0 || rz_new == 0.0) break;
     double beta = rz_new / rz;
     betas.push_back(beta);
-    dev::axpby<<<gr, 256, 0, s>>>(n, 1.0, z, beta, p);
-    d->launches++;
+    if (n > 0) {
+      dev::axpby<<<gr, 256, 0, s>>>(n, 1.0, z, beta, p);
+      d->launches++;
+    }
     rz = rz_new;
   }
   const int m = (int)alphas.size();
@@ -370,14 +431,15 @@ static double eigen_estimate(DeviceHierarchy* d, int l, const std::vector<double
 }
 
 // ---------------------------------------------------------------- creation
-DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const std::vector<double>& coef_flat,
-                               const std::vector<i64>& coef_off) {
+DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::unique_ptr<Comm> comm,
+                               i64 n0_global) {
   auto* d = new DeviceHierarchy();
   try {
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
     CK(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, dev_id));
+    d->comm = std::move(comm);
     d->dim = Tp.dim;
     d->k = Tp.k;
     d->L = Tp.L;
@@ -385,23 +447,26 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
     d->lo = prm.cheb_lo;
     d->hi = prm.cheb_hi;
     d->eig_iters = prm.eig_iters;
-    d->use_graph = !(prm.flags & GMG_NO_GRAPH);
-    if (const char* e = std::getenv("GMG_XFER")) d->xfer_warp = std::string(e) != "thread";
+    d->n0_global = n0_global;
+    d->use_graph = !(prm.flags & GMG_NO_GRAPH) && (!d->comm || d->comm->capturable());
     if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
     const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
     d->lv.resize(Tp.L + 1);
-    i64 off = 0;
+    i64 off = 0, xmax = 1;
     for (int l = 0; l <= Tp.L; ++l) {
-      const LevelTopo& t = Tp.lv[l];
+      const LocalLevel& t = Tp.lv[l];
       DevLevel& v = d->lv[l];
-      v.n = t.n_dofs;
+      v.n = t.n_local();
+      v.n_owned = t.n_owned;
       v.n_pad = (v.n + dev::VEC_PAD - 1) / dev::VEC_PAD * dev::VEC_PAD;   // zero padding
       v.n_cells = t.n_cells;
       v.n_fam = t.n_fam;
       v.n_leaf = (i64)t.leaf_cells.size();
       v.n_edge = (i64)t.edge_fams.size();
+      v.nS_global = t.nS_global;
+      v.eig_v = t.eig_v;
       v.off = off;
       off += v.n_pad;
       v.ldc = (long)t.n_cells;
@@ -409,10 +474,9 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
       for (i64 c = 0; c < t.n_cells; ++c)
         for (int b = 0; b < nn; ++b) soa[(size_t)b * t.n_cells + c] = t.cell_dofs[(size_t)c * nn + b];
       v.cell_dofs = d->upload(soa);
-      std::vector<unsigned char> cls(t.n_dofs);
-      for (i64 i = 0; i < t.n_dofs; ++i) cls[i] = t.dof_cls[i] == CLS_E ? 1 : 0;
+      std::vector<unsigned char> cls(v.n);
+      for (i64 i = 0; i < v.n; ++i) cls[i] = t.cls[i] == CLS_E ? 1 : 0;
       v.cls = d->upload(cls);
-      v.fam_parent = d->upload(t.fam_parent);
       {
         // patch table AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
         const size_t np = t.n_fam ? t.fam_dofs.size() / (size_t)t.n_fam : 0;
@@ -420,54 +484,42 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
         for (size_t f = 0; f < (size_t)t.n_fam; ++f)
           for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.fam_dofs[f * np + a];
         v.fam_dofs = d->upload(fs);
-        if (l > 0 && t.n_fam > 0) {
-          const size_t row = np + nn;
-          const LevelTopo& tc = Tp.lv[l - 1];
-          std::vector<int> xf((size_t)t.n_fam * row);
-          for (size_t f = 0; f < (size_t)t.n_fam; ++f) {
-            for (size_t a = 0; a < np; ++a) xf[f * row + a] = t.fam_dofs[f * np + a];
-            for (int j = 0; j < nn; ++j) xf[f * row + np + j] = tc.cell_dofs[(size_t)t.fam_parent[f] * nn + j];
-          }
-          v.xfer = d->upload(xf);
-        }
+        v.xfer = d->upload(t.xfer);
       }
       v.leaf_cells = d->upload(t.leaf_cells);
       v.edge_fams = d->upload(t.edge_fams);
       v.h = std::ldexp(1.0, -l);
       v.scale = Tp.dim == 3 ? v.h : 1.0;
-      if (!coef_off.empty()) {
-        std::vector<double> cc(coef_flat.begin() + coef_off[l], coef_flat.begin() + coef_off[l + 1]);
-        v.coef = d->upload(cc);
-      }
       v.Dinv = d->alloc<double>(v.n_pad);
       CK(cudaMemset(v.Dinv, 0, v.n_pad * sizeof(double)));
+      v.peers = t.peers;
+      v.send_off = t.send_off;
+      v.recv_off = t.recv_off;
+      v.n_send = (i64)t.send_idx.size();
+      v.n_recv = (i64)t.recv_idx.size();
+      v.send_idx = d->upload(t.send_idx);
+      v.recv_idx = d->upload(t.recv_idx);
+      xmax = std::max(xmax, std::max(v.n_send, v.n_recv));
     }
     d->N = off;
     const i64 N = d->N;
-    d->D = d->alloc<double>(N);
-    d->X = d->alloc<double>(N);
-    d->T = d->alloc<double>(N);
-    d->DV = d->alloc<double>(N);
-    d->W = d->alloc<double>(N);
-    d->Y = d->alloc<double>(N);
-    d->cx = d->alloc<double>(N);
-    d->cr = d->alloc<double>(N);
-    d->cp = d->alloc<double>(N);
-    d->cq = d->alloc<double>(N);
-    d->cz = d->alloc<double>(N);
-    for (double* p : {d->D, d->X, d->T, d->DV, d->W, d->Y, d->cx, d->cr, d->cp, d->cq, d->cz})
-      CK(cudaMemset(p, 0, N * sizeof(double)));
-    // lambda mask and leaf <-> MG maps
+    for (double** p : {&d->D, &d->X, &d->T, &d->DV, &d->W, &d->Y, &d->cx, &d->cr, &d->cp, &d->cq, &d->cz}) {
+      *p = d->alloc<double>(N);
+      CK(cudaMemset(*p, 0, N * sizeof(double)));
+    }
+    d->sbuf = d->alloc<double>(xmax);
+    d->rbuf = d->alloc<double>(xmax);
+    // lambda mask and leaf <-> MG maps (owned leaf DoFs of this rank)
     std::vector<unsigned char> lam(N, 0);
-    std::vector<long long> m2l(N, -1), l2m(Tp.n_leaf);
+    std::vector<long long> m2l(N, -1), l2m(Tp.n_leaf_owned);
     for (int l = 0; l <= Tp.L; ++l)
-      for (i64 i = 0; i < Tp.lv[l].n_dofs; ++i) lam[d->lv[l].off + i] = Tp.lv[l].dof_lam[i];
-    for (i64 g = 0; g < Tp.n_leaf; ++g) {
-      i64 m = d->lv[Tp.leaf_lambda[g]].off + Tp.leaf_level_index[g];
+      for (i64 i = 0; i < Tp.lv[l].n_local(); ++i) lam[d->lv[l].off + i] = Tp.lv[l].lam[i];
+    for (i64 g = 0; g < Tp.n_leaf_owned; ++g) {
+      i64 m = d->lv[Tp.leaf_level[g]].off + Tp.leaf_local[g];
       l2m[g] = m;
       m2l[m] = g;
     }
-    d->n_leaf = Tp.n_leaf;
+    d->n_leaf = Tp.n_leaf_owned;
     d->lam_mg = d->upload(lam);
     d->mg_to_leaf = d->upload(m2l);
     d->leaf_to_mg = d->upload(l2m);
@@ -477,43 +529,50 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
     CK(cudaMemset(d->scal, 0, 16 * sizeof(double)));
     CK(cudaMallocHost(&d->hscal, 16 * sizeof(double)));
     cudaStream_t s = d->cap;
-    // diagonal and D^-1 (S rows), zero-diagonal check
+    // diagonal and D^-1 on owned S rows (ghost contributions added to owners)
     int* bad = d->alloc<int>(1);
     CK(cudaMemset(bad, 0, sizeof(int)));
     for (int l = 0; l <= Tp.L; ++l) {
       DevLevel& v = d->lv[l];
-      if (v.n == 0) continue;
-      CK(cudaMemsetAsync(v.Dinv, 0, v.n * sizeof(double), s));
-      int grid = (int)((v.n_cells + 127) / 128);
-      DISPATCH_DK(d->dim, d->k,
-                  (dev::cell_diag<D_, K_><<<grid, 128, 0, s>>>((int)v.n_cells, v.cell_dofs, v.ldc, v.coef, v.scale,
-                                                               v.Dinv)));
-      dev::invert_diag<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.cls, v.Dinv, bad);
-      d->launches += 2;
+      if (v.n_cells > 0) {
+        int grid = (int)((v.n_cells + 127) / 128);
+        DISPATCH_DK(d->dim, d->k,
+                    (dev::cell_diag<D_, K_><<<grid, 128, 0, s>>>((int)v.n_cells, v.cell_dofs, v.ldc, v.coef, v.scale,
+                                                                 v.Dinv)));
+        d->launches++;
+      }
+      export_add(d, l, v.Dinv, s);
+      if (v.n_owned > 0) {
+        dev::invert_diag<<<(int)((v.n_owned + 255) / 256), 256, 0, s>>>(v.n_owned, v.cls, v.Dinv, bad);
+        d->launches++;
+      }
     }
     int hbad = 0;
     CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     GMG_REQUIRE(hbad == 0, GMG_E_ZERO_DIAG, "zero or negative diagonal on an S row");
-    // coarse matrix A_0^S: columns by applying K_0 to unit vectors; dense Cholesky
+    // coarse matrix A_0^S (all level-0 DoFs owned by rank 0): columns by a
+    // collective apply of K_0 to unit vectors; dense Cholesky on rank 0
     {
       DevLevel& v0 = d->lv[0];
-      const int n0 = (int)v0.n;
-      d->nS0 = n0;
-      if (n0 > 0) {
-        GMG_REQUIRE(n0 <= 4096, GMG_E_INVALID_ARG, "coarse level too large for the dense solver");
-        std::vector<double> A((size_t)n0 * n0), e(n0);
-        double *xe = d->X + v0.off, *ye = d->Y + v0.off;
-        for (int j = 0; j < n0; ++j) {
-          std::fill(e.begin(), e.end(), 0.0);
-          e[j] = 1.0;
-          CK(cudaMemcpyAsync(xe, e.data(), n0 * sizeof(double), cudaMemcpyHostToDevice, s));
-          CK(cudaMemsetAsync(ye, 0, n0 * sizeof(double), s));
-          k_apply(d, 0, nullptr, v0.n_cells, xe, ye, s);
-          CK(cudaMemcpyAsync(A.data() + (size_t)j * n0, ye, n0 * sizeof(double), cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
+      const int n0 = (int)n0_global;
+      d->nS0 = (int)v0.n_owned;
+      GMG_REQUIRE(n0 <= 4096, GMG_E_INVALID_ARG, "coarse level too large for the dense solver");
+      std::vector<double> A((size_t)n0 * n0), e(std::max<i64>(v0.n, 1));
+      double *xe = d->X + v0.off, *ye = d->Y + v0.off;
+      for (int j = 0; j < n0; ++j) {
+        std::fill(e.begin(), e.end(), 0.0);
+        if (d->nS0 > 0) e[j] = 1.0;
+        if (v0.n > 0) {
+          CK(cudaMemcpyAsync(xe, e.data(), v0.n * sizeof(double), cudaMemcpyHostToDevice, s));
+          CK(cudaMemsetAsync(ye, 0, v0.n * sizeof(double), s));
         }
-        // Cholesky A = L L^T, then inverse
+        apply_full(d, 0, xe, ye, s);
+        if (d->nS0 > 0)
+          CK(cudaMemcpyAsync(A.data() + (size_t)j * n0, ye, n0 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      }
+      if (d->nS0 > 0) {
         std::vector<double> Lm((size_t)n0 * n0, 0.0);
         for (int i = 0; i < n0; ++i)
           for (int j = 0; j <= i; ++j) {
@@ -547,16 +606,9 @@ DeviceHierarchy* device_create(const Topology& Tp, const gmg_params& prm, const 
         d->coarse_inv = d->upload(inv);
       }
     }
-    // eigenvalue estimates (levels >= 1)
+    // eigenvalue estimates (levels >= 1), collective
     for (int l = 1; l <= Tp.L; ++l) {
-      const LevelTopo& t = Tp.lv[l];
-      std::vector<double> vv(t.n_dofs, 0.0);
-      i64 cs = 0;
-      for (i64 c = 0; c < t.n_dofs; ++c) {
-        i64 g = t.canon_to_global[c];
-        if (t.dof_cls[g] == CLS_S) vv[g] = -5.5 + (double)(cs++ % 12);
-      }
-      d->lv[l].lam = eigen_estimate(d, l, vv, cs, s);
+      d->lv[l].lam = eigen_estimate(d, l, s);
       set_cheb(d, l);
     }
     // restore the work buffers to zero (T must be zero between applies)
@@ -587,9 +639,17 @@ void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream)
   dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);            // copy_to_mg
   d->launches++;
   run_vcycle_mg(d, s);
-  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);  // copy_from_mg
-  d->launches++;
+  if (d->n_leaf) {
+    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);  // copy_from_mg
+    d->launches++;
+  }
   CK(cudaPeekAtLastError());
+}
+
+static void global_dot_into(DeviceHierarchy* d, int slot, cudaStream_t s) {
+  dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + slot);
+  d->launches++;
+  allreduce(d, d->scal + slot, 1, s);
 }
 
 int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol, int max_it, int* iters,
@@ -601,8 +661,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
   dev::gather_to_mg<<<gr, 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
   CK(cudaMemsetAsync(d->cx, 0, N * sizeof(double), s));
   d->launches++;
-  double nb2 = host_dot(d, N, d->cr, d->cr, s);
-  double nb = std::sqrt(nb2);
+  double nb = std::sqrt(host_dot(d, N, d->cr, d->cr, s));
   int it = 0;
   double rel = nb > 0 ? 1.0 : 0.0;
   int status = 0;
@@ -611,16 +670,16 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
     CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     run_vcycle_mg(d, s);
     dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
-    dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 0);
+    d->launches++;
+    global_dot_into(d, 0, s);
     CK(cudaMemcpyAsync(d->cp, d->cz, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    d->launches += 2;
     status = 1;
     for (it = 1; it <= max_it; ++it) {
       leaf_apply_mg(d, d->cp, d->cq, d->partial, s);                           // q = A p, (p,q)
-      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 1);
+      global_dot_into(d, 1, s);
       dev::cg_update_xr<<<d->nred, dev::RED_NT, 0, s>>>(N, d->scal, d->cp, d->cq, d->cx, d->cr, d->partial);
-      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 3);
-      d->launches += 3;
+      d->launches++;
+      global_dot_into(d, 3, s);
       CK(cudaMemcpyAsync(d->hscal + 3, d->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       rel = std::sqrt(d->hscal[3]) / nb;
@@ -632,15 +691,18 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
       CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
       run_vcycle_mg(d, s);                                                      // z = V(r)
       dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
-      dev::reduce_final<<<1, dev::RED_NT, 0, s>>>(d->nred, d->partial, d->scal + 2);
+      d->launches++;
+      global_dot_into(d, 2, s);
       dev::cg_update_p<<<gr, 256, 0, s>>>(N, d->scal, d->cz, d->cp);            // p = z + beta p
       dev::copy_scalar<<<1, 1, 0, s>>>(d->scal + 2, d->scal + 0);
-      d->launches += 4;
+      d->launches += 2;
     }
     if (it > max_it) it = max_it;
   }
-  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
-  d->launches++;
+  if (d->n_leaf) {
+    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
+    d->launches++;
+  }
   CK(cudaPeekAtLastError());
   if (iters) *iters = it;
   if (rel_res) *rel_res = rel;
@@ -659,34 +721,47 @@ void device_rhs_constant(DeviceHierarchy* d, double f, double* b, void* stream) 
                                                                             v.ldc, fh, d->Y + v.off)));
     d->launches++;
   }
-  for (int l = d->L; l >= 1; --l)
+  for (int l = d->L; l >= 1; --l) {
+    export_add(d, l, d->Y + d->lv[l].off, s);
     k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
                                d->Y + d->lv[l - 1].off, s);
-  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
-  d->launches++;
+  }
+  export_add(d, 0, d->Y + d->lv[0].off, s);
+  if (d->n_leaf) {
+    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
+    d->launches++;
+  }
   CK(cudaPeekAtLastError());
 }
 
+static void need_single(const DeviceHierarchy* d) {
+  GMG_REQUIRE(!d->comm, GMG_E_STATE, "single-operator entry points are defined for n_ranks == 1");
+}
+
 void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
+  need_single(d);
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
-  CK(cudaMemsetAsync(y, 0, v.n * sizeof(double), s));
+  if (v.n) CK(cudaMemsetAsync(y, 0, v.n * sizeof(double), s));
   k_apply(d, l, nullptr, v.n_cells, x, y, s);
   CK(cudaPeekAtLastError());
 }
 
 void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
+  need_single(d);
   DevLevel& v = d->lv[l];
   k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
 
 void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
+  need_single(d);
   k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
 
 void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, void* stream) {
+  need_single(d);
   k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, xc, xf, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
@@ -697,12 +772,15 @@ void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* str
   dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
   d->launches++;
   leaf_apply_mg(d, d->cp, d->cq, d->partial, s);
-  dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
-  d->launches++;
+  if (d->n_leaf) {
+    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
+    d->launches++;
+  }
   CK(cudaPeekAtLastError());
 }
 
 void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, int x_zero, void* stream) {
+  need_single(d);
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   GMG_REQUIRE(l >= 1, GMG_E_INVALID_ARG, "no smoother on level 0");
@@ -719,6 +797,7 @@ void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, 
 }
 
 void device_level_diagonal(DeviceHierarchy* d, int l, double* diag, void* stream) {
+  need_single(d);
   DevLevel& v = d->lv[l];
   if (v.n == 0) return;
   dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v.n, v.cls, v.Dinv, diag);

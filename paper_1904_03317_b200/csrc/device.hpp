@@ -1,13 +1,17 @@
 // Device hierarchy interface (host C++ side; no CUDA types).
 #pragma once
+#include <memory>
+
 #include "forest.hpp"
 
 namespace gmg {
 
 struct DeviceHierarchy;
+struct Comm;
 
-DeviceHierarchy* device_create(const Topology& T, const gmg_params& prm, const std::vector<double>& coef_cells_flat,
-                               const std::vector<i64>& coef_offsets);
+// comm: nullptr for a single rank; n0_global: number of level-0 DoFs (all owned by rank 0)
+DeviceHierarchy* device_create(const LocalTopo& T, const gmg_params& prm, std::unique_ptr<Comm> comm,
+                               i64 n0_global);
 void device_destroy(DeviceHierarchy* d);
 
 void device_vcycle(DeviceHierarchy* d, const double* b_leaf, double* x_leaf, void* stream);

@@ -105,4 +105,41 @@ struct Topology {
 
 Topology make_topology(const Forest& f, const Partition& p, int k);
 
+// ------------------------------------------------------------------ rank-local view
+// Rank r computes the families whose parent it owns (first-child rule) and the
+// level-0 cells it owns.  Its level vector = owned DoFs (a contiguous range of
+// the global order) followed by ghost DoFs (owned elsewhere, needed by its
+// families' patches or by the parents of its next-finer families), sorted by
+// global index.  One exchange plan per level serves both directions:
+//   import     owner -> ghost copies   (send_idx owned values, recv_idx ghosts)
+//   export-add ghost -> owner, added    (reverse direction)
+struct LocalLevel {
+  int level = 0;
+  i64 n_owned = 0, n_ghost = 0, first_owned = 0;
+  std::vector<i64> ghost_global;           // sorted
+  std::vector<int> peers;                  // ranks exchanged with (sorted)
+  std::vector<i64> send_off, recv_off;     // [peers + 1]
+  std::vector<i32> send_idx;               // local owned indices, grouped by peer
+  std::vector<i32> recv_idx;               // local ghost indices, grouped by peer
+  i64 n_cells = 0, n_fam = 0;
+  std::vector<i32> cell_dofs;              // [n_cells][(k+1)^d] local index or -1
+  std::vector<i32> fam_dofs;               // [n_fam][(2k+1)^d] local, transfer-owner encoding
+  std::vector<i32> xfer;                   // [n_fam][(2k+1)^d + (k+1)^d] fine | parent (level l-1 local)
+  std::vector<i32> leaf_cells, edge_fams;
+  std::vector<uint8_t> cls, lam;           // per local DoF (ghosts: lam = 0)
+  std::vector<double> eig_v;               // eigen start vector on owned S DoFs
+  i64 nS_global = 0;
+  i64 n_local() const { return n_owned + n_ghost; }
+};
+
+struct LocalTopo {
+  int rank = 0, n_ranks = 1, dim = 2, k = 2, L = 0;
+  std::vector<LocalLevel> lv;
+  i64 n_leaf_owned = 0, leaf_first = 0, n_leaf_global = 0;
+  std::vector<int8_t> leaf_level;          // per owned leaf DoF
+  std::vector<i64> leaf_local;             // local index at its level
+};
+
+LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank);
+
 }  // namespace gmg

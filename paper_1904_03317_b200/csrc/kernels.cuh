@@ -610,95 +610,28 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
   }
 }
 
-// tensor weight of fine patch node a and coarse node j (compile-time after unrolling)
-template <int D, int K>
-__host__ __device__ __forceinline__ constexpr double pweight(int a, int j) {
-  constexpr int NP1 = 2 * K + 1, N = K + 1;
-  double w = 1.0;
-  for (int d = 0; d < D; ++d) {
-    w *= Q<K>::P(a % NP1, j % N);
-    a /= NP1;
-    j /= N;
-  }
-  return w;
+// ------------------------------------------------------------- ghost exchange
+__global__ void pack(long n, const int* __restrict__ idx, const double* __restrict__ v, double* __restrict__ buf) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) buf[i] = v[idx[i]];
 }
-
-// Thread per family (family list optional): the patch loops are unrolled with
-// compile-time weights, so each thread keeps (k+1)^d coarse values in registers
-// and issues its (2k+1)^d patch loads independently (no dependent warp phases).
-// fam_dofs is SoA [(2k+1)^d][nfam_all].
-template <int D, int K, int MODE>
-__global__ void __launch_bounds__(XFER_NT)
-fam_prolongate(int nfam, int nfam_all, const int* __restrict__ fam_list, const int* __restrict__ fam_parent,
-               const int* __restrict__ fam_dofs, const int* __restrict__ cdofs_coarse, long ldc_coarse,
-               const unsigned char* __restrict__ cls_fine, const double* __restrict__ xc, double* __restrict__ xf) {
-  constexpr int NC = Shape<D, K>::NN, NP = Shape<D, K>::NP;
-  const int t = blockIdx.x * XFER_NT + threadIdx.x;
-  if (t >= nfam) return;
-  const int f = fam_list ? __ldg(fam_list + t) : t;
-  const int p = __ldg(fam_parent + f);
-  double c[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const int i = __ldg(cdofs_coarse + (long)j * ldc_coarse + p);
-    c[j] = i >= 0 ? __ldg(xc + i) : 0.0;
-  }
-#pragma unroll
-  for (int a = 0; a < NP; ++a) {
-    const int v = __ldg(fam_dofs + (long)a * nfam_all + f);
-    if (v < 0) continue;                                     // not owned / Dirichlet
-    if (MODE == XFER_SET_E && !(cls_fine[v] & 1)) continue;
-    double val = 0.0;
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const double w = pweight<D, K>(a, j);
-      if (w != 0.0) val = fma(w, c[j], val);
-    }
-    if (MODE == XFER_SET_E) xf[v] = val;
-    else xf[v] += val;
+// ghosts -> buffer, ghost entries reset (data-dependent, see cheb_step)
+__global__ void pack_zero(long n, const int* __restrict__ idx, double* __restrict__ v, double* __restrict__ buf) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double a = v[idx[i]];
+    buf[i] = a;
+    v[idx[i]] = a - a;
   }
 }
-
-// d_c += P^T r with r = (MODE == RES_VCYCLE ? d - t (and t := 0) : v) on owned fine nodes
-template <int D, int K, int MODE>
-__global__ void __launch_bounds__(XFER_NT)
-fam_restrict(int nfam, int nfam_all, const int* __restrict__ fam_list, const int* __restrict__ fam_parent,
-             const int* __restrict__ fam_dofs, const int* __restrict__ cdofs_coarse, long ldc_coarse,
-             const unsigned char* __restrict__ cls_fine, const double* __restrict__ v, double* __restrict__ t,
-             double* __restrict__ dc) {
-  constexpr int NC = Shape<D, K>::NN, NP = Shape<D, K>::NP;
-  const int tt = blockIdx.x * XFER_NT + threadIdx.x;
-  if (tt >= nfam) return;
-  const int f = fam_list ? __ldg(fam_list + tt) : tt;
-  double acc[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) acc[j] = 0.0;
-#pragma unroll
-  for (int a = 0; a < NP; ++a) {
-    const int i = __ldg(fam_dofs + (long)a * nfam_all + f);
-    if (i < 0) continue;
-    double r;
-    if (MODE == RES_VCYCLE) {
-      const double tv = t[i];
-      r = v[i] - tv;
-      t[i] = tv - tv;                         // data-dependent reset (see cheb_step)
-    } else if (MODE == RES_EONLY) {
-      r = (cls_fine[i] & 1) ? v[i] : 0.0;
-    } else {
-      r = v[i];
-    }
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const double w = pweight<D, K>(a, j);
-      if (w != 0.0) acc[j] = fma(w, r, acc[j]);
-    }
-  }
-  const int p = __ldg(fam_parent + f);
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const int ci = __ldg(cdofs_coarse + (long)j * ldc_coarse + p);
-    if (ci >= 0) atomicAdd(dc + ci, acc[j]);
-  }
+__global__ void unpack_set(long n, const int* __restrict__ idx, const double* __restrict__ buf, double* __restrict__ v) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[idx[i]] = buf[i];
+}
+// an owned DoF may be a ghost of several peers: atomic add
+__global__ void unpack_add(long n, const int* __restrict__ idx, const double* __restrict__ buf, double* __restrict__ v) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(v + idx[i], buf[i]);
 }
 
 // ------------------------------------------------------------- misc vector kernels

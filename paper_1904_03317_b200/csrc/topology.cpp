@@ -148,7 +148,7 @@ Topology make_topology(const Forest& f, const Partition& p, int k) {
           okey[o] = morton(d, X);
           oid[o] = (u64)o;
           oflag[o] = (on_boundary(f, k, X) ? F_B : 0) | (cells.leaf[c] ? F_LEAF : 0);
-          oown[o] = cells.owner[c];
+          oown[o] = 0;   // coarse handoff: every level-0 DoF is owned by rank 0 (R25)
         }
       }
     } else {
@@ -185,14 +185,13 @@ Topology make_topology(const Forest& f, const Partition& p, int k) {
           uint8_t fl = 0;
           if (pt.dirmask[a] & outside) fl |= F_B;
           if (pt.dirmask[a] & leafn) fl |= F_EREG;
-          i32 own = INT32_MAX;
           for (int c = 0; c < nch; ++c)
-            if (pt.childmask[a] & (1u << c)) {
-              own = std::min(own, cells.owner[fi * nch + c]);
-              if (cells.leaf[fi * nch + c]) fl |= F_LEAF;
-            }
+            if ((pt.childmask[a] & (1u << c)) && cells.leaf[fi * nch + c]) fl |= F_LEAF;
           oflag[o] = fl;
-          oown[o] = own;
+          // DoF owner = min owner of the families (= of their parents, first-child
+          // rule) whose patch contains the node (R25): the rank that computes a
+          // family owns at least one DoF-containing family of each DoF it owns
+          oown[o] = par.owner[t.fam_parent[fi]];
         }
       }
     }
@@ -207,15 +206,18 @@ Topology make_topology(const Forest& f, const Partition& p, int k) {
       i64 e = s;
       uint8_t fl = 0;
       i32 own = INT32_MAX;
-      i64 first = INT64_MAX;
       while (e < n_occ && okey[e] == okey[s]) {
         i64 o = (i64)oid[e];
         fl |= oflag[o];
         own = std::min(own, oown[o]);
-        first = std::min(first, o);
         node_of_occ[o] = (i32)nkey.size();
         ++e;
       }
+      // transfer owner: the first family (SFC order) containing the node among
+      // the families computed by the node's owner rank (R26)
+      i64 first = INT64_MAX;
+      for (i64 q = s; q < e; ++q)
+        if (oown[oid[q]] == own) first = std::min(first, (i64)oid[q]);
       nkey.push_back(okey[s]);
       nfl.push_back(fl);
       nown.push_back(own);
