@@ -11,10 +11,12 @@ multigrid-layout vector is 466 MB > 126 MB), so no flush is needed.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config c3] [--profile]
 
---impl reference times the CPU oracle (oracle/, numpy/scipy, as it stands) on
-a bounded sample of the same workload family (c3 recipe truncated at 4 passes).
-For N > 1 this version runs N independent replicas (one per GPU, weak scaling,
-no collective): the sharded multi-GPU V-cycle is not implemented yet.
+N > 1 (torchrun, one rank per GPU): the same forest is sharded along the SFC
+partition with the first-child rule; every level exchanges ghosts with grouped
+ncclSend/ncclRecv and CG dots use ncclAllReduce (strong scaling: total work
+fixed).  --impl reference times the CPU oracle (oracle/, numpy/scipy, as it
+stands) on a bounded sample of the same workload family (c3 recipe truncated at
+4 passes).
 """
 from __future__ import annotations
 
@@ -115,7 +117,6 @@ class ClockSampler:
 # ---------------------------------------------------------------- reference arm
 def oracle_sample(steps: int, warmup: int):
     """The oracle V-cycle, as it stands, on the bounded sample (c3 recipe at 4 passes)."""
-    import numpy as np
     from gmg_inputs import config, uniform_pm1
     from oracle import forest as F, mg
     cfg = config(SAMPLE)
@@ -144,7 +145,7 @@ def run_reference(args):
                      f"(scipy CSR level matrices, single thread), setup {r['setup_s']:.1f}s excluded"}
     out = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * r["sec_per_vcycle"], "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
            "config": {"workload": WORKLOADS[SAMPLE], "sample_of": args.config},
            "cpu_baseline": cpu,
@@ -161,18 +162,27 @@ def run_ours(args):
     from gmg_inputs import config, uniform_pm1
 
     rank, world, local = env_rank()
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     cfg = config(args.config)
     t0 = time.time()
-    f, part, h = G.build_config(cfg)
+    f = G.gmg_forest_generate(G.recipe_from_config(cfg))
+    part = G.gmg_partition(f, world)
+    comm = None
+    if world > 1:
+        uid = [G.gmg_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = G.NcclComm(uid[0], world, rank)
+    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, comm=comm)
     setup_s = time.time() - t0
     info = h.info()
-    n_free = info["n_leaf_free"]
     n_dofs = info["n_leaf_nodes"]
-    b = torch.tensor(uniform_pm1(n_free), device=dev, dtype=torch.float64)
+    fo, n_own = info["first_owned"], info["n_owned"]
+    canon = h.leaf_dofs()[3]
+    b_can = uniform_pm1(info["n_leaf_free"])
+    b = torch.tensor(b_can[canon[fo:fo + n_own]], device=dev, dtype=torch.float64)
     x = torch.zeros_like(b)
     stream = torch.cuda.current_stream()
 
@@ -180,6 +190,13 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world > 1:
+            tt = torch.tensor([v], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            v = float(tt.item())
+        return v
 
     for _ in range(max(args.warmup, 1)):
         h.vcycle(b, x)
@@ -200,22 +217,18 @@ def run_ours(args):
         e1.synchronize()
         barrier()
     launches = h.launch_count() - launches0
-    t_dev = e0.elapsed_time(e1) / 1e3
-    if world > 1:
-        tt = torch.tensor([t_dev], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_dev = float(tt.item())
-    value = world * n_dofs * args.steps / t_dev
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    value = n_dofs * args.steps / t_dev            # one sharded V-cycle of the whole forest per step
 
-    # ---- roofline of the dominant kernel: cell_apply on the finest level
+    # ---- roofline of the dominant kernel: level operator on the finest level (rank-local)
     L = info["n_levels"] - 1
+    fo_l, no_l, gh_l = h.rank_level(L)
+    n_loc = no_l + len(gh_l)
     nL = info["level_dofs"][L]
     ncell = info["level_cells"][L]
     nn = (cfg["k"] + 1) ** cfg["dim"]
-    xa = torch.tensor(uniform_pm1(nL), device=dev, dtype=torch.float64)
+    xa = torch.tensor(uniform_pm1(n_loc), device=dev, dtype=torch.float64)
     ya = torch.zeros_like(xa)
-    h.level_apply(L, xa, ya)
-    ya.zero_()
     for _ in range(3):
         h.level_apply_kernel(L, xa, ya)
     reps = 20
@@ -223,19 +236,20 @@ def run_ours(args):
     torch.cuda.synchronize()
     a0.record(stream)
     for _ in range(reps):
-        h.level_apply_kernel(L, xa, ya)           # the kernel alone (no memset)
+        h.level_apply_kernel(L, xa, ya)           # the kernel alone (no memset, no exchange)
     a1.record(stream)
     a1.synchronize()
-    t_apply = a0.elapsed_time(a1) / 1e3 / reps
-    alg_bytes = 16 * nL + 4 * nn * ncell          # x read + y write + index table
+    t_apply = max_over_ranks(a0.elapsed_time(a1) / 1e3 / reps)
+    # 16 B per level DoF (x read, y write) + 4 B x 27 index entries per cell
+    alg_bytes = (16 * nL + 4 * nn * ncell) / world
     peak, peak_src = load_peaks()
     achieved = alg_bytes / t_apply / 1e9
     applies_per_vc = 2 * args.cheb_degree         # (m-1) pre + 1 residual + m post on every level
     share = applies_per_vc * t_apply / (t_dev / args.steps)
 
     # ---- end to end through the C ABI with host buffers (pinned), copies timed
-    bh = torch.tensor(uniform_pm1(n_free), dtype=torch.float64).pin_memory()
-    xh = torch.empty(n_free, dtype=torch.float64).pin_memory()
+    bh = torch.tensor(b_can[canon[fo:fo + n_own]], dtype=torch.float64).pin_memory()
+    xh = torch.empty(n_own, dtype=torch.float64).pin_memory()
     bd = torch.empty_like(b)
     xd = torch.empty_like(b)
     for _ in range(2):
@@ -252,22 +266,18 @@ def run_ours(args):
         xh.copy_(xd, non_blocking=True)
     s1.record(stream)
     s1.synchronize()
-    t_e2e = s0.elapsed_time(s1) / 1e3
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-    e2e_value = world * n_dofs * e2e_steps / t_e2e
+    t_e2e = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+    e2e_value = n_dofs * e2e_steps / t_e2e
 
     # ---- one GMG-CG solve (context, not the metric)
     bb = torch.zeros_like(b)
     h.rhs_constant(1.0, bb)
     xs = torch.zeros_like(b)
-    torch.cuda.synchronize()
+    barrier()
     c0 = time.perf_counter()
     its, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
     torch.cuda.synchronize()
-    t_cg = time.perf_counter() - c0
+    t_cg = max_over_ranks(time.perf_counter() - c0)
 
     per_vc, per_la = h.launch_profile()
     cpu = None
@@ -277,25 +287,27 @@ def run_ours(args):
                "sample": f"{SAMPLE}: c3 recipe at 4 passes, {r['n_dofs']} DoFs, 3 oracle V-cycles "
                          f"(scipy CSR, single thread), setup excluded"}
     if rank == 0:
+        model = part.model()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
-                          "n_leaf_dofs": n_dofs, "n_free_dofs": n_free, "levels": info["n_levels"],
+                          "n_leaf_dofs": n_dofs, "n_free_dofs": info["n_leaf_free"], "levels": info["n_levels"],
                           "level_dofs": info["level_dofs"], "k": cfg["k"], "dim": cfg["dim"],
                           "cheb_degree": args.cheb_degree, "global_batch": 1,
                           "l2": "inputs larger than L2 (MG-layout vectors %.0f MB each > 126 MB)"
                                 % (info["mg_vector_len"] * 8 / 1e6),
                           "parallelism": "single GPU" if world == 1 else
-                          f"{world} independent replicas (sharded V-cycle not implemented)",
-                          "setup_s": round(setup_s, 2)},
+                          f"{world} ranks, SFC partition + first-child rule, NCCL ghost exchange",
+                          "partition_eta": model["eta"], "setup_s": round(setup_s, 2)},
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": None, "kernel": "fam_tensor_apply<3,2> (level operator), finest level",
+                            "frac": achieved / peak, "traffic": None,
+                            "kernel": "fam_tensor_apply<3,2> (level operator), finest level",
                             "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,
                             "share_of_step": share, "peak_source": peak_src},
                "cpu_baseline": cpu,
-               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_free,
-                       "d2h_bytes_per_step": 8 * n_free},
+               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * info["n_leaf_free"],
+                       "d2h_bytes_per_step": 8 * info["n_leaf_free"]},
                "gpu_launches": launches,
                "launches_per_vcycle": per_vc,
                "clocks": clk.summary(),
@@ -304,6 +316,9 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
+        if comm is not None:
+            del h
+            comm.destroy()
         dist.destroy_process_group()
 
 

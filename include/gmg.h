@@ -259,9 +259,11 @@ gmg_status gmg_rhs_constant(gmg_hierarchy *h, double f, double *b_dev, void *cud
 /* y = K_l x over all cells of C_l on S u E rows (edge rows included). */
 gmg_status gmg_level_apply(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
                            void *cuda_stream);
-/* The level-operator kernel alone (no memset): y must be zero on entry, y = K_l x
- * on exit.  For timing the kernel in isolation (repeated calls on the same y
- * give a meaningless y but the same work per launch). */
+/* The level-operator kernel alone (no memset, no exchange): y must be zero on
+ * entry, y = (rank-local part of) K_l x on exit; vectors have the rank-local
+ * length n_owned + n_ghost (gmg_export_rank_level).  For timing the kernel in
+ * isolation (repeated calls on the same y give a meaningless y but the same
+ * work per launch). */
 gmg_status gmg_level_apply_kernel(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
                                   void *cuda_stream);
 /* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1) */

@@ -19,6 +19,18 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgmg.so")
 
+if "GMG_NCCL_LIB" not in os.environ:
+    # use the libnccl that torch loads (pip nvidia-nccl), not the system copy
+    try:
+        import nvidia.nccl as _nccl_pkg
+        for _p in _nccl_pkg.__path__:
+            _cand = os.path.join(_p, "lib", "libnccl.so.2")
+            if os.path.exists(_cand):
+                os.environ["GMG_NCCL_LIB"] = _cand
+                break
+    except Exception:
+        pass
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libgmg.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = C.CDLL(LIB_PATH)

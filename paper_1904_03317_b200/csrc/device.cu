@@ -748,7 +748,7 @@ void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, v
 }
 
 void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
-  need_single(d);
+  // rank-local kernel only (vectors of the local length n_owned + n_ghost), no exchange
   DevLevel& v = d->lv[l];
   k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());

@@ -178,6 +178,16 @@ def _local_group(cfg, p):
 
 
 @pytest.mark.gpu
+def test_nccl_transport_loads():
+    """libnccl is dlopen'ed (the torch copy) and a 1-rank communicator initialises."""
+    uid = G.gmg_nccl_get_unique_id()
+    assert len(uid) == 128
+    c = G.NcclComm(uid, 1, 0)
+    assert c.h
+    c.destroy()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,p", [("c1", 2), ("c1", 3), ("c3p2", 2), ("c3p2", 4), ("c2", 3)])
 def test_local_ranks_equal_single_rank(name, p):
     import torch
