@@ -16,7 +16,6 @@
 #include "comm.hpp"
 #include "device.hpp"
 #include "kernels.cuh"
-#include "plan.hpp"
 
 namespace gmg {
 
@@ -33,14 +32,8 @@ struct DevLevel {
   double* coef = nullptr;
   unsigned char* cls = nullptr;     // bit0 = E
   double* Dinv = nullptr;           // n_pad entries, 0 on E rows, ghosts and padding
+  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
-  // fused level operator (plan.hpp): device order [R1 | R2 | R3 | ghosts]
-  i64 n_chunks = 0, r2_begin = 0;
-  int max_slots = 0, max_r1 = 0, max_halo = 0;
-  int4* chunk_meta = nullptr;
-  int* chunk_halo = nullptr;
-  unsigned short* chunk_loc = nullptr;
-  int* perm = nullptr;              // level (rank-local) index -> device index
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
   double h = 1, scale = 1;          // scale = h^(d-2)
@@ -76,6 +69,8 @@ struct DeviceHierarchy {
   double* coarse_inv = nullptr;
   int* coarse_idx = nullptr;
   bool use_graph = true;
+  bool xfer_warp = true;        // warp-per-family transfers (GMG_XFER=thread: thread per family)
+  bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
@@ -148,44 +143,25 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- primitives
-// Launch of the persistent fused chunk kernel: grid = resident CTAs (a multiple
-// of the SM count, capped by the number of chunks), dynamic shared memory sized
-// by the level's largest chunk.
-template <int D, int K, int MODE, bool RDV, bool WDV>
-static void launch_chunk(DeviceHierarchy* d, DevLevel& v, double* x, double* t, const double* g, double* dv, double c1,
-                         double c2, cudaStream_t s) {
-  auto kern = dev::chunk_apply<D, K, MODE, RDV, WDV>;
-  const dev::ChunkSmem L = dev::chunk_smem_layout<D, K>(v.max_slots, v.max_r1, v.max_halo, MODE != dev::CM_APPLY,
-                                                        MODE == dev::CM_CHEB, MODE == dev::CM_CHEB && RDV);
-  static const bool attr_set = [&] {   // once per instantiation, the same value from every thread
-    int dev_id = 0, opt = 0;
-    CK(cudaGetDevice(&dev_id));
-    CK(cudaDeviceGetAttribute(&opt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id));
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, opt));
-    return true;
-  }();
-  (void)attr_set;
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * dev::CHUNK_F, L.total));
-  GMG_REQUIRE(per_sm >= 1, GMG_E_CUDA, "fused chunk kernel does not fit on an SM");
-  const i64 grid = std::min<i64>(v.n_chunks, (i64)per_sm * d->sms);
-  kern<<<(int)grid, 32 * dev::CHUNK_F, L.total, s>>>(L, (int)v.n_chunks, v.chunk_meta, v.chunk_halo, v.chunk_loc,
-                                                     (int)v.n_fam, v.scale, x, t, g, v.Dinv, dv, c1, c2);
-  CK(cudaPeekAtLastError());
-  d->launches++;
-}
-
-// y += K_l x over a cell list (leaf cells, thread per cell, atomic scatter) or,
-// list == nullptr, over all local cells.  Full levels >= 1 run the fused chunk
-// kernel in CM_APPLY mode: R1 rows are stored (y need not be zero there), all
-// other rows reduced (y must be zero there on entry).
+// y += K_l x over a cell list (leaf cells) or, list == nullptr, over all local
+// cells.  Full levels >= 1 run family-blocked (y must be zero on entry:
+// patch-interior nodes are stored, not added); level 0 and cell lists run
+// thread-per-cell.
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
-  if (list == nullptr && v.n_chunks > 0 && v.coef == nullptr) {
-    DISPATCH_DK(d->dim, d->k, (launch_chunk<D_, K_, dev::CM_APPLY, false, false>(
-                                   d, v, const_cast<double*>(x), y, nullptr, nullptr, 0.0, 0.0, s)));
-    return;
+  if (list == nullptr && l > 0 && v.n_fam > 0 && v.coef == nullptr && d->tensor_apply) {
+    const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
+    const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
+    int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
+    DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+                                  (int)v.n_fam, v.xfer, np + nn, v.scale, x, y)));
+  } else if (list == nullptr && l > 0 && v.n_fam > 0) {
+    DISPATCH_DK(d->dim, d->k, {
+      constexpr int FPB = dev::FamCfg<D_, K_>::FPB;
+      int grid = (int)((v.n_fam + FPB - 1) / FPB);
+      dev::fam_apply<D_, K_><<<grid, FPB * (1 << D_), 0, s>>>((int)v.n_fam, v.fam_dofs, v.coef, v.scale, x, y);
+    });
   } else {
     const int nt = 128;
     int grid = (int)((n + nt - 1) / nt);
@@ -234,28 +210,6 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const double* g, double* t, 
   d->launches++;
 }
 
-// One fused operator step on level l (MODE = CM_RESID: t = g - K x; CM_CHEB:
-// Chebyshev step on x, dv with t = K x formed on the fly): ghost import of x,
-// chunk kernel (R1 rows finished in its epilogue), export-add of the reduced
-// ghost rows, streaming finish of the reduced owned rows R2, R3.
-template <int MODE, bool RDV, bool WDV>
-static void fused_step(DeviceHierarchy* d, int l, double* x, double* t, const double* g, double* dv, double c1,
-                       double c2, cudaStream_t s) {
-  DevLevel& v = d->lv[l];
-  import_ghosts(d, l, x, s);
-  if (v.n_chunks > 0 && v.coef == nullptr) {
-    DISPATCH_DK(d->dim, d->k, (launch_chunk<D_, K_, MODE, RDV, WDV>(d, v, x, t, g, dv, c1, c2, s)));
-  } else {
-    k_apply(d, l, nullptr, v.n_cells, x, t, s);
-  }
-  export_add(d, l, t, s);
-  const i64 a = (v.n_chunks > 0 && v.coef == nullptr) ? v.r2_begin : 0, nt = v.n_owned - a;
-  if (nt > 0) {
-    dev::chunk_tail<MODE, RDV, WDV><<<(int)((nt + 255) / 256), 256, 0, s>>>(a, nt, g, v.Dinv, t, dv, x, c1, c2);
-    d->launches++;
-  }
-}
-
 // Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
 // first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
 // x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows and ghosts keeps those entries fixed).
@@ -266,12 +220,14 @@ static void smooth(DeviceHierarchy* d, int l, const double* g, double* x, double
   if (x_zero) {
     k_cheb<false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else {
-    if (m == 1) fused_step<dev::CM_CHEB, false, false>(d, l, x, t, g, dv, 0.0, v.c2[0], s);
-    else fused_step<dev::CM_CHEB, false, true>(d, l, x, t, g, dv, 0.0, v.c2[0], s);
+    apply_full(d, l, x, t, s);
+    if (m == 1) k_cheb<true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    else k_cheb<true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   }
   for (int j = 1; j < m; ++j) {
-    if (j == m - 1) fused_step<dev::CM_CHEB, true, false>(d, l, x, t, g, dv, v.c1[j], v.c2[j], s);
-    else fused_step<dev::CM_CHEB, true, true>(d, l, x, t, g, dv, v.c1[j], v.c2[j], s);
+    apply_full(d, l, x, t, s);
+    if (j == m - 1) k_cheb<true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
+    else k_cheb<true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
   }
 }
 
@@ -289,8 +245,8 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
     double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
     double* gc = d->D + d->lv[l - 1].off;
     smooth(d, l, g, x, t, dv, true, s);                                     // 1: pre-smooth from 0
-    fused_step<dev::CM_RESID, false, false>(d, l, x, t, g, nullptr, 0, 0, s);  // 2: t = d - K x
-    k_restrict<dev::RES_T>(d, l, nullptr, v.n_fam, nullptr, t, gc, s);      // 3: d_{l-1} += P^T t
+    apply_full(d, l, x, t, s);                                              // 2: t = K x
+    k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
     export_add(d, l - 1, gc, s);
   }
   coarse(d, d->D + d->lv[0].off, d->X + d->lv[0].off, s);                   // 4: coarse solve (rank 0)
@@ -475,11 +431,10 @@ static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- creation
-DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique_ptr<Comm> comm,
+DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::unique_ptr<Comm> comm,
                                i64 n0_global) {
   auto* d = new DeviceHierarchy();
   try {
-    const DevicePlan plan = plan_device_order(Tp);   // device order of the level vectors (rewrites Tp)
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
@@ -494,6 +449,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     d->eig_iters = prm.eig_iters;
     d->n0_global = n0_global;
     d->use_graph = !(prm.flags & GMG_NO_GRAPH) && (!d->comm || d->comm->capturable());
+    if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
     const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
@@ -521,20 +477,14 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       std::vector<unsigned char> cls(v.n);
       for (i64 i = 0; i < v.n; ++i) cls[i] = t.cls[i] == CLS_E ? 1 : 0;
       v.cls = d->upload(cls);
-      v.xfer = d->upload(t.xfer);
       {
-        const ChunkLevel& C = plan.lv[l];
-        v.n_chunks = C.n_chunks;
-        v.r2_begin = C.r2_begin;
-        v.max_slots = C.max_slots;
-        v.max_r1 = C.max_r1;
-        v.max_halo = C.max_halo;
-        v.chunk_meta = (int4*)d->upload(C.meta);
-        std::vector<i32> hp(C.halo);
-        hp.resize(hp.size() + 8, 0);          // slack for the 16-byte aligned bulk copies
-        v.chunk_halo = d->upload(hp);
-        v.chunk_loc = d->upload(C.loc);
-        v.perm = d->upload(plan.perm[l]);
+        // patch table AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
+        const size_t np = t.n_fam ? t.fam_dofs.size() / (size_t)t.n_fam : 0;
+        std::vector<int> fs(t.fam_dofs.size());
+        for (size_t f = 0; f < (size_t)t.n_fam; ++f)
+          for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.fam_dofs[f * np + a];
+        v.fam_dofs = d->upload(fs);
+        v.xfer = d->upload(t.xfer);
       }
       v.leaf_cells = d->upload(t.leaf_cells);
       v.edge_fams = d->upload(t.edge_fams);
@@ -788,40 +738,17 @@ static void need_single(const DeviceHierarchy* d) {
   GMG_REQUIRE(!d->comm, GMG_E_STATE, "single-operator entry points are defined for n_ranks == 1");
 }
 
-// The single-operator entry points take level vectors in the rank-local level
-// order (= global order for one rank) and permute to the device order at the
-// boundary, through the W / Y work buffers.
-static void to_dev(DeviceHierarchy* d, int l, const double* src, double* dst, cudaStream_t s) {
-  DevLevel& v = d->lv[l];
-  CK(cudaMemsetAsync(dst, 0, v.n_pad * sizeof(double), s));
-  if (v.n) {
-    dev::permute_in<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.perm, src, dst);
-    d->launches++;
-  }
-}
-static void from_dev(DeviceHierarchy* d, int l, const double* src, double* dst, cudaStream_t s) {
-  DevLevel& v = d->lv[l];
-  if (v.n) {
-    dev::permute_out<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.perm, src, dst);
-    d->launches++;
-  }
-}
-
 void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
   need_single(d);
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
-  double *xp = d->W + v.off, *yp = d->Y + v.off;
-  to_dev(d, l, x, xp, s);
-  CK(cudaMemsetAsync(yp, 0, v.n_pad * sizeof(double), s));
-  k_apply(d, l, nullptr, v.n_cells, xp, yp, s);
-  from_dev(d, l, yp, y, s);
+  if (v.n) CK(cudaMemsetAsync(y, 0, v.n * sizeof(double), s));
+  k_apply(d, l, nullptr, v.n_cells, x, y, s);
   CK(cudaPeekAtLastError());
 }
 
 void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
-  // rank-local kernel only (vectors of the local length n_owned + n_ghost in the
-  // device order), no exchange
+  // rank-local kernel only (vectors of the local length n_owned + n_ghost), no exchange
   DevLevel& v = d->lv[l];
   k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
@@ -829,23 +756,13 @@ void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, doubl
 
 void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
   need_single(d);
-  cudaStream_t s = (cudaStream_t)stream;
-  double *rp = d->W + d->lv[l].off, *cp = d->Y + d->lv[l - 1].off;
-  to_dev(d, l, r, rp, s);
-  to_dev(d, l - 1, dc, cp, s);
-  k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, rp, nullptr, cp, s);
-  from_dev(d, l - 1, cp, dc, s);
+  k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
 
 void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, void* stream) {
   need_single(d);
-  cudaStream_t s = (cudaStream_t)stream;
-  double *cp = d->W + d->lv[l - 1].off, *fp = d->Y + d->lv[l].off;
-  to_dev(d, l - 1, xc, cp, s);
-  to_dev(d, l, xf, fp, s);
-  k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, cp, fp, s);
-  from_dev(d, l, fp, xf, s);
+  k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, xc, xf, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
 
@@ -867,25 +784,24 @@ void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, 
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   GMG_REQUIRE(l >= 1, GMG_E_INVALID_ARG, "no smoother on level 0");
+  // padded internal copies (the vector kernels stream the padded segment)
   double* gg = d->W + v.off;
   double* xx = d->Y + v.off;
-  to_dev(d, l, g, gg, s);
-  if (x_zero) CK(cudaMemsetAsync(xx, 0, v.n_pad * sizeof(double), s));
-  else to_dev(d, l, x, xx, s);
+  CK(cudaMemcpyAsync(gg, g, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (!x_zero) CK(cudaMemcpyAsync(xx, x, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   smooth(d, l, gg, xx, d->T + v.off, d->DV + v.off, x_zero != 0, s);
-  from_dev(d, l, xx, x, s);
+  CK(cudaMemcpyAsync(x, xx, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(gg, 0, v.n_pad * sizeof(double), s));
+  CK(cudaMemsetAsync(xx, 0, v.n_pad * sizeof(double), s));
   CK(cudaPeekAtLastError());
 }
 
 void device_level_diagonal(DeviceHierarchy* d, int l, double* diag, void* stream) {
   need_single(d);
-  cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   if (v.n == 0) return;
-  double* yp = d->Y + v.off;
-  dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.cls, v.Dinv, yp);
+  dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v.n, v.cls, v.Dinv, diag);
   d->launches++;
-  from_dev(d, l, yp, diag, s);
   CK(cudaPeekAtLastError());
 }
 

@@ -1,28 +1,28 @@
 // sm_100a kernels of the local-smoothing GMG hot path (fp64, no tensor cores:
 // the contractions are 3x3 / 5x5 per direction, not a GEMM).
 //
-//  chunk_apply     fused level operator over chunks of 8 consecutive families:
-//                  coalesced R1 load + halo gather into shared memory, family
-//                  patch tensor operators (sum factorisation), and the
-//                  epilogue on the chunk's own rows: t = Kx, t = g - Kx (residual)
-//                  or the Chebyshev-Jacobi step; halo rows reduced
-//                  into t with fp64 RED at L2
-//  chunk_tail      finishes the reduced rows (R2, R3)
+//  fam_apply       y += K_l x over the cells of C_l, one block = FPB families of
+//                  2^d sibling cells (the children of a refined level-(l-1) cell),
+//                  thread per cell: register-resident sum-factorised Q_k Laplace
+//                  (P:565-578), per-cell results combined per family patch in
+//                  shared memory, patch-interior nodes stored exclusively, only
+//                  family-boundary nodes scattered with fp64 atomics at L2
 //  cell_apply      same operator over an explicit cell list (leaf cells of the
 //                  leaf operator, level 0), thread per cell, atomic scatter
 //  cell_diag       diagonal of the level operator
 //  cell_load       b += f h^d (w (x) w (x) w) on leaf cells (f = const)
-//  cheb_step       Chebyshev-Jacobi vector update over a whole level (first
-//                  pre-smoothing step from x = 0), double2 streaming
-//  warp_restrict   d_{l-1} += P^T r, warp per family; each
-//                  fine node is summed by the one family that owns it
-//  warp_prolongate x_l += P x_{l-1} on owned fine nodes (exclusive writes), or
+//  cheb_step       fused Chebyshev-Jacobi vector update + reset of the
+//                  apply accumulator, double2 streaming
+//  fam_restrict    d_{l-1} += P^T r, warp per family, r = d - K x computed on the
+//                  fly for the V-cycle residual (edge rows included);
+//                  each fine node is summed by the one family that owns it
+//  fam_prolongate  x_l += P x_{l-1} on owned fine nodes (exclusive writes), or
 //                  x_l[E] = (P x_{l-1})[E] (hanging / edge values, leaf operator)
 //  dot / axpy      CG vector kernels with deterministic two-stage reductions
 //
-// Family patch table (AoS [n_fam][(2k+1)^d]): v >= 0: level DoF v owned (for
-// transfers) by this family; v == -1: Dirichlet node; v <= -2: DoF -2-v owned by
-// an earlier family.
+// Family patch table fam_dofs (AoS [n_fam][(2k+1)^d]): v >= 0: level DoF v owned
+// (for transfers) by this family; v == -1: Dirichlet node; v <= -2: DoF -2-v
+// owned by an earlier family.
 #pragma once
 #include <cstdint>
 
@@ -179,12 +179,75 @@ __host__ __device__ __forceinline__ constexpr int patch_of(int c, int b) {
 __device__ __forceinline__ int decode_dof(int v) { return v >= 0 ? v : (v <= -2 ? -2 - v : -1); }
 
 // ------------------------------------------------------------- level operator
+template <int D, int K> struct FamCfg { static constexpr int FPB = D == 3 ? 16 : 32; };
+
+template <int D, int K>
+__global__ void __launch_bounds__(FamCfg<D, K>::FPB * (1 << D))
+fam_apply(int nfam, const int* __restrict__ fam_dofs, const double* __restrict__ coef, double scale,
+          const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int NN = Shape<D, K>::NN, NP = Shape<D, K>::NP, NCH = Shape<D, K>::NCH;
+  constexpr int NP1 = 2 * K + 1, N = K + 1;
+  constexpr int FPB = FamCfg<D, K>::FPB, NT = FPB * NCH;
+  __shared__ int sidx[FPB * NP];
+  __shared__ double sout[NT * NN];
+  const int tid = threadIdx.x;
+  const long fam0 = (long)blockIdx.x * FPB;
+  const int nf_here = (int)min((long)FPB, (long)nfam - fam0);
+  // SoA patch table [NP][nfam]: row a holds the FPB families of this block contiguously
+  for (int i = tid; i < FPB * NP; i += NT) {
+    const int a = i / FPB, fl = i % FPB;
+    sidx[fl * NP + a] = fl < nf_here ? __ldg(fam_dofs + (long)a * nfam + fam0 + fl) : -1;
+  }
+  __syncthreads();
+  const int fl = tid / NCH, c = tid % NCH;
+  if (fl < nf_here) {
+    double u[NN], v[NN];
+#pragma unroll
+    for (int b = 0; b < NN; ++b) {
+      const int i = decode_dof(sidx[fl * NP + patch_of<D, K>(c, b)]);
+      u[b] = i >= 0 ? __ldg(x + i) : 0.0;
+    }
+    elem_apply<D, K>(u, v);
+    const double s = coef ? scale * __ldg(coef + (fam0 + fl) * NCH + c) : scale;
+#pragma unroll
+    for (int b = 0; b < NN; ++b) sout[tid * NN + b] = s * v[b];
+  }
+  __syncthreads();
+  for (int i = tid; i < nf_here * NP; i += NT) {
+    const int fl2 = i / NP, a = i % NP;
+    const int dof = decode_dof(sidx[i]);
+    if (dof < 0) continue;
+    int ad[3] = {a % NP1, (a / NP1) % NP1, D == 3 ? a / (NP1 * NP1) : 0};
+    bool interior = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) interior &= (ad[j] > 0 && ad[j] < 2 * K);
+    double sum = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < NCH; ++cc) {
+      bool in = true;
+      int b = 0, mul = 1;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const int cj = (cc >> j) & 1;
+        const int bj = ad[j] - cj * K;
+        in &= (bj >= 0 && bj <= K);
+        b += bj * mul;
+        mul *= N;
+      }
+      if (in) sum += sout[(fl2 * NCH + cc) * NN + b];
+    }
+    if (interior) y[dof] = sum;          // only this family touches the node
+    else atomicAdd(y + dof, sum);
+  }
+}
+
 // Family-patch tensor form of the level operator.  On a family (2^d siblings of
 // width h, one coefficient) the sum of the 2^d cell operators is itself a
 // Kronecker sum over the (2k+1)^d patch: sum_i (x)_j (j == i ? Kt : Mt) with the
 // 1-D matrices Kt, Mt assembled over the two children (P:575-577 applied to the
-// patch): 7 one-dimensional passes in 3D, 4 in 2D, ~35% fewer DFMA than the
-// 2^d separate cell operators.
+// patch).  Warp per family, one lane per 1-D line of the patch, 1-D passes
+// through shared memory (7 passes in 3D, 4 in 2D); ~35% fewer DFMA than the 2^d
+// separate cell operators and ~40 registers per thread instead of ~130.
 template <int K>
 __host__ __device__ __forceinline__ constexpr double Kt(int i, int j) {
   double s = 0.0;
@@ -204,29 +267,29 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
   return s;
 }
 
-// One warp applies one family's patch operator: inputs gathered from the
-// chunk's shared-memory vector xs through the family's slot table sl
-// (LOC_NONE = Dirichlet node, value 0), outputs added to the chunk's
-// shared-memory accumulator acc.  Lanes = 1-D lines of the patch; s0/s1 are the
-// warp's transposition buffers.
-constexpr unsigned short LOC_NONE_D = 0xFFFF;
+constexpr int TENSOR_WARPS = 8;
+
 template <int D, int K>
-__device__ __forceinline__ void family_patch_apply(int lane, const unsigned short* __restrict__ sl,
-                                                   const double* __restrict__ xs, double* acc, double* s0,
-                                                   double* s1, double scale) {
+__global__ void __launch_bounds__(32 * TENSOR_WARPS)
+fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, double scale, const double* __restrict__ x,
+                 double* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
-  if (lane >= NL) return;
+  __shared__ double s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * TENSOR_WARPS + w;
+  if (f >= nfam) return;
+  const int* rp = xfer + (long)f * row;
   double out[NP1];
-  int ob, os;
+  int ob = 0, os = 0;   // output line: base and stride in the patch
   if constexpr (D == 3) {
     constexpr int S2 = NP1 * NP1;
-    {  // z lines: lane = (px, py)
+    if (lane < NL) {     // z lines: lane = (px, py), gathered straight into registers
+      int gi[NP1];
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
       double u[NP1];
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) {
-        const unsigned short l = sl[z * S2 + lane];
-        u[z] = l != LOC_NONE_D ? xs[l] : 0.0;
-      }
+      for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : 0.0;
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         double t1 = 0.0, t2 = 0.0;
@@ -235,18 +298,18 @@ __device__ __forceinline__ void family_patch_apply(int lane, const unsigned shor
           if (Mt<K>(z, q) != 0.0) t1 = fma(Mt<K>(z, q), u[q], t1);
           if (Kt<K>(z, q) != 0.0) t2 = fma(Kt<K>(z, q), u[q], t2);
         }
-        s0[z * S2 + lane] = t1;
-        s1[z * S2 + lane] = t2;
+        s0[w][z * S2 + lane] = t1;
+        s1[w][z * S2 + lane] = t2;
       }
     }
-    __syncwarp((1u << NL) - 1);
-    {  // y lines: lane = (px, pz)
+    __syncwarp();
+    if (lane < NL) {     // y lines: lane = (px, pz)
       const int px = lane % NP1, pz = lane / NP1, b = pz * S2 + px;
       double t1[NP1], t2[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        t1[q] = s0[b + q * NP1];
-        t2[q] = s1[b + q * NP1];
+        t1[q] = s0[w][b + q * NP1];
+        t2[q] = s1[w][b + q * NP1];
       }
 #pragma unroll
       for (int yy = 0; yy < NP1; ++yy) {
@@ -259,19 +322,19 @@ __device__ __forceinline__ void family_patch_apply(int lane, const unsigned shor
           }
           if (Kt<K>(yy, q) != 0.0) bb = fma(Kt<K>(yy, q), t1[q], bb);
         }
-        s0[b + yy * NP1] = a;
-        s1[b + yy * NP1] = bb;
+        s0[w][b + yy * NP1] = a;
+        s1[w][b + yy * NP1] = bb;
       }
     }
-    __syncwarp((1u << NL) - 1);
-    {  // x lines: lane = (py, pz)
+    __syncwarp();
+    if (lane < NL) {     // x lines: lane = (py, pz)
       ob = lane * NP1;
       os = 1;
       double a[NP1], bb[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        a[q] = s0[ob + q];
-        bb[q] = s1[ob + q];
+        a[q] = s0[w][ob + q];
+        bb[q] = s1[w][ob + q];
       }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
@@ -285,13 +348,13 @@ __device__ __forceinline__ void family_patch_apply(int lane, const unsigned shor
       }
     }
   } else {
-    {  // x lines: lane = py
+    if (lane < NL) {     // x lines: lane = py, gathered straight into registers
       const int b = lane * NP1;
       double u[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        const unsigned short l = sl[b + q];
-        u[q] = l != LOC_NONE_D ? xs[l] : 0.0;
+        const int gi = decode_dof(__ldg(rp + b + q));
+        u[q] = gi >= 0 ? __ldg(x + gi) : 0.0;
       }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
@@ -301,19 +364,19 @@ __device__ __forceinline__ void family_patch_apply(int lane, const unsigned shor
           if (Kt<K>(xx, q) != 0.0) a = fma(Kt<K>(xx, q), u[q], a);
           if (Mt<K>(xx, q) != 0.0) bb = fma(Mt<K>(xx, q), u[q], bb);
         }
-        s0[b + xx] = a;
-        s1[b + xx] = bb;
+        s0[w][b + xx] = a;
+        s1[w][b + xx] = bb;
       }
     }
-    __syncwarp((1u << NL) - 1);
-    {  // y lines: lane = px
+    __syncwarp();
+    if (lane < NL) {     // y lines: lane = px
       ob = lane;
       os = NP1;
       double a[NP1], bb[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        a[q] = s0[lane + q * NP1];
-        bb[q] = s1[lane + q * NP1];
+        a[q] = s0[w][lane + q * NP1];
+        bb[q] = s1[w][lane + q * NP1];
       }
 #pragma unroll
       for (int yy = 0; yy < NP1; ++yy) {
@@ -327,256 +390,18 @@ __device__ __forceinline__ void family_patch_apply(int lane, const unsigned shor
       }
     }
   }
+  if (lane < NL) {
 #pragma unroll
-  for (int q = 0; q < NP1; ++q) {
-    const unsigned short l = sl[ob + q * os];
-    if (l != LOC_NONE_D) atomicAdd(acc + l, out[q]);
-  }
-}
-
-// ---- async-copy primitives (sm_90+ PTX; TMA bulk engine = UBLKCP in SASS)
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-          smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared bulk copy (16-byte aligned addresses, size a multiple of 16),
-// completion counted in bytes on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(b))
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Fused level-operator kernel over chunks of CHUNK_F consecutive families
-// (device order and tables: plan.hpp).  Persistent CTAs, one warp per family;
-// each CTA walks its chunks through a two-stage shared-memory pipeline:
-//  * the chunk's R1 rows are one contiguous range: x (and g, D^-1, dv for the
-//    epilogue) arrive by TMA bulk copies, the family slot table likewise; the
-//    halo x values are gathered with cp.async (8 B) through the halo index list,
-//    itself bulk-copied two chunks ahead.  Chunk i+1 streams in while chunk i
-//    computes;
-//  * every family's patch operator accumulates into shared memory;
-//  * R1 rows are complete (no other chunk or rank touches them) and are
-//    finished in the epilogue:
-//       CM_APPLY  t = K x                     (store)
-//       CM_RESID  t = g - K x                 (store; the V-cycle residual)
-//       CM_CHEB   dv = c1 dv + c2 D^-1 (g - K x),  x += dv   (Chebyshev-Jacobi step,
-//                 P:882-887, x-form of the first-kind recurrence; x updated in place:
-//                 R1 values are read only by this CTA)
-//    halo rows get their partial sums by fp64 reductions (RED) into t and are
-//    finished by chunk_tail (R2, R3 after the ghost export-add).
-constexpr int CHUNK_F = 8;
-enum : int { CM_APPLY = 0, CM_RESID = 1, CM_CHEB = 2 };
-
-struct ChunkSmem {      // dynamic shared-memory layout (byte offsets), computed on the host
-  int acc, s0, s1;      // accumulator, transposition buffers
-  int st, stride;       // stage s at st + s * stride: x slots | g | D^-1 | dv | slot table
-  int ge, de, ve, sl;   // offsets inside a stage
-  int hi, hstride;      // halo index list h at hi + h * hstride
-  int mb, total;
-};
-
-template <int D, int K>
-__host__ __device__ inline ChunkSmem chunk_smem_layout(int max_slots, int max_r1, int max_halo, bool need_g,
-                                                       bool need_d, bool need_v) {
-  constexpr int NP = Shape<D, K>::NP;
-  ChunkSmem L{};
-  int o = 0;
-  auto take = [&](int bytes) {
-    const int r = o;
-    o += (bytes + 15) & ~15;
-    return r;
-  };
-  const int ns = max_slots + 2, nr = max_r1 + 2;
-  L.acc = take(8 * ns);
-  L.s0 = take(8 * CHUNK_F * NP);
-  L.s1 = take(8 * CHUNK_F * NP);
-  L.st = o;
-  take(8 * ns);
-  L.ge = need_g ? take(8 * nr) - L.st : 0;
-  L.de = need_d ? take(8 * nr) - L.st : 0;
-  L.ve = need_v ? take(8 * nr) - L.st : 0;
-  L.sl = take(2 * CHUNK_F * NP) - L.st;
-  L.stride = o - L.st;
-  take(L.stride);
-  L.hi = o;
-  L.hstride = (4 * (max_halo + 8) + 15) & ~15;
-  take(3 * L.hstride);
-  L.mb = take(8 * 5);
-  L.total = o;
-  return L;
-}
-
-template <int D, int K, int MODE, bool READ_DV, bool WRITE_DV>
-__global__ void __launch_bounds__(32 * CHUNK_F, 2)
-chunk_apply(ChunkSmem L, int n_chunks, const int4* __restrict__ meta, const int* __restrict__ halo,
-            const unsigned short* __restrict__ loc, int nfam, double scale, double* x, double* __restrict__ t,
-            const double* __restrict__ g, const double* __restrict__ Dinv, double* __restrict__ dv, double c1,
-            double c2) {
-  constexpr int NP = Shape<D, K>::NP, NT = 32 * CHUNK_F;
-  constexpr bool NG = MODE != CM_APPLY, ND = MODE == CM_CHEB, NV = MODE == CM_CHEB && READ_DV;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* acc = (double*)(smem + L.acc);
-  double* s0 = (double*)(smem + L.s0);
-  double* s1 = (double*)(smem + L.s1);
-  unsigned long long* mb = (unsigned long long*)(smem + L.mb);   // [0,1] stages, [2,3,4] halo lists
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int c0 = blockIdx.x, cs = gridDim.x;
-  if (c0 >= n_chunks) return;
-  const int my_n = (n_chunks - c0 + cs - 1) / cs;   // chunks of this CTA: c0 + i cs, i < my_n
-
-  // bulk copy of the 16-byte aligned span covering [a, a + n) doubles
-  auto span = [](int a, int n, int& a0, int& bytes) {
-    a0 = a & ~1;
-    bytes = n > 0 ? 8 * (((a + n + 1) & ~1) - a0) : 0;
-  };
-  auto issue_halo_list = [&](int i) {   // one thread
-    const int4 m = __ldg(meta + c0 + i * cs);
-    const int h0 = m.z & ~3, hb = m.w > 0 ? 4 * (((m.z + m.w + 3) & ~3) - h0) : 0;
-    unsigned long long* b = mb + 2 + i % 3;
-    mbar_expect_tx(b, hb);
-    if (hb) bulk_g2s(smem + L.hi + (i % 3) * L.hstride, halo + h0, hb, b);
-  };
-  auto issue_main = [&](int i) {   // bulk part: one thread
-    const int c = c0 + i * cs, s = i & 1;
-    const int4 m = __ldg(meta + c);
-    int a0, bytes;
-    span(m.x, m.y, a0, bytes);
-    unsigned long long* b = mb + s;
-    const unsigned lb = 2 * CHUNK_F * NP;
-    mbar_expect_tx(b, lb + bytes * (1 + NG + ND + NV));
-    bulk_g2s(smem + L.st + s * L.stride + L.sl, loc + (long)c * CHUNK_F * NP, lb, b);
-    if (bytes) {
-      bulk_g2s(smem + L.st + s * L.stride, x + a0, bytes, b);
-      if (NG) bulk_g2s(smem + L.st + s * L.stride + L.ge, g + a0, bytes, b);
-      if (ND) bulk_g2s(smem + L.st + s * L.stride + L.de, Dinv + a0, bytes, b);
-      if (NV) bulk_g2s(smem + L.st + s * L.stride + L.ve, dv + a0, bytes, b);
+    for (int q = 0; q < NP1; ++q) {
+      const int a = ob + q * os;
+      const int i = decode_dof(__ldg(rp + a));
+      if (i < 0) continue;
+      int ad[3] = {a % NP1, (a / NP1) % NP1, D == 3 ? a / (NP1 * NP1) : 1};
+      bool interior = ad[0] > 0 && ad[0] < 2 * K && ad[1] > 0 && ad[1] < 2 * K && (D == 2 || (ad[2] > 0 && ad[2] < 2 * K));
+      if (interior) y[i] = out[q];       // only this family touches the node
+      else atomicAdd(y + i, out[q]);
     }
-  };
-  auto issue_gather = [&](int i) {   // all threads: halo x values, one cp.async group
-    const int4 m = __ldg(meta + c0 + i * cs);
-    const int* hl = (const int*)(smem + L.hi + (i % 3) * L.hstride) + (m.z & 3);
-    double* xh = (double*)(smem + L.st + (i & 1) * L.stride) + m.y + 2;
-    for (int j = tid; j < m.w; j += NT) cp_async8(xh + j, x + hl[j]);
-    cp_async_commit();
-  };
-
-  if (tid == 0) {
-    for (int q = 0; q < 5; ++q) mbar_init(mb + q, 1);
-    mbar_fence_init();
   }
-  for (int i = tid; i < (L.s0 - L.acc) / 8; i += NT) acc[i] = 0.0;
-  __syncthreads();
-  if (tid == 0) {
-    issue_halo_list(0);
-    if (my_n > 1) issue_halo_list(1);
-    issue_main(0);
-  }
-  mbar_wait(mb + 2, 0);
-  issue_gather(0);
-
-  for (int i = 0; i < my_n; ++i) {
-    const int c = c0 + i * cs, s = i & 1;
-    // ---- prefetch chunk i+1 (main + halo gather) and the halo list of chunk i+2
-    if (i + 1 < my_n) {
-      mbar_wait(mb + 2 + (i + 1) % 3, ((i + 1) / 3) & 1);
-      if (tid == 0) {
-        issue_main(i + 1);
-        if (i + 2 < my_n) issue_halo_list(i + 2);
-      }
-      issue_gather(i + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    mbar_wait(mb + s, (i >> 1) & 1);
-    __syncthreads();
-    // ---- family patch operators
-    const int4 m = __ldg(meta + c);
-    const double* xs = (const double*)(smem + L.st + s * L.stride);
-    const int f = c * CHUNK_F + w;
-    if (f < nfam)
-      family_patch_apply<D, K>(lane, (const unsigned short*)(smem + L.st + s * L.stride + L.sl) + w * NP, xs, acc, s0 + w * NP,
-                               s1 + w * NP, scale);
-    __syncthreads();
-    // ---- epilogue: R1 rows finished here, halo rows reduced into t
-    const int sh = m.x & 1;
-    for (int r = tid; r < m.y; r += NT) {
-      const int q = r + sh;
-      const long gi = (long)m.x + r;
-      const double a = acc[q];
-      acc[q] = 0.0;
-      if (MODE == CM_APPLY) {
-        t[gi] = a;
-      } else if (MODE == CM_RESID) {
-        t[gi] = ((const double*)(smem + L.st + s * L.stride + L.ge))[q] - a;
-      } else {
-        double dd = c2 * ((const double*)(smem + L.st + s * L.stride + L.de))[q] * (((const double*)(smem + L.st + s * L.stride + L.ge))[q] - a);
-        if (READ_DV) dd = fma(c1, ((const double*)(smem + L.st + s * L.stride + L.ve))[q], dd);
-        if (WRITE_DV) dv[gi] = dd;
-        x[gi] = xs[q] + dd;
-      }
-    }
-    const int* hl = (const int*)(smem + L.hi + (i % 3) * L.hstride) + (m.z & 3);
-    for (int j = tid; j < m.w; j += NT) {
-      const int q = m.y + 2 + j;
-      atomicAdd(t + hl[j], acc[q]);
-      acc[q] = 0.0;
-    }
-    __syncthreads();
-  }
-}
-
-// Finishes the rows of [a, a + n) whose operator values were reduced into t
-// (R2, R3): CM_RESID t = g - t; CM_CHEB the Chebyshev step with t reset to 0
-// (data-dependent zero, see cheb_step).
-template <int MODE, bool READ_DV, bool WRITE_DV>
-__global__ void __launch_bounds__(256) chunk_tail(long a, long n, const double* __restrict__ g,
-                                                  const double* __restrict__ Dinv, double* __restrict__ t,
-                                                  double* __restrict__ dv, double* __restrict__ x, double c1,
-                                                  double c2) {
-  const long i = a + (long)blockIdx.x * 256 + threadIdx.x;
-  if (i >= a + n) return;
-  const double T = t[i];
-  if (MODE == CM_RESID) {
-    t[i] = g[i] - T;
-  } else {
-    t[i] = T - T;
-    double dd = c2 * Dinv[i] * (g[i] - T);
-    if (READ_DV) dd = fma(c1, dv[i], dd);
-    if (WRITE_DV) dv[i] = dd;
-    x[i] += dd;
-  }
-}
-
-// dst[perm[i]] = src[i] (level order -> device order) and the inverse
-__global__ void permute_in(long n, const int* __restrict__ perm, const double* __restrict__ src,
-                           double* __restrict__ dst) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[perm[i]] = src[i];
-}
-__global__ void permute_out(long n, const int* __restrict__ perm, const double* __restrict__ src,
-                            double* __restrict__ dst) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src[perm[i]];
 }
 
 // cell_dofs is SoA: dof of local node b of cell c at cell_dofs[b * ldc + c]
@@ -665,7 +490,7 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const double2* __restrict__ 
 
 // ------------------------------------------------------------- transfers
 enum : int { XFER_ADD = 0, XFER_SET_E = 1 };
-enum : int { RES_PLAIN = 0, RES_T = 1, RES_EONLY = 2 };
+enum : int { RES_PLAIN = 0, RES_VCYCLE = 1, RES_EONLY = 2 };
 
 constexpr int XFER_NT = 128;
 constexpr int XFER_WARPS = 4;
@@ -744,9 +569,9 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
     const int i = fine[q];
     r[q] = 0.0;
     if (i >= 0) {
-      if (MODE == RES_T) {                    // r = t (formed by chunk_apply<CM_RESID>)
+      if (MODE == RES_VCYCLE) {
         const double tv = t[i];
-        r[q] = tv;
+        r[q] = v[i] - tv;
         t[i] = tv - tv;                       // data-dependent reset (see cheb_step)
       } else if (MODE == RES_EONLY) {
         r[q] = (cls_fine[i] & 1) ? v[i] : 0.0;

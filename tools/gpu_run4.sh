@@ -1,0 +1,12 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/bench.log 2>&1; echo bench=$?
+tail -c 1500 gpurun_out/bench.log | python -c "import sys,json; l=sys.stdin.read().strip().splitlines()[-1]; d=json.loads(l); print(d['ms_per_step'], d['value'], d['roofline']['launch_s'], d['cg'])"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --profile"
+$CMD > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+echo launches=$?
+ncu --set full --clock-control none --import-source on --profile-from-start off \
+    -k regex:chunk_apply -c 1 -o gpurun_out/prof_chunk -f $CMD > gpurun_out/ncu_full.log 2>&1
+echo full=$?
