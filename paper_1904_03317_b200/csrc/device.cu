@@ -183,7 +183,7 @@ static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const
                        cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
   DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, vin, t, dc)));
   d->launches++;
@@ -194,7 +194,7 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
                          cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  int grid = (int)((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS);
+  const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
   DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, xc, xf)));
   d->launches++;

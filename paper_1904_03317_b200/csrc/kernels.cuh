@@ -489,60 +489,130 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const double2* __restrict__ 
 }
 
 // ------------------------------------------------------------- transfers
+// Sum-factorised cell-wise transfers.  Warp per family
+// (the 2^d children of one refined level-(l-1) cell, "parent"), persistent
+// grid-stride loop.  The family's AoS row xfer[f] = [NP fine patch entries
+// (family-patch encoding) | NC coarse DoFs of the parent (-1 Dirichlet)] is
+// staged in shared memory, the next family's row is prefetched into registers
+// while the current one computes.  With the 1-D embedding P (Q<K>::P, (2k+1) x
+// (k+1)) the patch values are P (x) P (x) P applied to the parent's values:
+// prolongation runs the three 1-D passes coarse -> fine (x, y, z), restriction
+// the transposed passes fine -> coarse (z, y, x).  Each fine node is written
+// (prolongation) or summed (restriction) by the one family that owns it, which
+// makes both exactly P and P^T (reading R26 of DESIGN.md).
 enum : int { XFER_ADD = 0, XFER_SET_E = 1 };
 enum : int { RES_PLAIN = 0, RES_VCYCLE = 1, RES_EONLY = 2 };
 
-constexpr int XFER_NT = 128;
 constexpr int XFER_WARPS = 4;
 
-// Warp per family over the AoS transfer table xfer[f] = [NP fine patch entries
-// (fam_dofs encoding) | NC coarse DoFs of the parent (-1 Dirichlet)]: one
-// contiguous row per family, all indices fetched in one coalesced pass.
+// one 1-D pass over `lines` lines of a 3-index array: in(i, q, o) -> out(i, p, o),
+// out = sum_q M(p, q) in, with M = P (UP: q < N, p < NP1) or P^T (!UP)
+template <int K, bool UP, int NI, int NO>
+__device__ __forceinline__ void xfer_pass(int lane, const double* in, double* out, int si_in, int sq_in, int so_in,
+                                          int si_out, int sp_out, int so_out) {
+  constexpr int N = K + 1, NP1 = 2 * K + 1;
+  constexpr int NQ = UP ? N : NP1, NPo = UP ? NP1 : N;
+  for (int L = lane; L < NI * NO; L += 32) {
+    const int i = L / NO, o = L % NO;
+    double v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = in[i * si_in + q * sq_in + o * so_in];
+#pragma unroll
+    for (int p = 0; p < NPo; ++p) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const double m = UP ? Q<K>::P(p, q) : Q<K>::P(q, p);
+        if (m != 0.0) s = fma(m, v[q], s);
+      }
+      out[i * si_out + p * sp_out + o * so_out] = s;
+    }
+  }
+}
+
+template <int D, int K>
+struct XferShape {
+  static constexpr int N = K + 1, NP1 = 2 * K + 1, NC = Shape<D, K>::NN, NP = Shape<D, K>::NP, ROW = NP + NC;
+  static constexpr int NR = (ROW + 31) / 32;   // row words per lane
+};
+
+template <int D, int K>
+__device__ __forceinline__ void row_fetch(const int* __restrict__ xfer, const int* __restrict__ fam_list, int tt,
+                                          int lane, int (&r)[XferShape<D, K>::NR]) {
+  using S = XferShape<D, K>;
+  const int f = fam_list ? __ldg(fam_list + tt) : tt;
+  const int* row = xfer + (long)f * S::ROW;
+#pragma unroll
+  for (int q = 0; q < S::NR; ++q) r[q] = (lane + 32 * q < S::ROW) ? __ldg(row + lane + 32 * q) : -1;
+}
+
 template <int D, int K, int MODE>
 __global__ void __launch_bounds__(32 * XFER_WARPS)
 warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
                 const unsigned char* __restrict__ cls_fine, const double* __restrict__ xc, double* __restrict__ xf) {
-  constexpr int NC = Shape<D, K>::NN, NP = Shape<D, K>::NP, NP1 = 2 * K + 1, N = K + 1, ROW = NP + NC;
-  __shared__ double sc[XFER_WARPS][NC];
+  using S = XferShape<D, K>;
+  constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
+  __shared__ int srow[XFER_WARPS][S::ROW];
+  __shared__ double b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int t = blockIdx.x * XFER_WARPS + w;
-  if (t >= nfam) return;
-  const int f = fam_list ? __ldg(fam_list + t) : t;
-  const int* row = xfer + (long)f * ROW;
-  constexpr int NIT = (NP + 31) / 32;
-  int fine[NIT];
+  const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
+  if (gw >= nfam) return;
+  int nxt[S::NR];
+  row_fetch<D, K>(xfer, fam_list, gw, lane, nxt);
+  for (int tt = gw; tt < nfam; tt += GW) {
 #pragma unroll
-  for (int q = 0; q < NIT; ++q) fine[q] = (lane + 32 * q < NP) ? __ldg(row + lane + 32 * q) : -1;
-  if (lane < NC) {
-    const int ci = __ldg(row + NP + lane);
-    sc[w][lane] = ci >= 0 ? __ldg(xc + ci) : 0.0;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < NIT; ++q) {
-    const int a = lane + 32 * q;
-    const int v = fine[q];
-    if (a >= NP || v < 0) continue;                          // not owned / Dirichlet
-    if (MODE == XFER_SET_E && !(cls_fine[v] & 1)) continue;
-    double wx[N], wy[N], wz[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      wx[j] = Q<K>::P(a % NP1, j);
-      wy[j] = Q<K>::P((a / NP1) % NP1, j);
-      wz[j] = D == 3 ? Q<K>::P(a / (NP1 * NP1), j) : 1.0;
+    for (int q = 0; q < S::NR; ++q)
+      if (lane + 32 * q < S::ROW) srow[w][lane + 32 * q] = nxt[q];
+    __syncwarp();
+    if (tt + GW < nfam) row_fetch<D, K>(xfer, fam_list, tt + GW, lane, nxt);
+    const int* rw = srow[w];
+    if (lane < NC) {
+      const int ci = rw[NP + lane];
+      b0[w][lane] = ci >= 0 ? __ldg(xc + ci) : 0.0;
     }
-    double val = 0.0;
+    __syncwarp();
+    double* fine;
+    if constexpr (D == 3) {
+      // x: c[jz][jy][jx] -> b1[jz][jy][ax];  y: -> b0[jz][ay][ax];  z: -> b1[az][ay][ax]
+      xfer_pass<K, true, N * N, 1>(lane, b0[w], b1[w], N, 1, 0, NP1, 1, 0);
+      __syncwarp();
+      xfer_pass<K, true, N, NP1>(lane, b1[w], b0[w], N * NP1, NP1, 1, NP1 * NP1, NP1, 1);
+      __syncwarp();
+      xfer_pass<K, true, 1, NP1 * NP1>(lane, b0[w], b1[w], 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
+      fine = b1[w];
+    } else {
+      xfer_pass<K, true, N, 1>(lane, b0[w], b1[w], N, 1, 0, NP1, 1, 0);
+      __syncwarp();
+      xfer_pass<K, true, 1, NP1>(lane, b1[w], b0[w], 0, NP1, 1, 0, NP1, 1);
+      fine = b0[w];
+    }
+    __syncwarp();
+    constexpr int NIT = (NP + 31) / 32;
+    int vi[NIT];
+    double old[NIT];
 #pragma unroll
-    for (int jz = 0; jz < (D == 3 ? N : 1); ++jz)
-#pragma unroll
-      for (int jy = 0; jy < N; ++jy) {
-        double s = 0.0;
-#pragma unroll
-        for (int jx = 0; jx < N; ++jx) s = fma(wx[jx], sc[w][(jz * N + jy) * N + jx], s);
-        val = fma(wy[jy] * wz[jz], s, val);
+    for (int q = 0; q < NIT; ++q) {   // all loads first: one memory round trip per family
+      const int a = lane + 32 * q;
+      vi[q] = a < NP ? rw[a] : -1;    // < 0: not owned / Dirichlet
+      old[q] = 0.0;
+      if (vi[q] >= 0) {
+        if (MODE == XFER_SET_E) old[q] = (cls_fine[vi[q]] & 1) ? 1.0 : 0.0;
+        else old[q] = xf[vi[q]];
       }
-    if (MODE == XFER_SET_E) xf[v] = val;
-    else xf[v] += val;
+    }
+#pragma unroll
+    for (int q = 0; q < NIT; ++q) {
+      const int a = lane + 32 * q;
+      if (vi[q] < 0) continue;
+      if (MODE == XFER_SET_E) {
+        if (old[q] != 0.0) xf[vi[q]] = fine[a];
+      } else {
+        xf[vi[q]] = old[q] + fine[a];
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -551,62 +621,76 @@ __global__ void __launch_bounds__(32 * XFER_WARPS)
 warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
               const unsigned char* __restrict__ cls_fine, const double* __restrict__ v, double* __restrict__ t,
               double* __restrict__ dc) {
-  constexpr int NC = Shape<D, K>::NN, NP = Shape<D, K>::NP, NP1 = 2 * K + 1, N = K + 1, ROW = NP + NC;
-  __shared__ double sr[XFER_WARPS][NP];
+  using S = XferShape<D, K>;
+  constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
+  __shared__ int srow[XFER_WARPS][S::ROW];
+  __shared__ double b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int tt = blockIdx.x * XFER_WARPS + w;
-  if (tt >= nfam) return;
-  const int f = fam_list ? __ldg(fam_list + tt) : tt;
-  const int* row = xfer + (long)f * ROW;
-  constexpr int NIT = (NP + 31) / 32;
-  int fine[NIT];
+  const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
+  if (gw >= nfam) return;
+  int nxt[S::NR];
+  row_fetch<D, K>(xfer, fam_list, gw, lane, nxt);
+  for (int tt = gw; tt < nfam; tt += GW) {
 #pragma unroll
-  for (int q = 0; q < NIT; ++q) fine[q] = (lane + 32 * q < NP) ? __ldg(row + lane + 32 * q) : -1;
-  const int ci = lane < NC ? __ldg(row + NP + lane) : -1;
-  double r[NIT];
+    for (int q = 0; q < S::NR; ++q)
+      if (lane + 32 * q < S::ROW) srow[w][lane + 32 * q] = nxt[q];
+    __syncwarp();
+    if (tt + GW < nfam) row_fetch<D, K>(xfer, fam_list, tt + GW, lane, nxt);
+    const int* rw = srow[w];
+    // residual on the family's owned fine nodes (0 elsewhere); all loads first
+    constexpr int NIT = (NP + 31) / 32;
+    int ii[NIT];
+    double va[NIT], ta[NIT];
 #pragma unroll
-  for (int q = 0; q < NIT; ++q) {
-    const int i = fine[q];
-    r[q] = 0.0;
-    if (i >= 0) {
-      if (MODE == RES_VCYCLE) {
-        const double tv = t[i];
-        r[q] = v[i] - tv;
-        t[i] = tv - tv;                       // data-dependent reset (see cheb_step)
-      } else if (MODE == RES_EONLY) {
-        r[q] = (cls_fine[i] & 1) ? v[i] : 0.0;
-      } else {
-        r[q] = v[i];
+    for (int q = 0; q < NIT; ++q) {
+      const int a = lane + 32 * q;
+      ii[q] = a < NP ? rw[a] : -1;
+      va[q] = 0.0;
+      ta[q] = 0.0;
+      if (ii[q] >= 0) {
+        va[q] = v[ii[q]];
+        if (MODE == RES_VCYCLE) ta[q] = t[ii[q]];
+        if (MODE == RES_EONLY) ta[q] = (cls_fine[ii[q]] & 1) ? 0.0 : 1.0;
       }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < NIT; ++q)
-    if (lane + 32 * q < NP) sr[w][lane + 32 * q] = r[q];
-  __syncwarp();
-  if (lane < NC && ci >= 0) {
-    // fine coordinates with a nonzero weight for coarse node j_d: the coincident
-    // node 2 j_d and the odd (mid-edge) nodes 1 (and 3 for K = 2)
-    const int j = lane;
-    const int jj[3] = {j % N, (j / N) % N, D == 3 ? j / (N * N) : 0};
-    double s = 0.0;
-#pragma unroll
-    for (int qz = 0; qz < (D == 3 ? N : 1); ++qz) {
-      const int az = D == 3 ? (qz == 0 ? 2 * jj[2] : 2 * qz - 1) : 0;
-      const double wz = D == 3 ? Q<K>::P(az, jj[2]) : 1.0;
-#pragma unroll
-      for (int qy = 0; qy < N; ++qy) {
-        const int ay = qy == 0 ? 2 * jj[1] : 2 * qy - 1;
-        const double wyz = wz * Q<K>::P(ay, jj[1]);
-#pragma unroll
-        for (int qx = 0; qx < N; ++qx) {
-          const int ax = qx == 0 ? 2 * jj[0] : 2 * qx - 1;
-          const int a = ax + NP1 * ay + (D == 3 ? NP1 * NP1 * az : 0);
-          s = fma(wyz * Q<K>::P(ax, jj[0]), sr[w][a], s);
+    for (int q = 0; q < NIT; ++q) {
+      const int a = lane + 32 * q;
+      double r = 0.0;
+      if (ii[q] >= 0) {
+        if (MODE == RES_VCYCLE) {
+          r = va[q] - ta[q];
+          t[ii[q]] = ta[q] - ta[q];             // data-dependent reset (see cheb_step)
+        } else if (MODE == RES_EONLY) {
+          r = ta[q] == 0.0 ? va[q] : 0.0;
+        } else {
+          r = va[q];
         }
       }
+      if (a < NP) b0[w][a] = r;
     }
-    atomicAdd(dc + ci, s);
+    __syncwarp();
+    double* coarse;
+    if constexpr (D == 3) {
+      // z: r[az][ay][ax] -> b1[jz][ay][ax];  y: -> b0[jz][jy][ax];  x: -> b1[jz][jy][jx]
+      xfer_pass<K, false, 1, NP1 * NP1>(lane, b0[w], b1[w], 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
+      __syncwarp();
+      xfer_pass<K, false, N, NP1>(lane, b1[w], b0[w], NP1 * NP1, NP1, 1, N * NP1, NP1, 1);
+      __syncwarp();
+      xfer_pass<K, false, N * N, 1>(lane, b0[w], b1[w], NP1, 1, 0, N, 1, 0);
+      coarse = b1[w];
+    } else {
+      xfer_pass<K, false, 1, NP1>(lane, b0[w], b1[w], 0, NP1, 1, 0, NP1, 1);
+      __syncwarp();
+      xfer_pass<K, false, N, 1>(lane, b1[w], b0[w], NP1, 1, 0, N, 1, 0);
+      coarse = b0[w];
+    }
+    __syncwarp();
+    if (lane < NC) {
+      const int ci = rw[NP + lane];
+      if (ci >= 0) atomicAdd(dc + ci, coarse[lane]);
+    }
+    __syncwarp();
   }
 }
 
