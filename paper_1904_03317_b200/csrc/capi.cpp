@@ -199,10 +199,7 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
     h->topo = gmg::make_topology(f->f, p->p, prm->k);
     h->local = gmg::make_local(f->f, p->p, h->topo, prm->rank);
     if (!(prm->flags & GMG_HOST_ONLY)) {
-      if (prm->coef_level2) {
-        GMG_REQUIRE(f->f.L >= 2, GMG_E_INVALID_ARG, "coefficient per level-2 cell needs >= 3 levels");
-        gmg::fail(GMG_E_INVALID_ARG, "variable coefficient (config 4) is not supported by this build yet");
-      }
+      if (prm->coef_level2) gmg::attach_coefficients(h->local, f->f, p->p, prm->coef_level2);
       std::unique_ptr<gmg::Comm> comm;
       if (prm->n_ranks > 1) {
         GMG_REQUIRE(prm->nccl_comm != nullptr, GMG_E_INVALID_ARG, "n_ranks > 1 needs a communicator");

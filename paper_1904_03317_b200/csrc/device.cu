@@ -29,7 +29,9 @@ struct DevLevel {
   i64 n = 0, n_owned = 0, n_pad = 0, n_cells = 0, n_fam = 0, n_leaf = 0, n_edge = 0, off = 0;
   int* cell_dofs = nullptr;         // SoA [(k+1)^d][n_cells]
   long ldc = 0;
-  double* coef = nullptr;
+  double* coef = nullptr;           // config 4, levels >= 2: coefficient per local cell
+  double* fcoef = nullptr;          // config 4, levels >= 3: coefficient per local family
+  double* elem = nullptr;           // config 4, levels 0-1: [n_cells][nn][nn] element matrices
   unsigned char* cls = nullptr;     // bit0 = E
   double* Dinv = nullptr;           // n_pad entries, 0 on E rows, ghosts and padding
   int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
@@ -150,13 +152,19 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
-  if (list == nullptr && l > 0 && v.n_fam > 0 && v.coef == nullptr && d->tensor_apply) {
+  const bool full = list == nullptr && l > 0 && v.n_fam > 0;
+  if (v.elem) {                                   // config 4, levels 0-1: explicit element matrices
+    const int nt = 128;
+    const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
+    DISPATCH_DK(d->dim, d->k, (dev::cell_apply_dense<D_, K_><<<(int)((n * nn + nt - 1) / nt), nt, 0, s>>>(
+                                  (int)n, list, v.cell_dofs, v.ldc, v.elem, x, y)));
+  } else if (full && (v.coef == nullptr || v.fcoef != nullptr) && d->tensor_apply) {
     const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
     const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
     int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
     DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
-                                  (int)v.n_fam, v.xfer, np + nn, v.scale, x, y)));
-  } else if (list == nullptr && l > 0 && v.n_fam > 0) {
+                                  (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y)));
+  } else if (full) {                              // per-cell coefficients inside a family (config 4, level 2)
     DISPATCH_DK(d->dim, d->k, {
       constexpr int FPB = dev::FamCfg<D_, K_>::FPB;
       int grid = (int)((v.n_fam + FPB - 1) / FPB);
@@ -487,6 +495,9 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
         v.xfer = d->upload(t.xfer);
       }
       v.leaf_cells = d->upload(t.leaf_cells);
+      if (!t.cell_coef.empty()) v.coef = d->upload(t.cell_coef);
+      if (!t.fam_coef.empty()) v.fcoef = d->upload(t.fam_coef);
+      if (!t.cell_elem.empty()) v.elem = d->upload(t.cell_elem);
       v.edge_fams = d->upload(t.edge_fams);
       v.h = std::ldexp(1.0, -l);
       v.scale = Tp.dim == 3 ? v.h : 1.0;
@@ -534,7 +545,13 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     CK(cudaMemset(bad, 0, sizeof(int)));
     for (int l = 0; l <= Tp.L; ++l) {
       DevLevel& v = d->lv[l];
-      if (v.n_cells > 0) {
+      if (v.n_cells > 0 && v.elem) {
+        const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
+        DISPATCH_DK(d->dim, d->k,
+                    (dev::cell_diag_dense<D_, K_><<<(int)((v.n_cells * nn + 127) / 128), 128, 0, s>>>(
+                        (int)v.n_cells, v.cell_dofs, v.ldc, v.elem, v.Dinv)));
+        d->launches++;
+      } else if (v.n_cells > 0) {
         int grid = (int)((v.n_cells + 127) / 128);
         DISPATCH_DK(d->dim, d->k,
                     (dev::cell_diag<D_, K_><<<grid, 128, 0, s>>>((int)v.n_cells, v.cell_dofs, v.ldc, v.coef, v.scale,

@@ -129,6 +129,11 @@ struct LocalLevel {
   std::vector<uint8_t> cls, lam;           // per local DoF (ghosts: lam = 0)
   std::vector<double> eig_v;               // eigen start vector on owned S DoFs
   i64 nS_global = 0;
+  std::vector<i64> cell_global;            // global index (in C_l) of each local cell
+  // variable coefficient (config 4; empty = a == 1), see coef.cpp
+  std::vector<double> cell_coef;           // levels >= 2: a of each local cell
+  std::vector<double> fam_coef;            // levels >= 3: a of each local family (one per family)
+  std::vector<double> cell_elem;           // levels < 2: [n_cells][nn][nn] exact sub-box element matrices
   i64 n_local() const { return n_owned + n_ghost; }
 };
 
@@ -141,5 +146,9 @@ struct LocalTopo {
 };
 
 LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank);
+
+// Piecewise-constant coefficient per level-2 cell (config 4): coef2[i] belongs to
+// the i-th cell of C_2 in SFC order.  Fills the coefficient fields of every level.
+void attach_coefficients(LocalTopo& Lt, const Forest& f, const Partition& p, const double* coef2);
 
 }  // namespace gmg

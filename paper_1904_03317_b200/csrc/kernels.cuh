@@ -271,14 +271,15 @@ constexpr int TENSOR_WARPS = 8;
 
 template <int D, int K>
 __global__ void __launch_bounds__(32 * TENSOR_WARPS)
-fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, double scale, const double* __restrict__ x,
-                 double* __restrict__ y) {
+fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale,
+                 const double* __restrict__ x, double* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
   __shared__ double s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int f = blockIdx.x * TENSOR_WARPS + w;
   if (f >= nfam) return;
   const int* rp = xfer + (long)f * row;
+  if (fcoef) scale *= __ldg(fcoef + f);   // config 4: one coefficient per family (levels >= 3)
   double out[NP1];
   int ob = 0, os = 0;   // output line: base and stride in the patch
   if constexpr (D == 3) {
@@ -439,6 +440,38 @@ __global__ void cell_diag(int n, const int* __restrict__ cell_dofs, long ldc, co
     int i = cell_dofs[(long)b * ldc + c];
     if (i >= 0) atomicAdd(diag + i, s * elem_diag<D, K>(b));
   }
+}
+
+// Levels 0-1 of config 4: cells coarser than the coefficient patches carry an
+// explicit element matrix (exact sub-box integration, coef.cpp); y += A_c x_c
+// over a cell list (or all cells), thread per (cell, row).
+template <int D, int K>
+__global__ void cell_apply_dense(int n, const int* __restrict__ list, const int* __restrict__ cell_dofs, long ldc,
+                                 const double* __restrict__ elem, const double* __restrict__ x,
+                                 double* __restrict__ y) {
+  constexpr int NN = Shape<D, K>::NN;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * NN) return;
+  const int c = list ? list[t / NN] : t / NN, b = t % NN;
+  const int row = cell_dofs[(long)b * ldc + c];
+  if (row < 0) return;
+  const double* A = elem + ((long)c * NN + b) * NN;
+  double s = 0.0;
+  for (int q = 0; q < NN; ++q) {
+    const int col = cell_dofs[(long)q * ldc + c];
+    if (col >= 0) s = fma(A[q], x[col], s);
+  }
+  atomicAdd(y + row, s);
+}
+template <int D, int K>
+__global__ void cell_diag_dense(int n, const int* __restrict__ cell_dofs, long ldc, const double* __restrict__ elem,
+                                double* __restrict__ diag) {
+  constexpr int NN = Shape<D, K>::NN;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * NN) return;
+  const int c = t / NN, b = t % NN;
+  const int row = cell_dofs[(long)b * ldc + c];
+  if (row >= 0) atomicAdd(diag + row, elem[((long)c * NN + b) * NN + b]);
 }
 
 template <int D, int K>

@@ -113,6 +113,7 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
         }
     }
     v.n_cells = (i64)cellg[l].size();
+    v.cell_global = cellg[l];
     v.n_fam = (i64)famg[l].size();
   }
   auto local_of = [&](int l, i64 g) -> i32 {

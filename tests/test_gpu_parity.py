@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_1904_03317_b200 as G  # noqa: E402
-from gmg_inputs import config, uniform_pm1, STREAM_PROBE  # noqa: E402
+from gmg_inputs import config, uniform_pm1, log_uniform_coef, STREAM_PROBE  # noqa: E402
 from oracle import forest as F, mg  # noqa: E402
 
 OP_TOL = 1e-12
@@ -42,17 +42,25 @@ def pair(name, k=None, passes=-1, cfg_over=None):
         cfg.update(cfg_over)
     if k is not None:
         cfg["k"] = k
-    f, part, h = G.build_config(cfg, passes=passes)
+    coef = None
+    if cfg.get("coef") == "level2_log_uniform":       # config 4: a per level-2 cell, SFC order
+        coef = log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+    f, part, h = G.build_config(cfg, passes=passes, coef_level2=coef)
     of = F.generate(cfg, passes=passes)
-    oh = mg.build(of, cfg["k"])
+    oh = mg.build(of, cfg["k"], coef_level2=coef)
     _cache[key] = (h, oh, (f, part))
     return _cache[key]
 
 
-CASES = [("c1", None), ("c1", 2), ("c3p2", None), ("c3p2", 1)]
+# c4s: the config-4 recipe (variable coefficient, corner-graded) at a small size
+# (s = 2, lmax = 7): levels 0-1 exact sub-box matrices, level 2 per-cell and
+# levels >= 3 per-family coefficients are all exercised.
+C4S = {"s": 2, "lmax": 7}
+CASES = [("c1", None), ("c1", 2), ("c3p2", None), ("c3p2", 1), ("c4", None, -1, C4S), ("c4", 1, -1, C4S)]
 
 
-@pytest.fixture(scope="module", params=CASES, ids=[f"{n}-k{k}" for n, k in CASES])
+@pytest.fixture(scope="module", params=CASES,
+                ids=[f"{c[0]}{'s' if len(c) > 2 else ''}-k{c[1]}" for c in CASES])
 def hp(request):
     return pair(*request.param)
 
