@@ -12,7 +12,7 @@ import pytest
 import paper_1904_03317_b200 as G
 from oracle import forest as F, mg
 from oracle.spaces import parent_owner
-from gmg_inputs import config, uniform_pm1
+from gmg_inputs import config, uniform_pm1, log_uniform_coef
 
 
 # ------------------------------------------------------------------ oracle ghost sets
@@ -159,6 +159,12 @@ def _run_threads(fns):
         raise errs[0]
 
 
+def _coef(cfg):
+    if cfg.get("coef") == "level2_log_uniform":       # config 4: a per level-2 cell, SFC order
+        return log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+    return None
+
+
 def _local_group(cfg, p):
     import torch
     world = G.LocalWorld(p)
@@ -170,7 +176,7 @@ def _local_group(cfg, p):
     def setup(r):
         def fn():
             torch.cuda.set_device(0)
-            hs[r] = G.gmg_setup(lf, part, k=cfg["k"], rank=r, comm=world)
+            hs[r] = G.gmg_setup(lf, part, k=cfg["k"], rank=r, comm=world, coef_level2=_coef(cfg))
         return fn
 
     _run_threads([setup(r) for r in range(p)])
@@ -188,11 +194,15 @@ def test_nccl_transport_loads():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,p", [("c1", 2), ("c1", 3), ("c3p2", 2), ("c3p2", 4), ("c2", 3)])
+@pytest.mark.parametrize("name,p", [("c1", 2), ("c1", 3), ("c3p2", 2), ("c3p2", 4), ("c2", 3), ("c4s", 3)])
 def test_local_ranks_equal_single_rank(name, p):
     import torch
-    cfg = config(name)
-    _, _, h1 = G.build_config(cfg)
+    if name == "c4s":      # config-4 recipe at a small size (variable coefficient)
+        cfg = config("c4")
+        cfg.update(s=2, lmax=7)
+    else:
+        cfg = config(name)
+    _, _, h1 = G.build_config(cfg, coef_level2=_coef(cfg))
     n = h1.info()["n_leaf_free"]
     canon1 = h1.leaf_dofs()[3]
     b_can = uniform_pm1(n)
