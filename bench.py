@@ -175,7 +175,8 @@ def run_ours(args):
         uid = [G.gmg_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = G.NcclComm(uid[0], world, rank)
-    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, comm=comm)
+    mixed = args.precision == "mixed"
+    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, comm=comm, mixed=mixed)
     setup_s = time.time() - t0
     info = h.info()
     n_dofs = info["n_leaf_nodes"]
@@ -227,7 +228,8 @@ def run_ours(args):
     nL = info["level_dofs"][L]
     ncell = info["level_cells"][L]
     nn = (cfg["k"] + 1) ** cfg["dim"]
-    xa = torch.tensor(uniform_pm1(n_loc), device=dev, dtype=torch.float64)
+    vdt = torch.float32 if mixed else torch.float64
+    xa = torch.tensor(uniform_pm1(n_loc), device=dev, dtype=vdt)
     ya = torch.zeros_like(xa)
     for _ in range(3):
         h.level_apply_kernel(L, xa, ya)
@@ -241,7 +243,9 @@ def run_ours(args):
     a1.synchronize()
     t_apply = max_over_ranks(a0.elapsed_time(a1) / 1e3 / reps)
     # 16 B per level DoF (x read, y write) + 4 B x 27 index entries per cell
-    alg_bytes = (16 * nL + 4 * nn * ncell) / world
+    # (fp32 vectors in the mixed-precision V-cycle: 8 B per level DoF)
+    vb = 4 if mixed else 8
+    alg_bytes = (2 * vb * nL + 4 * nn * ncell) / world
     peak, peak_src = load_peaks()
     achieved = alg_bytes / t_apply / 1e9
     applies_per_vc = 2 * args.cheb_degree         # (m-1) pre + 1 residual + m post on every level
@@ -290,8 +294,9 @@ def run_ours(args):
         model = part.model()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32" if mixed else "f64", "data": "synthetic",
                "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
+                          "precision": "fp32 V-cycle in fp64 CG" if mixed else "fp64",
                           "n_leaf_dofs": n_dofs, "n_free_dofs": info["n_leaf_free"], "levels": info["n_levels"],
                           "level_dofs": info["level_dofs"], "k": cfg["k"], "dim": cfg["dim"],
                           "cheb_degree": args.cheb_degree, "global_batch": 1,
@@ -302,7 +307,8 @@ def run_ours(args):
                           "partition_eta": model["eta"], "setup_s": round(setup_s, 2)},
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": None,
-                            "kernel": "fam_tensor_apply<3,2> (level operator), finest level",
+                            "kernel": "fam_tensor_apply<3,2,%s> (level operator), finest level"
+                                      % ("float" if mixed else "double"),
                             "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,
                             "share_of_step": share, "peak_source": peak_src},
                "cpu_baseline": cpu,
@@ -330,6 +336,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--cheb-degree", type=int, default=4)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
+                    help="fp64 V-cycle (default, BASELINE) or fp32 V-cycle inside the fp64 CG (P:897)")
     ap.add_argument("--profile", action="store_true", help="cudaProfilerStart/Stop around one V-cycle")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -149,6 +149,9 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
  */
 #define GMG_HOST_ONLY 1u      /* integer topology only, no device data (exports, CPU tests) */
 #define GMG_NO_GRAPH 2u       /* do not capture the V-cycle in a CUDA graph */
+#define GMG_MIXED_PRECISION 8u /* V-cycle in fp32 (vectors, operators, smoother, transfers;
+                                 P:897) inside the fp64 CG; gmg_vcycle keeps its
+                                 fp64 interface (conversion at copy_to/from_mg) */
 #define GMG_LOCAL_RANKS 4u    /* all n_ranks ranks live in this process (one host thread and
                                  stream each, same GPU); params.nccl_comm is a gmg_local_world */
 
@@ -266,6 +269,10 @@ gmg_status gmg_level_apply(gmg_hierarchy *h, int level, const double *x_dev, dou
  * work per launch). */
 gmg_status gmg_level_apply_kernel(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
                                   void *cuda_stream);
+/* The same kernel in fp32 (the operator of the mixed-precision V-cycle,
+ * GMG_MIXED_PRECISION): x_dev, y_dev are float arrays of the rank-local length. */
+gmg_status gmg_level_apply_kernel_f32(gmg_hierarchy *h, int level, const float *x_dev, float *y_dev,
+                                      void *cuda_stream);
 /* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1) */
 gmg_status gmg_restrict(gmg_hierarchy *h, int level, const double *r_fine_dev,
                         double *d_coarse_dev, void *cuda_stream);

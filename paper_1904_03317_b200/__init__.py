@@ -44,6 +44,7 @@ STATUS = {0: "GMG_OK", 1: "GMG_E_INVALID_ARG", 2: "GMG_E_UNSORTED", 3: "GMG_E_NO
 GMG_CLOSE_BALANCE = 1
 GMG_HOST_ONLY = 1
 GMG_NO_GRAPH = 2
+GMG_MIXED_PRECISION = 8
 MAX_LEVELS = 64
 
 
@@ -120,6 +121,7 @@ _SIGS = {
     "gmg_rhs_constant": ([_vp, C.c_double, _vp, _vp], C.c_int),
     "gmg_level_apply": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_level_apply_kernel": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_level_apply_kernel_f32": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_restrict": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_prolongate": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_leaf_apply": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -360,7 +362,11 @@ class Hierarchy:
         _check(_lib.gmg_level_apply(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
 
     def level_apply_kernel(self, level, x, y, stream=None):
-        _check(_lib.gmg_level_apply_kernel(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
+        """Rank-local kernel only (timing); fp64 tensors, or fp32 tensors for the
+        operator of the mixed-precision V-cycle."""
+        import torch
+        fn = _lib.gmg_level_apply_kernel_f32 if x.dtype == torch.float32 else _lib.gmg_level_apply_kernel
+        _check(fn(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
 
     def restrict(self, level, r, dc, stream=None):
         _check(_lib.gmg_restrict(self.h, level, _ptr(r), _ptr(dc), _stream(stream)))
@@ -428,7 +434,7 @@ class NcclComm:
 
 
 def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
-              coef_level2=None, graph=True, device=-1, comm=None) -> Hierarchy:
+              coef_level2=None, graph=True, device=-1, comm=None, mixed=False) -> Hierarchy:
     """comm: None (one rank), a LocalWorld (ranks as threads) or an NcclComm."""
     p = gmg_params_default()
     p.k = k
@@ -436,7 +442,8 @@ def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_deg
     p.rank = rank
     p.n_ranks = part.n_ranks
     p.device = device
-    p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH)
+    p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH) | \
+        (GMG_MIXED_PRECISION if mixed else 0)
     if isinstance(comm, LocalWorld):
         p.flags |= GMG_LOCAL_RANKS
         p.nccl_comm = comm.h

@@ -403,6 +403,16 @@ gmg_status gmg_level_apply_kernel(gmg_hierarchy* h, int level, const double* x, 
   });
 }
 
+gmg_status gmg_level_apply_kernel_f32(gmg_hierarchy* h, int level, const float* x, float* y, void* s) {
+  return guard([&] {
+    NEED(h);
+    NEED(x);
+    NEED(y);
+    need_level(h, level);
+    gmg::device_level_apply_kernel_f32(need_dev(h), level, x, y, s);
+  });
+}
+
 gmg_status gmg_restrict(gmg_hierarchy* h, int level, const double* r, double* dc, void* s) {
   return guard([&] {
     NEED(h);

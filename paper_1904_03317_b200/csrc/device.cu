@@ -34,6 +34,7 @@ struct DevLevel {
   double* elem = nullptr;           // config 4, levels 0-1: [n_cells][nn][nn] element matrices
   unsigned char* cls = nullptr;     // bit0 = E
   double* Dinv = nullptr;           // n_pad entries, 0 on E rows, ghosts and padding
+  float* Dinv32 = nullptr;          // the same in fp32 (mixed-precision V-cycle)
   int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   int* leaf_cells = nullptr;
@@ -58,6 +59,10 @@ struct DeviceHierarchy {
   std::vector<DevLevel> lv;
   i64 N = 0, n_leaf = 0, n0_global = 0;
   double *D = nullptr, *X = nullptr, *T = nullptr, *DV = nullptr, *W = nullptr, *Y = nullptr;
+  // mixed precision (GMG_MIXED_PRECISION): the V-cycle runs on fp32 copies
+  // of the MG-layout buffers; CG and the setup stay fp64
+  bool mixed = false;
+  float *D32 = nullptr, *X32 = nullptr, *T32 = nullptr, *DV32 = nullptr;
   double *cx = nullptr, *cr = nullptr, *cp = nullptr, *cq = nullptr, *cz = nullptr;
   double *sbuf = nullptr, *rbuf = nullptr;
   unsigned char* lam_mg = nullptr;
@@ -111,32 +116,51 @@ struct DeviceHierarchy {
     else { constexpr int D_ = 3, K_ = 2; __VA_ARGS__; }             \
   } while (0)
 
+// ---------------------------------------------------------------- V-cycle buffers by precision
+template <typename T> struct MG;
+template <> struct MG<double> {
+  static double* D(DeviceHierarchy* d) { return d->D; }
+  static double* X(DeviceHierarchy* d) { return d->X; }
+  static double* T(DeviceHierarchy* d) { return d->T; }
+  static double* DV(DeviceHierarchy* d) { return d->DV; }
+  static double* Dinv(DevLevel& v) { return v.Dinv; }
+};
+template <> struct MG<float> {
+  static float* D(DeviceHierarchy* d) { return d->D32; }
+  static float* X(DeviceHierarchy* d) { return d->X32; }
+  static float* T(DeviceHierarchy* d) { return d->T32; }
+  static float* DV(DeviceHierarchy* d) { return d->DV32; }
+  static float* Dinv(DevLevel& v) { return v.Dinv32; }
+};
+
 // ---------------------------------------------------------------- exchanges
 // ghosts <- owners (copy)
-static void import_ghosts(DeviceHierarchy* d, int l, double* vec, cudaStream_t s) {
+template <typename T>
+static void import_ghosts(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
   if (v.n_send) {
-    dev::pack<<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, d->sbuf);
+    dev::pack<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, d->sbuf);
     d->launches++;
   }
   d->comm->exchange(v.peers, d->sbuf, v.send_off, d->rbuf, v.recv_off, s);
   if (v.n_recv) {
-    dev::unpack_set<<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, d->rbuf, vec);
+    dev::unpack_set<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, d->rbuf, vec);
     d->launches++;
   }
 }
 // owners += ghosts; ghosts := 0
-static void export_add(DeviceHierarchy* d, int l, double* vec, cudaStream_t s) {
+template <typename T>
+static void export_add(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
   if (v.n_recv) {
-    dev::pack_zero<<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, d->sbuf);
+    dev::pack_zero<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, d->sbuf);
     d->launches++;
   }
   d->comm->exchange(v.peers, d->sbuf, v.recv_off, d->rbuf, v.send_off, s);
   if (v.n_send) {
-    dev::unpack_add<<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, d->rbuf, vec);
+    dev::unpack_add<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, d->rbuf, vec);
     d->launches++;
   }
 }
@@ -149,119 +173,125 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 // cells.  Full levels >= 1 run family-blocked (y must be zero on entry:
 // patch-interior nodes are stored, not added); level 0 and cell lists run
 // thread-per-cell.
-static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const double* x, double* y, cudaStream_t s) {
+template <typename T>
+static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* x, T* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
   const bool full = list == nullptr && l > 0 && v.n_fam > 0;
   if (v.elem) {                                   // config 4, levels 0-1: explicit element matrices
     const int nt = 128;
     const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
-    DISPATCH_DK(d->dim, d->k, (dev::cell_apply_dense<D_, K_><<<(int)((n * nn + nt - 1) / nt), nt, 0, s>>>(
+    DISPATCH_DK(d->dim, d->k, (dev::cell_apply_dense<D_, K_, T><<<(int)((n * nn + nt - 1) / nt), nt, 0, s>>>(
                                   (int)n, list, v.cell_dofs, v.ldc, v.elem, x, y)));
   } else if (full && (v.coef == nullptr || v.fcoef != nullptr) && d->tensor_apply) {
     const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
     const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
     int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
-    DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+    DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
                                   (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y)));
   } else if (full) {                              // per-cell coefficients inside a family (config 4, level 2)
     DISPATCH_DK(d->dim, d->k, {
       constexpr int FPB = dev::FamCfg<D_, K_>::FPB;
       int grid = (int)((v.n_fam + FPB - 1) / FPB);
-      dev::fam_apply<D_, K_><<<grid, FPB * (1 << D_), 0, s>>>((int)v.n_fam, v.fam_dofs, v.coef, v.scale, x, y);
+      dev::fam_apply<D_, K_, T><<<grid, FPB * (1 << D_), 0, s>>>((int)v.n_fam, v.fam_dofs, v.coef, v.scale, x, y);
     });
   } else {
     const int nt = 128;
     int grid = (int)((n + nt - 1) / nt);
-    DISPATCH_DK(d->dim, d->k, (dev::cell_apply<D_, K_><<<grid, nt, 0, s>>>((int)n, list, v.cell_dofs, v.ldc, v.coef,
+    DISPATCH_DK(d->dim, d->k, (dev::cell_apply<D_, K_, T><<<grid, nt, 0, s>>>((int)n, list, v.cell_dofs, v.ldc, v.coef,
                                                                               v.scale, x, y)));
   }
   d->launches++;
 }
 
 // t = K_l x on owned rows: ghost import of x, local family apply, export-add of t
-static void apply_full(DeviceHierarchy* d, int l, double* x, double* t, cudaStream_t s) {
+template <typename T>
+static void apply_full(DeviceHierarchy* d, int l, T* x, T* t, cudaStream_t s) {
   import_ghosts(d, l, x, s);
   k_apply(d, l, nullptr, d->lv[l].n_cells, x, t, s);
   export_add(d, l, t, s);
 }
 
-template <int MODE>
-static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const double* vin, double* t, double* dc,
+template <int MODE, typename T>
+static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const T* vin, T* t, T* dc,
                        cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
   const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
-  DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+  DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE, T><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, vin, t, dc)));
   d->launches++;
 }
 
-template <int MODE>
-static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, const double* xc, double* xf,
+template <int MODE, typename T>
+static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, const T* xc, T* xf,
                          cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
   const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
-  DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+  DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE, T><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, xc, xf)));
   d->launches++;
 }
 
-template <bool RT, bool RDV, bool WDV, bool XZ>
-static void k_cheb(DeviceHierarchy* d, DevLevel& v, const double* g, double* t, double* dv, double* x, double c1,
-                   double c2, cudaStream_t s) {
+template <typename T, bool RT, bool RDV, bool WDV, bool XZ>
+static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* x, double c1, double c2,
+                   cudaStream_t s) {
   if (v.n_pad == 0) return;
+  using V2 = typename dev::Vec2<T>::type;
   // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
-  dev::cheb_step<RT, RDV, WDV, XZ><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
-      (const double2*)g, (const double2*)v.Dinv, (double2*)t, (double2*)dv, (double2*)x, c1, c2);
+  dev::cheb_step<T, RT, RDV, WDV, XZ><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
+      (const V2*)g, (const V2*)MG<T>::Dinv(v), (V2*)t, (V2*)dv, (V2*)x, c1, c2);
   d->launches++;
 }
 
 // Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
 // first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
 // x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows and ghosts keeps those entries fixed).
-static void smooth(DeviceHierarchy* d, int l, const double* g, double* x, double* t, double* dv, bool x_zero,
-                   cudaStream_t s) {
+template <typename T>
+static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, bool x_zero, cudaStream_t s) {
   DevLevel& v = d->lv[l];
   const int m = d->m;
   if (x_zero) {
-    k_cheb<false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    k_cheb<T, false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else {
     apply_full(d, l, x, t, s);
-    if (m == 1) k_cheb<true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
-    else k_cheb<true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    if (m == 1) k_cheb<T, true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    else k_cheb<T, true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   }
   for (int j = 1; j < m; ++j) {
     apply_full(d, l, x, t, s);
-    if (j == m - 1) k_cheb<true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
-    else k_cheb<true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
+    if (j == m - 1) k_cheb<T, true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
+    else k_cheb<T, true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
   }
 }
 
-static void coarse(DeviceHierarchy* d, const double* d0, double* x0, cudaStream_t s) {
+template <typename T>
+static void coarse(DeviceHierarchy* d, const T* d0, T* x0, cudaStream_t s) {
   if (d->nS0 == 0) return;
-  dev::coarse_solve<<<1, 256, 0, s>>>(d->nS0, d->coarse_idx, d->coarse_inv, d0, x0);
+  dev::coarse_solve<T><<<1, 256, 0, s>>>(d->nS0, d->coarse_idx, d->coarse_inv, d0, x0);
   d->launches++;
 }
 
 // The V-cycle on the MG-layout buffers D (defects, copy_to_mg done), X (out).
+template <typename T>
 static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
   const int L = d->L;
+  T *D = MG<T>::D(d), *X = MG<T>::X(d), *Tb = MG<T>::T(d), *DV = MG<T>::DV(d);
   for (int l = L; l >= 1; --l) {
     DevLevel& v = d->lv[l];
-    double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
-    double* gc = d->D + d->lv[l - 1].off;
+    T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
+    T* gc = D + d->lv[l - 1].off;
     smooth(d, l, g, x, t, dv, true, s);                                     // 1: pre-smooth from 0
     apply_full(d, l, x, t, s);                                              // 2: t = K x
     k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
     export_add(d, l - 1, gc, s);
   }
-  coarse(d, d->D + d->lv[0].off, d->X + d->lv[0].off, s);                   // 4: coarse solve (rank 0)
+  coarse(d, D + d->lv[0].off, X + d->lv[0].off, s);                         // 4: coarse solve (rank 0)
   for (int l = 1; l <= L; ++l) {
     DevLevel& v = d->lv[l];
-    double *g = d->D + v.off, *x = d->X + v.off, *t = d->T + v.off, *dv = d->DV + v.off;
-    double* xc = d->X + d->lv[l - 1].off;
+    T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
+    T* xc = X + d->lv[l - 1].off;
     import_ghosts(d, l - 1, xc, s);
     k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, xc, x, s);         // 5: x += P x_{l-1}
     smooth(d, l, g, x, t, dv, false, s);                                    // 6: post-smooth
@@ -270,14 +300,16 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
 
 static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s) {
   if (!d->use_graph) {
-    vcycle_levels(d, s);
+    if (d->mixed) vcycle_levels<float>(d, s);
+    else vcycle_levels<double>(d, s);
     return;
   }
   if (!d->vgraph) {
     long long before = d->launches;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal));
-    vcycle_levels(d, d->cap);
+    if (d->mixed) vcycle_levels<float>(d, d->cap);
+    else vcycle_levels<double>(d, d->cap);
     CK(cudaStreamEndCapture(d->cap, &g));
     CK(cudaGraphInstantiate(&d->vgraph, g, 0));
     CK(cudaGraphDestroy(g));
@@ -304,7 +336,7 @@ static void leaf_apply_mg(DeviceHierarchy* d, const double* p, double* q, double
     k_apply(d, l, d->lv[l].leaf_cells, d->lv[l].n_leaf, d->W + d->lv[l].off, d->Y + d->lv[l].off, s);
   for (int l = L; l >= 1; --l) {
     export_add(d, l, d->Y + d->lv[l].off, s);
-    k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
+    k_restrict<dev::RES_EONLY, double>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
                                d->Y + d->lv[l - 1].off, s);
   }
   export_add(d, 0, d->Y + d->lv[0].off, s);
@@ -457,6 +489,7 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     d->eig_iters = prm.eig_iters;
     d->n0_global = n0_global;
     d->use_graph = !(prm.flags & GMG_NO_GRAPH) && (!d->comm || d->comm->capturable());
+    d->mixed = (prm.flags & GMG_MIXED_PRECISION) != 0;
     if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
@@ -630,6 +663,18 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     }
     // restore the work buffers to zero (T must be zero between applies)
     for (double* p : {d->X, d->T, d->DV, d->W, d->Y}) CK(cudaMemsetAsync(p, 0, N * sizeof(double), s));
+    if (d->mixed) {   // fp32 V-cycle buffers; D^-1 rounded once from the fp64 diagonal
+      for (float** p : {&d->D32, &d->X32, &d->T32, &d->DV32}) {
+        *p = d->alloc<float>(N);
+        CK(cudaMemsetAsync(*p, 0, N * sizeof(float), s));
+      }
+      for (int l = 0; l <= Tp.L; ++l) {
+        DevLevel& v = d->lv[l];
+        v.Dinv32 = d->alloc<float>(v.n_pad);
+        dev::cast_vec<float><<<d->vgrid(v.n_pad), 256, 0, s>>>(v.n_pad, v.Dinv, v.Dinv32);
+        d->launches++;
+      }
+    }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
   } catch (...) {
@@ -653,14 +698,31 @@ void device_destroy(DeviceHierarchy* d) {
 void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int gr = d->vgrid(d->N);
-  dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);            // copy_to_mg
+  if (d->mixed) dev::gather_to_mg<float><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32);   // copy_to_mg
+  else dev::gather_to_mg<double><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);
   d->launches++;
   run_vcycle_mg(d, s);
-  if (d->n_leaf) {
-    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);  // copy_from_mg
+  if (d->n_leaf) {                                                                              // copy_from_mg
+    if (d->mixed) dev::gather_from_mg<float><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X32, x);
+    else dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
+}
+
+// z = V(r) (MG layout, fp64 in and out; the V-cycle itself in fp32 if mixed), (r, z) partials
+static void precondition(DeviceHierarchy* d, cudaStream_t s) {
+  const i64 N = d->N;
+  if (d->mixed) {
+    dev::cast_vec<float><<<d->vgrid(N), 256, 0, s>>>(N, d->cr, d->D32);
+    d->launches++;
+  } else {
+    CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  run_vcycle_mg(d, s);
+  if (d->mixed) dev::mask_copy_dot<float><<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X32, d->cr, d->cz, d->partial);
+  else dev::mask_copy_dot<double><<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
+  d->launches++;
 }
 
 static void global_dot_into(DeviceHierarchy* d, int slot, cudaStream_t s) {
@@ -675,7 +737,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
   const i64 N = d->N;
   const int gr = d->vgrid(N);
   // r = b (MG layout), x = 0
-  dev::gather_to_mg<<<gr, 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
+  dev::gather_to_mg<double><<<gr, 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
   CK(cudaMemsetAsync(d->cx, 0, N * sizeof(double), s));
   d->launches++;
   double nb = std::sqrt(host_dot(d, N, d->cr, d->cr, s));
@@ -684,10 +746,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
   int status = 0;
   if (nb > 0) {
     // z = V(r); p = z; rz = (r, z) -> scal[0]
-    CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    run_vcycle_mg(d, s);
-    dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
-    d->launches++;
+    precondition(d, s);
     global_dot_into(d, 0, s);
     CK(cudaMemcpyAsync(d->cp, d->cz, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     status = 1;
@@ -705,10 +764,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
         break;
       }
       if (it == max_it) break;
-      CK(cudaMemcpyAsync(d->D, d->cr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      run_vcycle_mg(d, s);                                                      // z = V(r)
-      dev::mask_copy_dot<<<d->nred, dev::RED_NT, 0, s>>>(N, d->lam_mg, d->X, d->cr, d->cz, d->partial);
-      d->launches++;
+      precondition(d, s);                                                       // z = V(r)
       global_dot_into(d, 2, s);
       dev::cg_update_p<<<gr, 256, 0, s>>>(N, d->scal, d->cz, d->cp);            // p = z + beta p
       dev::copy_scalar<<<1, 1, 0, s>>>(d->scal + 2, d->scal + 0);
@@ -717,7 +773,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
     if (it > max_it) it = max_it;
   }
   if (d->n_leaf) {
-    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
+    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
@@ -740,12 +796,12 @@ void device_rhs_constant(DeviceHierarchy* d, double f, double* b, void* stream) 
   }
   for (int l = d->L; l >= 1; --l) {
     export_add(d, l, d->Y + d->lv[l].off, s);
-    k_restrict<dev::RES_EONLY>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
+    k_restrict<dev::RES_EONLY, double>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
                                d->Y + d->lv[l - 1].off, s);
   }
   export_add(d, 0, d->Y + d->lv[0].off, s);
   if (d->n_leaf) {
-    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
+    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
@@ -771,9 +827,15 @@ void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, doubl
   CK(cudaPeekAtLastError());
 }
 
+void device_level_apply_kernel_f32(DeviceHierarchy* d, int l, const float* x, float* y, void* stream) {
+  DevLevel& v = d->lv[l];
+  k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
+  CK(cudaPeekAtLastError());
+}
+
 void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
   need_single(d);
-  k_restrict<dev::RES_PLAIN>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
+  k_restrict<dev::RES_PLAIN, double>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
 }
 
@@ -786,11 +848,11 @@ void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, 
 void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int gr = d->vgrid(d->N);
-  dev::gather_to_mg<<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
+  dev::gather_to_mg<double><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
   d->launches++;
   leaf_apply_mg(d, d->cp, d->cq, d->partial, s);
   if (d->n_leaf) {
-    dev::gather_from_mg<<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
+    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
     d->launches++;
   }
   CK(cudaPeekAtLastError());

@@ -20,6 +20,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b_leaf, double* x_leaf, do
 void device_rhs_constant(DeviceHierarchy* d, double f, double* b_leaf, void* stream);
 void device_level_apply(DeviceHierarchy* d, int level, const double* x, double* y, void* stream);
 void device_level_apply_kernel(DeviceHierarchy* d, int level, const double* x, double* y, void* stream);
+void device_level_apply_kernel_f32(DeviceHierarchy* d, int level, const float* x, float* y, void* stream);
 void device_restrict(DeviceHierarchy* d, int level, const double* r, double* dc, void* stream);
 void device_prolongate(DeviceHierarchy* d, int level, const double* xc, double* xf, void* stream);
 void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* stream);

@@ -71,20 +71,20 @@ template <int D, int K> struct Shape {
 };
 
 // out = A_ref u on one cell (x fastest local numbering)
-template <int D, int K>
-__device__ __forceinline__ void elem_apply(const double (&u)[Shape<D, K>::NN], double (&out)[Shape<D, K>::NN]) {
+template <int D, int K, typename T>
+__device__ __forceinline__ void elem_apply(const T (&u)[Shape<D, K>::NN], T (&out)[Shape<D, K>::NN]) {
   constexpr int N = K + 1;
   if constexpr (D == 2) {
-    double a[N * N], b[N * N];
+    T a[N * N], b[N * N];
 #pragma unroll
     for (int y = 0; y < N; ++y)
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        double sa = 0, sb = 0;
+        T sa = 0, sb = 0;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-          sa = fma(Q<K>::Km(x, q), u[y * N + q], sa);
-          sb = fma(Q<K>::Mm(x, q), u[y * N + q], sb);
+          sa = fma((T)Q<K>::Km(x, q), u[y * N + q], sa);
+          sb = fma((T)Q<K>::Mm(x, q), u[y * N + q], sb);
         }
         a[y * N + x] = sa;
         b[y * N + x] = sb;
@@ -93,46 +93,46 @@ __device__ __forceinline__ void elem_apply(const double (&u)[Shape<D, K>::NN], d
     for (int y = 0; y < N; ++y)
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        double s = 0;
+        T s = 0;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-          s = fma(Q<K>::Mm(y, q), a[q * N + x], s);
-          s = fma(Q<K>::Km(y, q), b[q * N + x], s);
+          s = fma((T)Q<K>::Mm(y, q), a[q * N + x], s);
+          s = fma((T)Q<K>::Km(y, q), b[q * N + x], s);
         }
         out[y * N + x] = s;
       }
   } else {
     constexpr int NN = N * N * N;
-    double t1[NN], t2[NN];
+    T t1[NN], t2[NN];
     // z direction: t1 = M_z u, t2 = K_z u
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int yx = 0; yx < N * N; ++yx) {
-        double s1 = 0, s2 = 0;
+        T s1 = 0, s2 = 0;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-          s1 = fma(Q<K>::Mm(z, q), u[q * N * N + yx], s1);
-          s2 = fma(Q<K>::Km(z, q), u[q * N * N + yx], s2);
+          s1 = fma((T)Q<K>::Mm(z, q), u[q * N * N + yx], s1);
+          s2 = fma((T)Q<K>::Km(z, q), u[q * N * N + yx], s2);
         }
         t1[z * N * N + yx] = s1;
         t2[z * N * N + yx] = s2;
       }
     // y direction: a = M_y t1, b = K_y t1 + M_y t2
-    double a[NN], b[NN];
+    T a[NN], b[NN];
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
       for (int y = 0; y < N; ++y)
 #pragma unroll
         for (int x = 0; x < N; ++x) {
-          double sa = 0, sb = 0;
+          T sa = 0, sb = 0;
 #pragma unroll
           for (int q = 0; q < N; ++q) {
             const int iq = z * N * N + q * N + x;
-            sa = fma(Q<K>::Mm(y, q), t1[iq], sa);
-            sb = fma(Q<K>::Km(y, q), t1[iq], sb);
-            sb = fma(Q<K>::Mm(y, q), t2[iq], sb);
+            sa = fma((T)Q<K>::Mm(y, q), t1[iq], sa);
+            sb = fma((T)Q<K>::Km(y, q), t1[iq], sb);
+            sb = fma((T)Q<K>::Mm(y, q), t2[iq], sb);
           }
           a[z * N * N + y * N + x] = sa;
           b[z * N * N + y * N + x] = sb;
@@ -142,11 +142,11 @@ __device__ __forceinline__ void elem_apply(const double (&u)[Shape<D, K>::NN], d
     for (int zy = 0; zy < N * N; ++zy)
 #pragma unroll
       for (int x = 0; x < N; ++x) {
-        double s = 0;
+        T s = 0;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-          s = fma(Q<K>::Km(x, q), a[zy * N + q], s);
-          s = fma(Q<K>::Mm(x, q), b[zy * N + q], s);
+          s = fma((T)Q<K>::Km(x, q), a[zy * N + q], s);
+          s = fma((T)Q<K>::Mm(x, q), b[zy * N + q], s);
         }
         out[zy * N + x] = s;
       }
@@ -181,15 +181,15 @@ __device__ __forceinline__ int decode_dof(int v) { return v >= 0 ? v : (v <= -2 
 // ------------------------------------------------------------- level operator
 template <int D, int K> struct FamCfg { static constexpr int FPB = D == 3 ? 16 : 32; };
 
-template <int D, int K>
+template <int D, int K, typename T>
 __global__ void __launch_bounds__(FamCfg<D, K>::FPB * (1 << D))
 fam_apply(int nfam, const int* __restrict__ fam_dofs, const double* __restrict__ coef, double scale,
-          const double* __restrict__ x, double* __restrict__ y) {
+          const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NN = Shape<D, K>::NN, NP = Shape<D, K>::NP, NCH = Shape<D, K>::NCH;
   constexpr int NP1 = 2 * K + 1, N = K + 1;
   constexpr int FPB = FamCfg<D, K>::FPB, NT = FPB * NCH;
   __shared__ int sidx[FPB * NP];
-  __shared__ double sout[NT * NN];
+  __shared__ T sout[NT * NN];
   const int tid = threadIdx.x;
   const long fam0 = (long)blockIdx.x * FPB;
   const int nf_here = (int)min((long)FPB, (long)nfam - fam0);
@@ -201,14 +201,14 @@ fam_apply(int nfam, const int* __restrict__ fam_dofs, const double* __restrict__
   __syncthreads();
   const int fl = tid / NCH, c = tid % NCH;
   if (fl < nf_here) {
-    double u[NN], v[NN];
+    T u[NN], v[NN];
 #pragma unroll
     for (int b = 0; b < NN; ++b) {
       const int i = decode_dof(sidx[fl * NP + patch_of<D, K>(c, b)]);
-      u[b] = i >= 0 ? __ldg(x + i) : 0.0;
+      u[b] = i >= 0 ? __ldg(x + i) : T(0);
     }
-    elem_apply<D, K>(u, v);
-    const double s = coef ? scale * __ldg(coef + (fam0 + fl) * NCH + c) : scale;
+    elem_apply<D, K, T>(u, v);
+    const T s = (T)(coef ? scale * __ldg(coef + (fam0 + fl) * NCH + c) : scale);
 #pragma unroll
     for (int b = 0; b < NN; ++b) sout[tid * NN + b] = s * v[b];
   }
@@ -221,7 +221,7 @@ fam_apply(int nfam, const int* __restrict__ fam_dofs, const double* __restrict__
     bool interior = true;
 #pragma unroll
     for (int j = 0; j < D; ++j) interior &= (ad[j] > 0 && ad[j] < 2 * K);
-    double sum = 0.0;
+    T sum = 0;
 #pragma unroll
     for (int cc = 0; cc < NCH; ++cc) {
       bool in = true;
@@ -269,18 +269,18 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
 
 constexpr int TENSOR_WARPS = 8;
 
-template <int D, int K>
+template <int D, int K, typename T>
 __global__ void __launch_bounds__(32 * TENSOR_WARPS)
-fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale,
-                 const double* __restrict__ x, double* __restrict__ y) {
+fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
+                 const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
-  __shared__ double s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
+  __shared__ T s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int f = blockIdx.x * TENSOR_WARPS + w;
   if (f >= nfam) return;
   const int* rp = xfer + (long)f * row;
-  if (fcoef) scale *= __ldg(fcoef + f);   // config 4: one coefficient per family (levels >= 3)
-  double out[NP1];
+  const T scale = (T)(fcoef ? scale_ * __ldg(fcoef + f) : scale_);   // config 4: one coefficient per family (levels >= 3)
+  T out[NP1];
   int ob = 0, os = 0;   // output line: base and stride in the patch
   if constexpr (D == 3) {
     constexpr int S2 = NP1 * NP1;
@@ -288,16 +288,16 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       int gi[NP1];
 #pragma unroll
       for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
-      double u[NP1];
+      T u[NP1];
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : 0.0;
+      for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
-        double t1 = 0.0, t2 = 0.0;
+        T t1 = 0, t2 = 0;
 #pragma unroll
         for (int q = 0; q < NP1; ++q) {
-          if (Mt<K>(z, q) != 0.0) t1 = fma(Mt<K>(z, q), u[q], t1);
-          if (Kt<K>(z, q) != 0.0) t2 = fma(Kt<K>(z, q), u[q], t2);
+          if (Mt<K>(z, q) != 0.0) t1 = fma((T)Mt<K>(z, q), u[q], t1);
+          if (Kt<K>(z, q) != 0.0) t2 = fma((T)Kt<K>(z, q), u[q], t2);
         }
         s0[w][z * S2 + lane] = t1;
         s1[w][z * S2 + lane] = t2;
@@ -306,7 +306,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     __syncwarp();
     if (lane < NL) {     // y lines: lane = (px, pz)
       const int px = lane % NP1, pz = lane / NP1, b = pz * S2 + px;
-      double t1[NP1], t2[NP1];
+      T t1[NP1], t2[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
         t1[q] = s0[w][b + q * NP1];
@@ -314,14 +314,14 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
 #pragma unroll
       for (int yy = 0; yy < NP1; ++yy) {
-        double a = 0.0, bb = 0.0;
+        T a = 0, bb = 0;
 #pragma unroll
         for (int q = 0; q < NP1; ++q) {
           if (Mt<K>(yy, q) != 0.0) {
-            a = fma(Mt<K>(yy, q), t1[q], a);
-            bb = fma(Mt<K>(yy, q), t2[q], bb);
+            a = fma((T)Mt<K>(yy, q), t1[q], a);
+            bb = fma((T)Mt<K>(yy, q), t2[q], bb);
           }
-          if (Kt<K>(yy, q) != 0.0) bb = fma(Kt<K>(yy, q), t1[q], bb);
+          if (Kt<K>(yy, q) != 0.0) bb = fma((T)Kt<K>(yy, q), t1[q], bb);
         }
         s0[w][b + yy * NP1] = a;
         s1[w][b + yy * NP1] = bb;
@@ -331,7 +331,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     if (lane < NL) {     // x lines: lane = (py, pz)
       ob = lane * NP1;
       os = 1;
-      double a[NP1], bb[NP1];
+      T a[NP1], bb[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
         a[q] = s0[w][ob + q];
@@ -339,11 +339,11 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
-        double o = 0.0;
+        T o = 0;
 #pragma unroll
         for (int q = 0; q < NP1; ++q) {
-          if (Kt<K>(xx, q) != 0.0) o = fma(Kt<K>(xx, q), a[q], o);
-          if (Mt<K>(xx, q) != 0.0) o = fma(Mt<K>(xx, q), bb[q], o);
+          if (Kt<K>(xx, q) != 0.0) o = fma((T)Kt<K>(xx, q), a[q], o);
+          if (Mt<K>(xx, q) != 0.0) o = fma((T)Mt<K>(xx, q), bb[q], o);
         }
         out[xx] = scale * o;
       }
@@ -351,19 +351,19 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   } else {
     if (lane < NL) {     // x lines: lane = py, gathered straight into registers
       const int b = lane * NP1;
-      double u[NP1];
+      T u[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
         const int gi = decode_dof(__ldg(rp + b + q));
-        u[q] = gi >= 0 ? __ldg(x + gi) : 0.0;
+        u[q] = gi >= 0 ? __ldg(x + gi) : T(0);
       }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
-        double a = 0.0, bb = 0.0;
+        T a = 0, bb = 0;
 #pragma unroll
         for (int q = 0; q < NP1; ++q) {
-          if (Kt<K>(xx, q) != 0.0) a = fma(Kt<K>(xx, q), u[q], a);
-          if (Mt<K>(xx, q) != 0.0) bb = fma(Mt<K>(xx, q), u[q], bb);
+          if (Kt<K>(xx, q) != 0.0) a = fma((T)Kt<K>(xx, q), u[q], a);
+          if (Mt<K>(xx, q) != 0.0) bb = fma((T)Mt<K>(xx, q), u[q], bb);
         }
         s0[w][b + xx] = a;
         s1[w][b + xx] = bb;
@@ -373,7 +373,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     if (lane < NL) {     // y lines: lane = px
       ob = lane;
       os = NP1;
-      double a[NP1], bb[NP1];
+      T a[NP1], bb[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
         a[q] = s0[w][lane + q * NP1];
@@ -381,11 +381,11 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
 #pragma unroll
       for (int yy = 0; yy < NP1; ++yy) {
-        double o = 0.0;
+        T o = 0;
 #pragma unroll
         for (int q = 0; q < NP1; ++q) {
-          if (Mt<K>(yy, q) != 0.0) o = fma(Mt<K>(yy, q), a[q], o);
-          if (Kt<K>(yy, q) != 0.0) o = fma(Kt<K>(yy, q), bb[q], o);
+          if (Mt<K>(yy, q) != 0.0) o = fma((T)Mt<K>(yy, q), a[q], o);
+          if (Kt<K>(yy, q) != 0.0) o = fma((T)Kt<K>(yy, q), bb[q], o);
         }
         out[yy] = scale * o;
       }
@@ -406,23 +406,23 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
 }
 
 // cell_dofs is SoA: dof of local node b of cell c at cell_dofs[b * ldc + c]
-template <int D, int K>
+template <int D, int K, typename T>
 __global__ void __launch_bounds__(128) cell_apply(int n, const int* __restrict__ list,
                                                   const int* __restrict__ cell_dofs, long ldc,
                                                   const double* __restrict__ coef, double scale,
-                                                  const double* __restrict__ x, double* __restrict__ y) {
+                                                  const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NN = Shape<D, K>::NN;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int c = list ? list[t] : t;
   int idx[NN];
-  double u[NN], v[NN];
+  T u[NN], v[NN];
 #pragma unroll
   for (int b = 0; b < NN; ++b) idx[b] = __ldg(cell_dofs + (long)b * ldc + c);
 #pragma unroll
-  for (int b = 0; b < NN; ++b) u[b] = idx[b] >= 0 ? __ldg(x + idx[b]) : 0.0;
-  elem_apply<D, K>(u, v);
-  const double s = coef ? scale * __ldg(coef + c) : scale;
+  for (int b = 0; b < NN; ++b) u[b] = idx[b] >= 0 ? __ldg(x + idx[b]) : T(0);
+  elem_apply<D, K, T>(u, v);
+  const T s = (T)(coef ? scale * __ldg(coef + c) : scale);
 #pragma unroll
   for (int b = 0; b < NN; ++b)
     if (idx[b] >= 0) atomicAdd(y + idx[b], s * v[b]);
@@ -445,10 +445,9 @@ __global__ void cell_diag(int n, const int* __restrict__ cell_dofs, long ldc, co
 // Levels 0-1 of config 4: cells coarser than the coefficient patches carry an
 // explicit element matrix (exact sub-box integration, coef.cpp); y += A_c x_c
 // over a cell list (or all cells), thread per (cell, row).
-template <int D, int K>
+template <int D, int K, typename T>
 __global__ void cell_apply_dense(int n, const int* __restrict__ list, const int* __restrict__ cell_dofs, long ldc,
-                                 const double* __restrict__ elem, const double* __restrict__ x,
-                                 double* __restrict__ y) {
+                                 const double* __restrict__ elem, const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NN = Shape<D, K>::NN;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * NN) return;
@@ -456,10 +455,10 @@ __global__ void cell_apply_dense(int n, const int* __restrict__ list, const int*
   const int row = cell_dofs[(long)b * ldc + c];
   if (row < 0) return;
   const double* A = elem + ((long)c * NN + b) * NN;
-  double s = 0.0;
+  T s = 0;
   for (int q = 0; q < NN; ++q) {
     const int col = cell_dofs[(long)q * ldc + c];
-    if (col >= 0) s = fma(A[q], x[col], s);
+    if (col >= 0) s = fma((T)A[q], x[col], s);
   }
   atomicAdd(y + row, s);
 }
@@ -497,28 +496,36 @@ __global__ void cell_load(int n, const int* __restrict__ list, const int* __rest
 // padding, so the grid covers the segment exactly (no bounds branch).
 constexpr int VEC_NT = 256;
 constexpr int VEC_PAD = 2 * VEC_NT;
-template <bool READ_T, bool READ_DV, bool WRITE_DV, bool X_ZERO>
-__global__ void __launch_bounds__(VEC_NT) cheb_step(const double2* __restrict__ g, const double2* __restrict__ Dinv,
-                                                    double2* __restrict__ t, double2* __restrict__ dv,
-                                                    double2* __restrict__ x, double c1, double c2) {
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+template <typename S, bool READ_T, bool READ_DV, bool WRITE_DV, bool X_ZERO>
+__global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type* __restrict__ g,
+                                                    const typename Vec2<S>::type* __restrict__ Dinv,
+                                                    typename Vec2<S>::type* __restrict__ t,
+                                                    typename Vec2<S>::type* __restrict__ dv,
+                                                    typename Vec2<S>::type* __restrict__ x, double c1_, double c2_) {
+  using V2 = typename Vec2<S>::type;
+  const S c1 = (S)c1_, c2 = (S)c2_;
   const long i = (long)blockIdx.x * VEC_NT + threadIdx.x;
-  const double2 G = g[i];
-  double2 T = make_double2(0.0, 0.0), V = T, X = T;
+  const V2 G = g[i];
+  V2 T = {S(0), S(0)}, V = T, X = T;
   if (READ_T) T = t[i];
-  const double2 Di = Dinv[i];
+  const V2 Di = Dinv[i];
   if (READ_DV) V = dv[i];
   if (!X_ZERO) X = x[i];
   // reset of the accumulator: the stored zero is made data-dependent on the loaded
   // value so that the store cannot be issued while the load of the same address is
   // in flight (that ordering costs 2.25x on B200: tools/microbench8.cu)
-  if (READ_T) t[i] = make_double2(T.x - T.x, T.y - T.y);
-  double dx = c2 * Di.x * (G.x - T.x), dy = c2 * Di.y * (G.y - T.y);
+  if (READ_T) t[i] = V2{T.x - T.x, T.y - T.y};
+  S dx = c2 * Di.x * (G.x - T.x), dy = c2 * Di.y * (G.y - T.y);
   if (READ_DV) {
     dx = fma(c1, V.x, dx);
     dy = fma(c1, V.y, dy);
   }
-  if (WRITE_DV) dv[i] = make_double2(dx, dy);
-  x[i] = make_double2(X.x + dx, X.y + dy);
+  if (WRITE_DV) dv[i] = V2{dx, dy};
+  x[i] = V2{X.x + dx, X.y + dy};
 }
 
 // ------------------------------------------------------------- transfers
@@ -540,25 +547,25 @@ constexpr int XFER_WARPS = 4;
 
 // one 1-D pass over `lines` lines of a 3-index array: in(i, q, o) -> out(i, p, o),
 // out = sum_q M(p, q) in, with M = P (UP: q < N, p < NP1) or P^T (!UP)
-template <int K, bool UP, int NI, int NO>
-__device__ __forceinline__ void xfer_pass(int lane, const double* in, double* out, int si_in, int sq_in, int so_in,
+template <int K, bool UP, int NI, int NO, typename T>
+__device__ __forceinline__ void xfer_pass(int lane, const T* in, T* out, int si_in, int sq_in, int so_in,
                                           int si_out, int sp_out, int so_out) {
   constexpr int N = K + 1, NP1 = 2 * K + 1;
   constexpr int NQ = UP ? N : NP1, NPo = UP ? NP1 : N;
   for (int L = lane; L < NI * NO; L += 32) {
     const int i = L / NO, o = L % NO;
-    double v[NQ];
+    T v[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) v[q] = in[i * si_in + q * sq_in + o * so_in];
 #pragma unroll
     for (int p = 0; p < NPo; ++p) {
-      double s = 0.0;
+      T s = 0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         constexpr int dummy = 0;
         (void)dummy;
         const double m = UP ? Q<K>::P(p, q) : Q<K>::P(q, p);
-        if (m != 0.0) s = fma(m, v[q], s);
+        if (m != 0.0) s = fma((T)m, v[q], s);
       }
       out[i * si_out + p * sp_out + o * so_out] = s;
     }
@@ -581,14 +588,14 @@ __device__ __forceinline__ void row_fetch(const int* __restrict__ xfer, const in
   for (int q = 0; q < S::NR; ++q) r[q] = (lane + 32 * q < S::ROW) ? __ldg(row + lane + 32 * q) : -1;
 }
 
-template <int D, int K, int MODE>
+template <int D, int K, int MODE, typename T>
 __global__ void __launch_bounds__(32 * XFER_WARPS)
 warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
-                const unsigned char* __restrict__ cls_fine, const double* __restrict__ xc, double* __restrict__ xf) {
+                const unsigned char* __restrict__ cls_fine, const T* __restrict__ xc, T* __restrict__ xf) {
   using S = XferShape<D, K>;
   constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
   __shared__ int srow[XFER_WARPS][S::ROW];
-  __shared__ double b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
+  __shared__ T b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
   if (gw >= nfam) return;
@@ -603,10 +610,10 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
     const int* rw = srow[w];
     if (lane < NC) {
       const int ci = rw[NP + lane];
-      b0[w][lane] = ci >= 0 ? __ldg(xc + ci) : 0.0;
+      b0[w][lane] = ci >= 0 ? __ldg(xc + ci) : T(0);
     }
     __syncwarp();
-    double* fine;
+    T* fine;
     if constexpr (D == 3) {
       // x: c[jz][jy][jx] -> b1[jz][jy][ax];  y: -> b0[jz][ay][ax];  z: -> b1[az][ay][ax]
       xfer_pass<K, true, N * N, 1>(lane, b0[w], b1[w], N, 1, 0, NP1, 1, 0);
@@ -624,14 +631,14 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
     __syncwarp();
     constexpr int NIT = (NP + 31) / 32;
     int vi[NIT];
-    double old[NIT];
+    T old[NIT];
 #pragma unroll
     for (int q = 0; q < NIT; ++q) {   // all loads first: one memory round trip per family
       const int a = lane + 32 * q;
       vi[q] = a < NP ? rw[a] : -1;    // < 0: not owned / Dirichlet
-      old[q] = 0.0;
+      old[q] = 0;
       if (vi[q] >= 0) {
-        if (MODE == XFER_SET_E) old[q] = (cls_fine[vi[q]] & 1) ? 1.0 : 0.0;
+        if (MODE == XFER_SET_E) old[q] = (cls_fine[vi[q]] & 1) ? T(1) : T(0);
         else old[q] = xf[vi[q]];
       }
     }
@@ -640,7 +647,7 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
       const int a = lane + 32 * q;
       if (vi[q] < 0) continue;
       if (MODE == XFER_SET_E) {
-        if (old[q] != 0.0) xf[vi[q]] = fine[a];
+        if (old[q] != T(0)) xf[vi[q]] = fine[a];
       } else {
         xf[vi[q]] = old[q] + fine[a];
       }
@@ -649,15 +656,15 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
   }
 }
 
-template <int D, int K, int MODE>
+template <int D, int K, int MODE, typename T>
 __global__ void __launch_bounds__(32 * XFER_WARPS)
 warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
-              const unsigned char* __restrict__ cls_fine, const double* __restrict__ v, double* __restrict__ t,
-              double* __restrict__ dc) {
+              const unsigned char* __restrict__ cls_fine, const T* __restrict__ v, T* __restrict__ t,
+              T* __restrict__ dc) {
   using S = XferShape<D, K>;
   constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
   __shared__ int srow[XFER_WARPS][S::ROW];
-  __shared__ double b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
+  __shared__ T b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
   if (gw >= nfam) return;
@@ -673,29 +680,29 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
     // residual on the family's owned fine nodes (0 elsewhere); all loads first
     constexpr int NIT = (NP + 31) / 32;
     int ii[NIT];
-    double va[NIT], ta[NIT];
+    T va[NIT], ta[NIT];
 #pragma unroll
     for (int q = 0; q < NIT; ++q) {
       const int a = lane + 32 * q;
       ii[q] = a < NP ? rw[a] : -1;
-      va[q] = 0.0;
-      ta[q] = 0.0;
+      va[q] = 0;
+      ta[q] = 0;
       if (ii[q] >= 0) {
         va[q] = v[ii[q]];
         if (MODE == RES_VCYCLE) ta[q] = t[ii[q]];
-        if (MODE == RES_EONLY) ta[q] = (cls_fine[ii[q]] & 1) ? 0.0 : 1.0;
+        if (MODE == RES_EONLY) ta[q] = (cls_fine[ii[q]] & 1) ? T(0) : T(1);
       }
     }
 #pragma unroll
     for (int q = 0; q < NIT; ++q) {
       const int a = lane + 32 * q;
-      double r = 0.0;
+      T r = 0;
       if (ii[q] >= 0) {
         if (MODE == RES_VCYCLE) {
           r = va[q] - ta[q];
           t[ii[q]] = ta[q] - ta[q];             // data-dependent reset (see cheb_step)
         } else if (MODE == RES_EONLY) {
-          r = ta[q] == 0.0 ? va[q] : 0.0;
+          r = ta[q] == T(0) ? va[q] : T(0);
         } else {
           r = va[q];
         }
@@ -703,7 +710,7 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
       if (a < NP) b0[w][a] = r;
     }
     __syncwarp();
-    double* coarse;
+    T* coarse;
     if constexpr (D == 3) {
       // z: r[az][ay][ax] -> b1[jz][ay][ax];  y: -> b0[jz][jy][ax];  x: -> b1[jz][jy][jx]
       xfer_pass<K, false, 1, NP1 * NP1>(lane, b0[w], b1[w], 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
@@ -728,56 +735,71 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
 }
 
 // ------------------------------------------------------------- ghost exchange
-__global__ void pack(long n, const int* __restrict__ idx, const double* __restrict__ v, double* __restrict__ buf) {
+// (the wire format is fp64 for every vector precision)
+template <typename T>
+__global__ void pack(long n, const int* __restrict__ idx, const T* __restrict__ v, double* __restrict__ buf) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) buf[i] = v[idx[i]];
+  if (i < n) buf[i] = (double)v[idx[i]];
 }
 // ghosts -> buffer, ghost entries reset (data-dependent, see cheb_step)
-__global__ void pack_zero(long n, const int* __restrict__ idx, double* __restrict__ v, double* __restrict__ buf) {
+template <typename T>
+__global__ void pack_zero(long n, const int* __restrict__ idx, T* __restrict__ v, double* __restrict__ buf) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    const double a = v[idx[i]];
-    buf[i] = a;
+    const T a = v[idx[i]];
+    buf[i] = (double)a;
     v[idx[i]] = a - a;
   }
 }
-__global__ void unpack_set(long n, const int* __restrict__ idx, const double* __restrict__ buf, double* __restrict__ v) {
+template <typename T>
+__global__ void unpack_set(long n, const int* __restrict__ idx, const double* __restrict__ buf, T* __restrict__ v) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[idx[i]] = buf[i];
+  if (i < n) v[idx[i]] = (T)buf[i];
 }
 // an owned DoF may be a ghost of several peers: atomic add
-__global__ void unpack_add(long n, const int* __restrict__ idx, const double* __restrict__ buf, double* __restrict__ v) {
+template <typename T>
+__global__ void unpack_add(long n, const int* __restrict__ idx, const double* __restrict__ buf, T* __restrict__ v) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(v + idx[i], buf[i]);
+  if (i < n) atomicAdd(v + idx[i], (T)buf[i]);
 }
 
 // ------------------------------------------------------------- misc vector kernels
+template <typename T>
 __global__ void coarse_solve(int n, const int* __restrict__ sidx, const double* __restrict__ Ainv,
-                             const double* __restrict__ d, double* __restrict__ x) {
+                             const T* __restrict__ d, T* __restrict__ x) {
   int i = threadIdx.x;
   for (; i < n; i += blockDim.x) {
     double s = 0.0;
-    for (int j = 0; j < n; ++j) s = fma(Ainv[(long)i * n + j], d[sidx[j]], s);
-    x[sidx[i]] = s;
+    for (int j = 0; j < n; ++j) s = fma(Ainv[(long)i * n + j], (double)d[sidx[j]], s);
+    x[sidx[i]] = (T)s;
   }
 }
 
+template <typename T>
+__global__ void cast_vec(long n, const double* __restrict__ in, T* __restrict__ out) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) out[i] = (T)in[i];
+}
+
 // MG layout <- leaf order: out[m] = (inv[m] >= 0 ? in[inv[m]] : 0)
+template <typename T>
 __global__ void gather_to_mg(long n, const long long* __restrict__ inv, const double* __restrict__ in,
-                             double* __restrict__ out) {
+                             T* __restrict__ out) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long stride = (long)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
     long long s = inv[i];
-    out[i] = s >= 0 ? in[s] : 0.0;
+    out[i] = s >= 0 ? (T)in[s] : T(0);
   }
 }
 // leaf order <- MG layout
-__global__ void gather_from_mg(long n, const long long* __restrict__ perm, const double* __restrict__ in,
+template <typename T>
+__global__ void gather_from_mg(long n, const long long* __restrict__ perm, const T* __restrict__ in,
                                double* __restrict__ out) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long stride = (long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) out[i] = in[perm[i]];
+  for (; i < n; i += stride) out[i] = (double)in[perm[i]];
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -853,13 +875,14 @@ __global__ void __launch_bounds__(RED_NT) cg_update_xr(long n, const double* __r
   block_store_partial<RED_NT>(s, partial);
 }
 
-// z = lam * X ; partial (r, z)
+// z = lam * X ; partial (r, z)   (X: the V-cycle result, fp64 or fp32)
+template <typename T>
 __global__ void __launch_bounds__(RED_NT) mask_copy_dot(long n, const unsigned char* __restrict__ lam,
-                                                        const double* __restrict__ X, const double* __restrict__ r,
+                                                        const T* __restrict__ X, const double* __restrict__ r,
                                                         double* __restrict__ z, double* __restrict__ partial) {
   double s = 0.0;
   for (long i = (long)blockIdx.x * RED_NT + threadIdx.x; i < n; i += (long)gridDim.x * RED_NT) {
-    double v = lam[i] ? X[i] : 0.0;
+    double v = lam[i] ? (double)X[i] : 0.0;
     z[i] = v;
     s = fma(r[i], v, s);
   }

@@ -240,3 +240,40 @@ def test_large_config_vcycle_and_cg(name):
     it, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
     _, it_ref, _, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
     assert abs(it - it_ref) <= 1, (it, it_ref)
+
+
+# ---------------------------------------------------------------- mixed precision
+# SURVEY §8(f) row 1 / P:897: the V-cycle in fp32 inside the fp64 CG.
+# The fp32 V-cycle is the fp64 one up to single-precision rounding: relative
+# max-norm error bounded by a few hundred ulp(fp32) = 2^-24 per operation chain
+# (MIXED_VC_TOL); CG keeps its fp64 residual and stopping test, so the iteration
+# count stays within +-1 of the oracle's fp64 CG and the true residual <= 1e-8.
+MIXED_VC_TOL = 2e-5
+MIXED_CASES = [("c1", None), ("c3p2", None), ("c4", None, -1, C4S)]
+
+
+@pytest.mark.parametrize("case", MIXED_CASES, ids=["c1", "c3p2", "c4s"])
+def test_mixed_precision_vcycle_and_cg(case):
+    name = case[0]
+    cfg = dict(config(name))
+    if len(case) > 2:
+        cfg.update(case[3])
+    coef = log_uniform_coef(4 ** cfg["dim"]) if cfg.get("coef") else None
+    _, _, h = G.build_config(cfg, coef_level2=coef, mixed=True)
+    _, oh, _ = pair(*case)
+    for l in range(1, oh.L + 1):
+        h.set_eigen(l, oh.levels[l].lam)
+    n = oh.leaf.n_free
+    b = uniform_pm1(n)
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.vcycle(dev(b), x)
+    err = rel(x.cpu().numpy(), mg.vcycle(oh, b))
+    assert 1e-9 < err < MIXED_VC_TOL, err          # fp32 rounding visible, bounded
+    bb = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, bb)
+    xs = torch.zeros(n, device="cuda", dtype=torch.float64)
+    it, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
+    _, it_ref, _, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
+    assert abs(it - it_ref) <= 1, (it, it_ref)
+    tr = np.linalg.norm(oh.b_leaf - oh.A_leaf @ xs.cpu().numpy()) / np.linalg.norm(oh.b_leaf)
+    assert tr <= 1.01e-8
