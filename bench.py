@@ -38,8 +38,24 @@ WORKLOADS = {
           "refinements + 7 sphere-surface passes (|x-(.5,.5,.5)| = 0.3), 2:1 vertex balanced",
     "c2": "BASELINE configs[1]: 2D L-shape Q2, corner-graded to ~1M DoFs",
     "c3p4": "c3 recipe truncated at 4 passes (774,181 DoFs)",
+    "c4": "BASELINE configs[3]: 3D -div(a grad u) = 1 on [0,1]^3, Q2, fp64, a log-uniform in [1e-2,1e2] per "
+          "level-2 cell; corner-graded toward (0,0,0), s = 6, lmax = 19 (107M DoFs, 20 levels)",
+    "c5": "BASELINE configs[4]: the c3 sphere forest with a shell half-width w_n (2^-10 units) giving "
+          ">= 125M DoFs per GPU (weak scaling)",
 }
 SAMPLE = "c3p4"
+
+
+def load_traffic(config, precision):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu capture
+    (tools/traffic_from_ncu.py -> profiles/*_traffic.json), else None."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
+        with open(p) as fh:
+            e = json.load(fh).get(f"{config}/{precision}")
+        if e:
+            return e["traffic_bytes"], os.path.relpath(p, ROOT)
+    return None, None
 
 
 def env_rank():
@@ -166,7 +182,11 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = config(args.config)
+    if args.config == "c5":
+        from gmg_inputs import config_c5
+        cfg = config_c5(world)
+    else:
+        cfg = config(args.config)
     t0 = time.time()
     f = G.gmg_forest_generate(G.recipe_from_config(cfg))
     part = G.gmg_partition(f, world)
@@ -176,7 +196,11 @@ def run_ours(args):
         dist.broadcast_object_list(uid, src=0)
         comm = G.NcclComm(uid[0], world, rank)
     mixed = args.precision == "mixed"
-    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, comm=comm, mixed=mixed)
+    coef = None
+    if cfg.get("coef") == "level2_log_uniform":        # config 4: a per level-2 cell (SFC order)
+        from gmg_inputs import log_uniform_coef
+        coef = log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, comm=comm, mixed=mixed, coef_level2=coef)
     setup_s = time.time() - t0
     info = h.info()
     n_dofs = info["n_leaf_nodes"]
@@ -284,6 +308,7 @@ def run_ours(args):
     t_cg = max_over_ranks(time.perf_counter() - c0)
 
     per_vc, per_la = h.launch_profile()
+    traffic, traffic_src = load_traffic(args.config, args.precision) if world == 1 else (None, None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = oracle_sample(steps=3, warmup=1)
@@ -294,7 +319,8 @@ def run_ours(args):
         model = part.model()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32" if mixed else "f64", "data": "synthetic",
+               "scaling": "weak" if args.config == "c5" else "strong", "vs_baseline": None,
+               "dtype": "f32" if mixed else "f64", "data": "synthetic",
                "config": {"workload": WORKLOADS.get(args.config, args.config), "config": args.config,
                           "precision": "fp32 V-cycle in fp64 CG" if mixed else "fp64",
                           "n_leaf_dofs": n_dofs, "n_free_dofs": info["n_leaf_free"], "levels": info["n_levels"],
@@ -306,7 +332,8 @@ def run_ours(args):
                           f"{world} ranks, SFC partition + first-child rule, NCCL ghost exchange",
                           "partition_eta": model["eta"], "setup_s": round(setup_s, 2)},
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": None,
+                            "frac": achieved / peak, "traffic": traffic,
+                            "traffic_source": traffic_src if traffic is not None else None,
                             "kernel": "fam_tensor_apply<3,2,%s> (level operator), finest level"
                                       % ("float" if mixed else "double"),
                             "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,

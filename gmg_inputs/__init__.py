@@ -90,11 +90,32 @@ CONFIGS = {
                  rule="sphere_surface", center=((1, 2), (1, 2), (1, 2)), radius=(3, 10),
                  shell=(0, 1), passes=4),
     # configs[3]: 3D variable coefficient, corner-graded toward (0,0,0)
-    # (SURVEY c.2#20: dist(closure T, 0) <= 2^(s - level), level < lmax).
+    # (SURVEY c.2#20: dist(closure T, 0) <= 2^(s - level), level < lmax).  lmax
+    # = 19 is the first value reaching ~100M leaf nodes (reading R20: 13,193,951
+    # leaves, 107,140,241 nodes, 20 levels; lmax = 18 gives 99,063,795).
     "c4": dict(dim=3, k=2, trees=[(0, 0, 0)], global_refinements=3,
                rule="corner_dist", corner=(0, 0, 0), s=6, lmax=19, passes=None,
                coef="level2_log_uniform"),
+    # configs[4]: the sphere-refined forest of config 3 scaled to ~125M DoFs per
+    # GPU (reading R21): the 7 passes refine leaves meeting the closed shell
+    # 0.3 - w <= |x - c| <= 0.3 + w, w = shell[0] / shell[1] the smallest multiple
+    # of 2^-10 reaching 125M leaf nodes times the GPU count.  n = 1: w = 4/1024,
+    # 125,785,013 nodes (w = 3/1024: 106,745,081).
+    "c5": dict(dim=3, k=2, trees=[(0, 0, 0)], global_refinements=3,
+               rule="sphere_surface", center=((1, 2), (1, 2), (1, 2)), radius=(3, 10),
+               shell=(4, 1024), passes=7),
 }
+
+# config 5 for n GPUs: w_n / 2^-10.  n = 1 is measured; n > 1 are estimates from
+# the measured growth (~19M nodes per 2^-10 of half-width) pending a count on a
+# host large enough to build the 0.25-1B node forests.
+C5_SHELL = {1: 4, 2: 11, 4: 24, 8: 50}
+
+
+def config_c5(n_gpus: int) -> dict:
+    cfg = dict(CONFIGS["c5"])
+    cfg["shell"] = (C5_SHELL[n_gpus], 1024)
+    return cfg
 
 
 def config(name: str) -> dict:
