@@ -95,6 +95,21 @@ typedef struct {
 } gmg_recipe;
 
 gmg_status gmg_forest_generate(const gmg_recipe *recipe, gmg_forest **out);
+
+/* The mesh sequences of the paper's partitioning study (Fig. 3), one
+ * coarse cell read as [-1,1]^d (reading R27), each step closed to 2:1 vertex
+ * balance:
+ *  UNIFORM   L global refinements;
+ *  CIRCLE    L times: refine every leaf whose closed box meets the disc/ball of
+ *            radius 1/(4 pi) about the origin;
+ *  QUADRANT  one global refinement, then L-1 times: refine every leaf inside the
+ *            negative quadrant/octant [-1,0]^d;
+ *  ANNULUS   L-3 global refinements, then refine the leaves whose centre lies in
+ *            |x| <= 0.55, then in 0.3 <= |x| <= 0.43, then in 0.335 <= |x| <= 0.39
+ *            (L >= 4).
+ * Errors: INVALID_ARG (dim, kind, L out of range). */
+typedef enum { GMG_SEQ_UNIFORM = 0, GMG_SEQ_CIRCLE = 1, GMG_SEQ_QUADRANT = 2, GMG_SEQ_ANNULUS = 3 } gmg_sequence;
+gmg_status gmg_forest_sequence(int dim, gmg_sequence kind, int L, gmg_forest **out);
 gmg_status gmg_forest_destroy(gmg_forest *f);
 gmg_status gmg_forest_info(const gmg_forest *f, int *dim, int *n_trees, int64_t *n_leaves,
                            int *max_level);

@@ -293,3 +293,67 @@ def generate(cfg: dict, passes: int | None = -1) -> Forest:
 def from_leaves(dim: int, trees, level, gc) -> Forest:
     return Forest(dim, tree_order(trees), np.asarray(level, dtype=np.int64),
                   np.asarray(gc, dtype=np.int64).reshape(-1, dim)).sorted()
+
+
+# ---------------------------------------------------------------------------
+# Mesh sequences of the partitioning study (§3.5, Fig. 3),
+# one coarse cell read as [-1,1]^d (reading R27).  Every refinement
+# step is followed by the closure.  A level-l cell G spans
+# x_j in [2 G_j - 2^l, 2 G_j + 2 - 2^l] / 2^l; its centre is (2 G_j + 1 - 2^l) / 2^l.
+
+def _centre2_times_4l(f: Forest) -> np.ndarray:
+    """|centre|^2 * 4^level, exact in int64 for the small levels the tests use."""
+    two_l = np.left_shift(np.int64(1), f.level)
+    n = 2 * f.gc + 1 - two_l[:, None]
+    _i64_guard(n.astype(np.float64) ** 2)
+    return (n * n).sum(axis=1)
+
+
+def sequence(dim: int, kind: str, L: int) -> Forest:
+    """uniform: L global refinements.  circle: L times refine every leaf with a
+    point inside the ball of radius 1/(4 pi) about the origin.  quadrant: one
+    global refinement, then L-1 times refine the leaves of the negative
+    quadrant [-1,0]^d.  annulus: L-3 global refinements, then refine the leaves
+    whose centre lies in |x| <= 0.55, then 0.3 <= |x| <= 0.43, then
+    0.335 <= |x| <= 0.39 (P:783-790)."""
+    f = coarse_forest(dim, [tuple([0] * dim)])
+
+    def step(mark):
+        nonlocal f
+        if mark.any():
+            f = close(refine(f, mark))
+
+    def all_leaves():
+        return np.ones(f.n_leaves, dtype=bool)
+
+    four_l = lambda: np.left_shift(np.int64(1), 2 * f.level)
+    if kind == "uniform":
+        for _ in range(L):
+            step(all_leaves())
+    elif kind == "circle":
+        for _ in range(L):
+            two_l = np.left_shift(np.int64(1), f.level)[:, None]
+            lo = 2 * f.gc - two_l                      # box in units 2^-l
+            hi = lo + 2
+            v = np.where(lo > 0, lo, np.where(hi < 0, -hi, 0))
+            d2 = (v * v).sum(axis=1).astype(np.float64)
+            # distance < 1/(4 pi)  <=>  d2 / 4^l < 1 / (16 pi^2)
+            step(d2 * (16.0 * np.pi ** 2) < four_l().astype(np.float64))
+    elif kind == "quadrant":
+        step(all_leaves())
+        for _ in range(L - 1):
+            two_l = np.left_shift(np.int64(1), f.level)[:, None]
+            step(np.all(2 * f.gc + 2 - two_l <= 0, axis=1))
+    elif kind == "annulus":
+        if L < 4:
+            raise ValueError("annulus needs L >= 4")
+        for _ in range(L - 3):
+            step(all_leaves())
+        step(_centre2_times_4l(f) * 400 <= 121 * four_l())                       # r <= 0.55
+        c2 = _centre2_times_4l(f)
+        step((c2 * 100 >= 9 * four_l()) & (c2 * 10000 <= 1849 * four_l()))       # 0.3 .. 0.43
+        c2 = _centre2_times_4l(f)
+        step((c2 * 40000 >= 4489 * four_l()) & (c2 * 10000 <= 1521 * four_l()))  # 0.335 .. 0.39
+    else:
+        raise ValueError(kind)
+    return f

@@ -100,6 +100,7 @@ _SIGS = {
     "gmg_abi_version": ([], C.c_int),
     "gmg_forest_create": ([C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, C.c_uint32, C.POINTER(_vp)], C.c_int),
     "gmg_forest_generate": ([C.POINTER(Recipe), C.POINTER(_vp)], C.c_int),
+    "gmg_forest_sequence": ([C.c_int, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "gmg_forest_destroy": ([_vp], C.c_int),
     "gmg_forest_info": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int)], C.c_int),
     "gmg_export_leaves": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -222,6 +223,16 @@ class Forest:
 def gmg_forest_generate(recipe: Recipe) -> Forest:
     h = _vp()
     _check(_lib.gmg_forest_generate(C.byref(recipe), C.byref(h)))
+    return Forest(h)
+
+
+SEQUENCES = {"uniform": 0, "circle": 1, "quadrant": 2, "annulus": 3}
+
+
+def gmg_forest_sequence(dim: int, kind: str, L: int) -> Forest:
+    """The paper's partitioning-study mesh sequences, see gmg.h."""
+    h = _vp()
+    _check(_lib.gmg_forest_sequence(dim, SEQUENCES[kind], L, C.byref(h)))
     return Forest(h)
 
 

@@ -83,6 +83,15 @@ gmg_status gmg_forest_generate(const gmg_recipe* r, gmg_forest** out) {
   });
 }
 
+gmg_status gmg_forest_sequence(int dim, gmg_sequence kind, int L, gmg_forest** out) {
+  return guard([&] {
+    NEED(out);
+    auto f = std::make_unique<gmg_forest>();
+    f->f = gmg::forest_sequence(dim, kind, L);
+    *out = f.release();
+  });
+}
+
 gmg_status gmg_forest_destroy(gmg_forest* f) {
   delete f;
   return GMG_OK;

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <numeric>
 
+#include <functional>
+
 #include "forest.hpp"
 
 namespace gmg {
@@ -283,6 +285,96 @@ Forest forest_generate(const gmg_recipe& r) {
     close_balance(dim, dom, R, work);
     f = forest_from_refined(dim, trees, R);
     ++passes;
+  }
+  return f;
+}
+
+// ------------------------------------------------------------------ mesh sequences
+// The refinement sequences of the paper's partitioning study, on one
+// coarse cell read as [-1,1]^d (the "negative quadrant" and the annulus radii
+// need the origin at the cell centre; reading R27).  A level-l cell with global
+// coordinates G spans x in [(2G - 2^l), (2G + 2 - 2^l)] / 2^l per direction.
+static void refine_marked(int dim, const Forest& dom, std::vector<FlatSet>& R, const Forest& f,
+                          const std::function<bool(int, const Vec3&)>& mark) {
+  std::vector<std::pair<int, u64>> work;
+  for (i64 i = 0; i < f.n_leaves(); ++i) {
+    const int l = f.level[i];
+    if (!mark(l, f.gc[i])) continue;
+    if ((int)R.size() <= l) R.resize(l + 1);
+    const u64 key = morton(dim, f.gc[i]);
+    if (R[l].insert(key)) work.push_back({l, key});
+  }
+  close_balance(dim, dom, R, work);
+}
+
+Forest forest_sequence(int dim, gmg_sequence kind, int L) {
+  GMG_REQUIRE(dim == 2 || dim == 3, GMG_E_INVALID_ARG, "sequence dim");
+  GMG_REQUIRE(L >= 1 && L <= (dim == 3 ? 19 : 29), GMG_E_INVALID_ARG, "sequence level");
+  GMG_REQUIRE(kind != GMG_SEQ_ANNULUS || L >= 4, GMG_E_INVALID_ARG, "annulus needs L >= 4");
+  const std::vector<Vec3> trees{{0, 0, 0}};
+  Forest dom = domain_of(dim, trees);
+  std::vector<FlatSet> R(1);
+  Forest f = forest_from_refined(dim, trees, R);
+  auto step = [&](const std::function<bool(int, const Vec3&)>& mark) {
+    refine_marked(dim, dom, R, f, mark);
+    f = forest_from_refined(dim, trees, R);
+  };
+  auto all = [](int, const Vec3&) { return true; };
+  // |centre|^2 * 4^l  (integer): centre x_j = (2 G_j + 1 - 2^l) / 2^l
+  auto centre2 = [dim](int l, const Vec3& g) {
+    i128 s = 0;
+    for (int j = 0; j < dim; ++j) {
+      const i128 n = 2 * (i128)g[j] + 1 - ((i128)1 << l);
+      s += n * n;
+    }
+    return s;
+  };
+  auto centre_in = [&](int l, const Vec3& g, i128 num, i128 den) {   // |c|^2 <= num/den
+    return centre2(l, g) * den <= num * ((i128)1 << (2 * l));
+  };
+  auto centre_out = [&](int l, const Vec3& g, i128 num, i128 den) {  // |c|^2 >= num/den
+    return centre2(l, g) * den >= num * ((i128)1 << (2 * l));
+  };
+  switch (kind) {
+    case GMG_SEQ_UNIFORM:                       // "global refinement of the coarse mesh L times"
+      for (int i = 0; i < L; ++i) step(all);
+      break;
+    case GMG_SEQ_CIRCLE: {                      // "all mesh cells with at least one point inside the
+      const long double rho2 = 1.0L / (16.0L * 3.14159265358979323846264338327950288L *
+                                       3.14159265358979323846264338327950288L);   // (1/(4 pi))^2
+      for (int i = 0; i < L; ++i)               //  circle of radius 1/(4 pi) around the origin"
+        step([&](int l, const Vec3& g) {
+          i128 d2 = 0;                          // (distance of the closed box to 0)^2 * 4^l
+          for (int j = 0; j < dim; ++j) {
+            const i128 lo = 2 * (i128)g[j] - ((i128)1 << l), hi = lo + 2;
+            const i128 v = lo > 0 ? lo : (hi < 0 ? -hi : 0);
+            d2 += v * v;
+          }
+          return (long double)d2 < rho2 * (long double)((i128)1 << (2 * l));   // irrational: no ties
+        });
+      break;
+    }
+    case GMG_SEQ_QUADRANT:                      // "after one uniform refinement ... refine the cell in
+      step(all);                                //  the negative quadrant L-1 times"
+      for (int i = 1; i < L; ++i)
+        step([&](int l, const Vec3& g) {
+          for (int j = 0; j < dim; ++j)
+            if (2 * (i128)g[j] + 2 - ((i128)1 << l) > 0) return false;   // box inside [-1,0]^d
+          return true;
+        });
+      break;
+    case GMG_SEQ_ANNULUS:                       // L-3 uniform refinements, then three centre rules
+      for (int i = 0; i < L - 3; ++i) step(all);
+      step([&](int l, const Vec3& g) { return centre_in(l, g, 121, 400); });               // r <= 0.55
+      step([&](int l, const Vec3& g) {
+        return centre_out(l, g, 9, 100) && centre_in(l, g, 1849, 10000);                  // 0.3 .. 0.43
+      });
+      step([&](int l, const Vec3& g) {
+        return centre_out(l, g, 4489, 40000) && centre_in(l, g, 1521, 10000);             // 0.335 .. 0.39
+      });
+      break;
+    default:
+      fail(GMG_E_INVALID_ARG, "unknown sequence");
   }
   return f;
 }
