@@ -47,6 +47,10 @@ gmg_status guard(F&& fn) {
 }
 
 #define NEED(p) GMG_REQUIRE((p) != nullptr, GMG_E_INVALID_ARG, #p " is NULL")
+// leaf vectors of this rank: NULL is legal when the rank owns no leaf DoF (zero-size
+// vectors, e.g. more ranks than leaves); every rank still joins the collectives
+#define NEED_LEAF(h, p) \
+  GMG_REQUIRE((p) != nullptr || (h)->local.n_leaf_owned == 0, GMG_E_INVALID_ARG, #p " is NULL")
 
 gmg::DeviceHierarchy* need_dev(gmg_hierarchy* h) {
   GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "hierarchy has no device data (GMG_HOST_ONLY)");
@@ -360,9 +364,9 @@ gmg_status gmg_export_cell_dofs(const gmg_hierarchy* h, int level, int64_t* n_ce
 gmg_status gmg_vcycle(gmg_hierarchy* h, const double* b, double* x, void* s) {
   return guard([&] {
     NEED(h);
-    NEED(b);
-    NEED(x);
-    GMG_REQUIRE(b != x, GMG_E_INVALID_ARG, "b and x must not alias");
+    NEED_LEAF(h, b);
+    NEED_LEAF(h, x);
+    GMG_REQUIRE(b != x || h->local.n_leaf_owned == 0, GMG_E_INVALID_ARG, "b and x must not alias");
     gmg::device_vcycle(need_dev(h), b, x, s);
   });
 }
@@ -372,8 +376,8 @@ gmg_status gmg_solve_cg(gmg_hierarchy* h, const double* b, double* x, double rto
   gmg_status st = GMG_OK;
   gmg_status g = guard([&] {
     NEED(h);
-    NEED(b);
-    NEED(x);
+    NEED_LEAF(h, b);
+    NEED_LEAF(h, x);
     GMG_REQUIRE(rtol >= 0 && max_it >= 1, GMG_E_INVALID_ARG, "rtol >= 0 and max_it >= 1 required");
     int rc = gmg::device_solve_cg(need_dev(h), b, x, rtol, max_it, iters, rel_res, s);
     if (rc) {
@@ -387,7 +391,7 @@ gmg_status gmg_solve_cg(gmg_hierarchy* h, const double* b, double* x, double rto
 gmg_status gmg_rhs_constant(gmg_hierarchy* h, double f, double* b, void* s) {
   return guard([&] {
     NEED(h);
-    NEED(b);
+    NEED_LEAF(h, b);
     gmg::device_rhs_constant(need_dev(h), f, b, s);
   });
 }
@@ -447,8 +451,8 @@ gmg_status gmg_prolongate(gmg_hierarchy* h, int level, const double* xc, double*
 gmg_status gmg_leaf_apply(gmg_hierarchy* h, const double* u, double* v, void* s) {
   return guard([&] {
     NEED(h);
-    NEED(u);
-    NEED(v);
+    NEED_LEAF(h, u);
+    NEED_LEAF(h, v);
     gmg::device_leaf_apply(need_dev(h), u, v, s);
   });
 }

@@ -277,3 +277,87 @@ def test_mixed_precision_vcycle_and_cg(case):
     assert abs(it - it_ref) <= 1, (it, it_ref)
     tr = np.linalg.norm(oh.b_leaf - oh.A_leaf @ xs.cpu().numpy()) / np.linalg.norm(oh.b_leaf)
     assert tr <= 1.01e-8
+
+
+# ---------------------------------------------------------------- degenerate cases
+# Edge cases of the method: a forest whose only level has no free DoF (every
+# node on the Dirichlet boundary), a single free DoF, a sequence mesh with a
+# long chain of nearly empty levels, and more ranks than leaves.
+DEGENERATE = [("uniform", 2, 1, 1), ("uniform", 3, 1, 1), ("uniform", 2, 1, 2), ("quadrant", 2, 6, 1),
+              ("circle", 3, 4, 2), ("quadrant", 2, 4, 1)]
+
+
+@pytest.mark.parametrize("kind,d,L,k", DEGENERATE, ids=[f"{a}{b}d-L{c}-k{e}" for a, b, c, e in DEGENERATE])
+def test_degenerate_forests(kind, d, L, k):
+    f = G.gmg_forest_sequence(d, kind, L)
+    part = G.gmg_partition(f, 1)
+    h = G.gmg_setup(f, part, k=k)
+    of = F.sequence(d, kind, L)
+    oh = mg.build(of, k)
+    n = oh.leaf.n_free
+    assert h.info()["n_leaf_free"] == n
+    for l in range(1, oh.L + 1):
+        h.set_eigen(l, oh.levels[l].lam)
+    b = uniform_pm1(n)
+    x = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.vcycle(dev(b), x)
+    if n:
+        assert rel(x.cpu().numpy(), mg.vcycle(oh, b)) < VC_TOL
+    bb = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, bb)
+    xs = torch.zeros(n, device="cuda", dtype=torch.float64)
+    it, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
+    if n:
+        _, it_ref, _, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
+        assert abs(it - it_ref) <= 1, (it, it_ref)
+    else:
+        assert it == 0
+
+
+def test_more_ranks_than_leaves_local_ranks():
+    """p = 6 ranks on a 4-leaf forest: ranks without cells on some levels still
+    take part in every exchange; the result equals one rank."""
+    import threading
+    f = G.gmg_forest_sequence(2, "uniform", 1)     # 4 leaves, one free Q2 DoF ring
+    _, _, h1 = None, None, G.gmg_setup(f, G.gmg_partition(f, 1), k=2)
+    n = h1.info()["n_leaf_free"]
+    canon1 = h1.leaf_dofs()[3]
+    b_can = uniform_pm1(n)
+    x1 = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h1.vcycle(dev(b_can[canon1]), x1)
+    ref = np.empty(n)
+    ref[canon1] = x1.cpu().numpy()
+    p = 6
+    world = G.LocalWorld(p)
+    part = G.gmg_partition(f, p)
+    hs = [None] * p
+    streams = [torch.cuda.Stream() for _ in range(p)]
+
+    def setup(r):
+        torch.cuda.set_device(0)
+        hs[r] = G.gmg_setup(f, part, k=2, rank=r, comm=world)
+
+    ts = [threading.Thread(target=setup, args=(r,)) for r in range(p)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    canon = hs[0].leaf_dofs()[3]
+    res = [None] * p
+
+    def work(r):
+        torch.cuda.set_device(0)
+        info = hs[r].info()
+        fo, no = info["first_owned"], info["n_owned"]
+        with torch.cuda.stream(streams[r]):
+            bl = torch.tensor(b_can[canon[fo:fo + no]], device="cuda", dtype=torch.float64)
+            xl = torch.zeros_like(bl)
+            hs[r].vcycle(bl, xl, stream=streams[r].cuda_stream)
+            streams[r].synchronize()
+        res[r] = (fo, no, xl.cpu().numpy())
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(p)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    xv = np.empty(n)
+    for fo, no, xl in res:
+        xv[canon[fo:fo + no]] = xl
+    assert rel(xv, ref) < 1e-13
