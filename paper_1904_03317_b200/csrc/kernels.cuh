@@ -282,10 +282,10 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   const T scale = (T)(fcoef ? scale_ * __ldg(fcoef + f) : scale_);   // config 4: one coefficient per family (levels >= 3)
   T out[NP1];
   int ob = 0, os = 0;   // output line: base and stride in the patch
+  int gi[NP1];           // 3D: the z-line DoFs of this lane, reused by the scatter
   if constexpr (D == 3) {
     constexpr int S2 = NP1 * NP1;
     if (lane < NL) {     // z lines: lane = (px, py), gathered straight into registers
-      int gi[NP1];
 #pragma unroll
       for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
       T u[NP1];
@@ -391,7 +391,28 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
     }
   }
-  if (lane < NL) {
+  if constexpr (D == 3) {
+    // x-line results -> smem (each lane rewrites the positions it just read), then the
+    // scatter runs along the z lines of the gather with the DoF indices still in registers
+    constexpr int S2 = NP1 * NP1;
+    if (lane < NL) {
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) s0[w][ob + q] = out[q];
+    }
+    __syncwarp();
+    if (lane < NL) {
+      const int px = lane % NP1, py = lane / NP1;
+      const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) {
+        const int i = gi[z];
+        if (i < 0) continue;
+        const T v = s0[w][z * S2 + lane];
+        if (inner && z > 0 && z < 2 * K) y[i] = v;      // only this family touches the node
+        else atomicAdd(y + i, v);
+      }
+    }
+  } else if (lane < NL) {
 #pragma unroll
     for (int q = 0; q < NP1; ++q) {
       const int a = ob + q * os;
