@@ -269,12 +269,31 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
 
 constexpr int TENSOR_WARPS = 8;
 
+// Transposition layouts of fam_tensor_apply (3D): A holds the z-pass result for
+// the y pass, B the y-pass result for the x pass; index = cx x + cy y + cz z.
+// Chosen by exhaustive search so that every pass's shared-memory accesses (25
+// lanes; fp64 served per 16-lane half-warp over 16 bank pairs, fp32 in one pass
+// over 32 banks) take the minimum number of wavefronts (tools/smem_layouts.py).
+template <int K, typename T> struct PatchLayout {   // K = 1: natural order (27 nodes)
+  static constexpr int ax = 1, ay = 2 * K + 1, az = (2 * K + 1) * (2 * K + 1);
+  static constexpr int bx = 1, by = 2 * K + 1, bz = (2 * K + 1) * (2 * K + 1);
+  static constexpr int size = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);
+};
+template <> struct PatchLayout<2, double> {
+  static constexpr int ax = 5, ay = 9, az = 25, bx = 1, by = 33, bz = 5, size = 157;
+};
+template <> struct PatchLayout<2, float> {
+  static constexpr int ax = 5, ay = 1, az = 25, bx = 1, by = 25, bz = 5, size = 125;
+};
+
 template <int D, int K, typename T>
 __global__ void __launch_bounds__(32 * TENSOR_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
-  __shared__ T s0[TENSOR_WARPS][NP], s1[TENSOR_WARPS][NP];
+  using LY = PatchLayout<K, T>;
+  constexpr int NS = D == 3 && LY::size > NP ? LY::size : NP;
+  __shared__ T s0[TENSOR_WARPS][NS], s1[TENSOR_WARPS][NS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int f = blockIdx.x * TENSOR_WARPS + w;
   if (f >= nfam) return;
@@ -299,19 +318,24 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
           if (Mt<K>(z, q) != 0.0) t1 = fma((T)Mt<K>(z, q), u[q], t1);
           if (Kt<K>(z, q) != 0.0) t2 = fma((T)Kt<K>(z, q), u[q], t2);
         }
-        s0[w][z * S2 + lane] = t1;
-        s1[w][z * S2 + lane] = t2;
+        // transposition layout A (PatchLayout): minimum wavefronts for this store
+        // (lanes over x, y) and for the y-pass load (lanes over x, z)
+        const int ia = LY::ax * (lane % NP1) + LY::ay * (lane / NP1) + LY::az * z;
+        s0[w][ia] = t1;
+        s1[w][ia] = t2;
       }
     }
     __syncwarp();
     if (lane < NL) {     // y lines: lane = (px, pz)
-      const int px = lane % NP1, pz = lane / NP1, b = pz * S2 + px;
+      const int px = lane % NP1, pz = lane / NP1;
+      const int ba = LY::ax * px + LY::az * pz, bb_ = LY::bx * px + LY::bz * pz;
       T t1[NP1], t2[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        t1[q] = s0[w][b + q * NP1];
-        t2[q] = s1[w][b + q * NP1];
+        t1[q] = s0[w][ba + LY::ay * q];
+        t2[q] = s1[w][ba + LY::ay * q];
       }
+      __syncwarp((1u << NL) - 1);   // layout B differs from A: all loads before any store
 #pragma unroll
       for (int yy = 0; yy < NP1; ++yy) {
         T a = 0, bb = 0;
@@ -323,19 +347,22 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
           }
           if (Kt<K>(yy, q) != 0.0) bb = fma((T)Kt<K>(yy, q), t1[q], bb);
         }
-        s0[w][b + yy * NP1] = a;
-        s1[w][b + yy * NP1] = bb;
+        // layout B (PatchLayout): minimum wavefronts for this store (lanes over x, z)
+        // and for the x-pass load (lanes over y, z)
+        s0[w][bb_ + LY::by * yy] = a;
+        s1[w][bb_ + LY::by * yy] = bb;
       }
     }
     __syncwarp();
     if (lane < NL) {     // x lines: lane = (py, pz)
       ob = lane * NP1;
       os = 1;
+      const int bx = LY::by * (lane % NP1) + LY::bz * (lane / NP1);
       T a[NP1], bb[NP1];
 #pragma unroll
       for (int q = 0; q < NP1; ++q) {
-        a[q] = s0[w][ob + q];
-        bb[q] = s1[w][ob + q];
+        a[q] = s0[w][bx + LY::bx * q];
+        bb[q] = s1[w][bx + LY::bx * q];
       }
 #pragma unroll
       for (int xx = 0; xx < NP1; ++xx) {
@@ -395,6 +422,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     // x-line results -> smem (each lane rewrites the positions it just read), then the
     // scatter runs along the z lines of the gather with the DoF indices still in registers
     constexpr int S2 = NP1 * NP1;
+    __syncwarp();        // every lane has read layout B before the natural-layout stores
     if (lane < NL) {
 #pragma unroll
       for (int q = 0; q < NP1; ++q) s0[w][ob + q] = out[q];
