@@ -89,6 +89,11 @@ CONFIGS = {
     "c3p4": dict(dim=3, k=2, trees=[(0, 0, 0)], global_refinements=3,
                  rule="sphere_surface", center=((1, 2), (1, 2), (1, 2)), radius=(3, 10),
                  shell=(0, 1), passes=4),
+    # a 2x2x2 brick of trees (multi-cell coarse mesh: 27 free Q2 DoFs on level 0)
+    # for the Chebyshev coarse solver; test case, not a BASELINE config
+    "brick8": dict(dim=3, k=2, trees=[(x, y, z) for z in (0, 1) for y in (0, 1) for x in (0, 1)],
+                   global_refinements=1, rule="sphere_surface", center=((1, 1), (1, 1), (1, 1)),
+                   radius=(3, 5), shell=(0, 1), passes=2),
     # configs[3]: 3D variable coefficient, corner-graded toward (0,0,0)
     # (SURVEY c.2#20: dist(closure T, 0) <= 2^(s - level), level < lmax).  lmax
     # = 19 is the first value reaching ~100M leaf nodes (reading R20: 13,193,951

@@ -199,8 +199,13 @@ typedef struct {
   int rank, n_ranks;        /* this process' rank; must equal the partition's n_ranks */
   void *nccl_comm;          /* ncclComm_t for n_ranks > 1 (not yet used), else NULL */
   int device;               /* CUDA device ordinal; -1 = current */
-  uint32_t flags;           /* GMG_HOST_ONLY | GMG_NO_GRAPH */
+  uint32_t flags;           /* GMG_HOST_ONLY | GMG_NO_GRAPH | GMG_MIXED_PRECISION | ... */
+  int coarse_solver;        /* GMG_COARSE_CHOLESKY (default: dense Cholesky of A_0^S, P:331-334,
+                               reading R12) or GMG_COARSE_CHEBYSHEV (reading R28) */
 } gmg_params;
+
+#define GMG_COARSE_CHOLESKY 0
+#define GMG_COARSE_CHEBYSHEV 1
 
 /* Fills *p with the defaults above (k = 2). */
 void gmg_params_default(gmg_params *p);
@@ -305,6 +310,9 @@ gmg_status gmg_level_diagonal(gmg_hierarchy *h, int level, double *diag_dev, voi
 
 /* lambda_bar of D^{-1} A_l^S; set overrides it (parity decoupling). */
 gmg_status gmg_get_eigen(const gmg_hierarchy *h, int level, double *lambda_bar);
+/* GMG_COARSE_CHEBYSHEV: the coarse Chebyshev range [lo, hi] of D^-1 A_0^S and its
+ * a priori degree (0 with the Cholesky coarse solver). */
+gmg_status gmg_get_coarse_chebyshev(const gmg_hierarchy *h, double *lo, double *hi, int *degree);
 gmg_status gmg_set_eigen(gmg_hierarchy *h, int level, double lambda_bar);
 
 /* Kernel launches issued by the library since creation (evidence counter). */

@@ -15,7 +15,13 @@ Level-cell storage of the paper's algorithm:
       4. V(l-1)
       5. x^{S u E} += (P_l x_{l-1})^{S u E}
       6. x^S = Cheb(A^S, d^S - A^{SE} x^E, x^S)
-  and x_0^S = (A_0^S)^{-1} d_0^S at l = 0 (direct coarse solver P:331).
+  and x_0^S = (A_0^S)^{-1} d_0^S at l = 0 (direct coarse solver P:331),
+  or -- coarse="chebyshev", P:890-895 -- x_0^S = Chebyshev iteration from 0 on
+  D^{-1} A_0^S over the full eigenvalue range [lambda_min, lambda_max] of the
+  Lanczos tridiagonal of a Jacobi-PCG run to relative unpreconditioned residual
+  1e-3, with the smallest degree m whose a priori bound
+  2 rho^m / (1 + rho^(2m)) (rho = (sqrt(kappa) - 1)/(sqrt(kappa) + 1),
+  kappa = lambda_max / lambda_min) is <= 1e-3 (reading R28).
   copy_to_mg: d_{lambda(n)}[n] = b[n]; copy_from_mg: u[n] = x_{lambda(n)}[n].
 * Chebyshev-Jacobi smoother: first-kind Chebyshev iteration on
   D^{-1} A^S over [0.08 lambda, 1.2 lambda] (reading R7/R8), degree m = 4
@@ -67,6 +73,7 @@ class Hierarchy:
     b_leaf: np.ndarray
     degree: int = 4
     coarse_factor: object = None
+    coarse_cheb: object = None      # (lambda_min, lambda_max, degree) for coarse="chebyshev"
     lam_slot: list = field(default_factory=list)   # per level: (level index of free DoFs)
 
     @property
@@ -111,7 +118,7 @@ def topology(f: Forest, k: int, n_ranks: int = 1) -> Topology:
 
 
 def build(f: Forest, k: int, n_ranks: int = 1, coef_level2: np.ndarray | None = None,
-          degree: int = 4, eig=True, rhs="one") -> Hierarchy:
+          degree: int = 4, eig=True, rhs="one", coarse: str = "cholesky") -> Hierarchy:
     lat = Lattice(f, k)
     owners = leaf_owners(f, n_ranks)
     cells = level_cells(f, owners)
@@ -149,12 +156,16 @@ def build(f: Forest, k: int, n_ranks: int = 1, coef_level2: np.ndarray | None = 
         assert np.all(lk[p] == q)
         slots[sel] = p
     h.lam_slot = slots
-    # coarse solver: dense Cholesky of A_0^S
+    # coarse solver: dense Cholesky of A_0^S or a priori Chebyshev
     l0 = levels[0]
     nS0 = int(l0.S.sum())
-    if nS0:
+    if nS0 and coarse == "cholesky":
         A0 = l0.K[l0.S][:, l0.S].toarray()
         h.coarse_factor = sla.cho_factor(A0)
+    elif nS0 and coarse == "chebyshev":
+        h.coarse_cheb = coarse_chebyshev_setup(l0)
+    elif coarse not in ("cholesky", "chebyshev"):
+        raise ValueError(coarse)
     if eig:
         for l in range(1, len(levels)):
             levels[l].lam = eigen_estimate(levels[l])
@@ -225,6 +236,54 @@ def eigen_estimate(lev: Level, iters: int = 10) -> float:
     return float(np.linalg.eigvalsh(T).max())
 
 
+COARSE_REDUCTION = 1e-3      # P:892-893 "residual reduction by 10^3"
+COARSE_CG_TOL = 1e-3         # P:894-895 "relative tolerance ... of 10^-3"
+
+
+def chebyshev_degree(kappa: float, eps: float = COARSE_REDUCTION) -> int:
+    """Smallest m with the classical Chebyshev bound 2 rho^m / (1 + rho^(2m)) <= eps,
+    rho = (sqrt(kappa) - 1) / (sqrt(kappa) + 1)."""
+    if kappa <= 1.0 + 1e-12:
+        return 1
+    rho = (np.sqrt(kappa) - 1.0) / (np.sqrt(kappa) + 1.0)
+    m = 1
+    while 2.0 * rho ** m / (1.0 + rho ** (2 * m)) > eps:
+        m += 1
+    return m
+
+
+def coarse_chebyshev_setup(lev: Level):
+    """(lambda_min, lambda_max, degree) of the coarse Chebyshev solver."""
+    nS = int(lev.S.sum())
+    S = lev.S
+    alphas, betas = cg_lanczos(lev.K[S][:, S], lev.Dinv[S], eigen_rhs(lev)[S], nS, tol=COARSE_CG_TOL)
+    ev = np.linalg.eigvalsh(lanczos_tridiag(alphas, betas))
+    lo, hi = float(ev.min()), float(ev.max())
+    return lo, hi, chebyshev_degree(hi / lo)
+
+
+def chebyshev_range(lev: Level, g: np.ndarray, lam_lo: float, lam_hi: float, degree: int) -> np.ndarray:
+    """First-kind Chebyshev-Jacobi from x = 0 over [lam_lo, lam_hi] (SURVEY c.1 step 9)."""
+    theta = 0.5 * (lam_hi + lam_lo)
+    delta = 0.5 * (lam_hi - lam_lo)
+    A, Dinv = lev.K, lev.Dinv
+    x = np.zeros_like(g)
+    r = Dinv * g
+    if delta <= 1e-14 * theta:              # one eigenvalue: the first step is exact
+        return r / theta
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    dvec = r / theta
+    for j in range(degree):
+        x = x + dvec
+        if j < degree - 1:
+            r = r - Dinv * (A @ dvec)
+            rho_new = 1.0 / (2.0 * sigma - rho)
+            dvec = rho_new * rho * dvec + (2.0 * rho_new / delta) * r
+            rho = rho_new
+    return x
+
+
 # --------------------------------------------------------------------------
 # smoother and V-cycle
 # --------------------------------------------------------------------------
@@ -262,6 +321,9 @@ def coarse_solve(h: Hierarchy, d0: np.ndarray) -> np.ndarray:
     x = np.zeros_like(d0)
     if h.coarse_factor is not None:
         x[lev.S] = sla.cho_solve(h.coarse_factor, d0[lev.S])
+    elif getattr(h, "coarse_cheb", None) is not None:
+        lo, hi, m = h.coarse_cheb
+        x = chebyshev_range(lev, d0 * lev.S, lo, hi, m)
     return x
 
 

@@ -80,7 +80,8 @@ class Model(C.Structure):
 class Params(C.Structure):
     _fields_ = [("k", C.c_int), ("cheb_degree", C.c_int), ("cheb_lo", C.c_double), ("cheb_hi", C.c_double),
                 ("eig_iters", C.c_int), ("coef_level2", C.POINTER(C.c_double)), ("rank", C.c_int),
-                ("n_ranks", C.c_int), ("nccl_comm", C.c_void_p), ("device", C.c_int), ("flags", C.c_uint32)]
+                ("n_ranks", C.c_int), ("nccl_comm", C.c_void_p), ("device", C.c_int), ("flags", C.c_uint32),
+                ("coarse_solver", C.c_int)]
 
 
 class Info(C.Structure):
@@ -123,6 +124,7 @@ _SIGS = {
     "gmg_level_apply": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_level_apply_kernel": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_level_apply_kernel_f32": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
+    "gmg_get_coarse_chebyshev": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)], C.c_int),
     "gmg_restrict": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_prolongate": ([_vp, C.c_int, _vp, _vp, _vp], C.c_int),
     "gmg_leaf_apply": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -394,6 +396,12 @@ class Hierarchy:
     def level_diagonal(self, level, diag, stream=None):
         _check(_lib.gmg_level_diagonal(self.h, level, _ptr(diag), _stream(stream)))
 
+    def coarse_chebyshev(self):
+        """(lambda_min, lambda_max, degree) of the Chebyshev coarse solver (degree 0: Cholesky)."""
+        lo, hi, m = C.c_double(), C.c_double(), C.c_int()
+        _check(_lib.gmg_get_coarse_chebyshev(self.h, C.byref(lo), C.byref(hi), C.byref(m)))
+        return lo.value, hi.value, m.value
+
     def get_eigen(self, level):
         v = C.c_double()
         _check(_lib.gmg_get_eigen(self.h, level, C.byref(v)))
@@ -445,7 +453,8 @@ class NcclComm:
 
 
 def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
-              coef_level2=None, graph=True, device=-1, comm=None, mixed=False) -> Hierarchy:
+              coef_level2=None, graph=True, device=-1, comm=None, mixed=False,
+              coarse="cholesky") -> Hierarchy:
     """comm: None (one rank), a LocalWorld (ranks as threads) or an NcclComm."""
     p = gmg_params_default()
     p.k = k
@@ -455,6 +464,7 @@ def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_deg
     p.device = device
     p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH) | \
         (GMG_MIXED_PRECISION if mixed else 0)
+    p.coarse_solver = {"cholesky": 0, "chebyshev": 1}[coarse]
     if isinstance(comm, LocalWorld):
         p.flags |= GMG_LOCAL_RANKS
         p.nccl_comm = comm.h

@@ -193,6 +193,7 @@ void gmg_params_default(gmg_params* p) {
   p->nccl_comm = nullptr;
   p->device = -1;
   p->flags = 0;
+  p->coarse_solver = GMG_COARSE_CHOLESKY;
 }
 
 gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_params* prm, gmg_hierarchy** out) {
@@ -207,6 +208,8 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
     GMG_REQUIRE(prm->cheb_degree >= 1 && prm->cheb_degree <= 16, GMG_E_INVALID_ARG, "cheb_degree");
     GMG_REQUIRE(prm->cheb_lo > 0 && prm->cheb_hi > prm->cheb_lo, GMG_E_INVALID_ARG, "cheb range");
     GMG_REQUIRE(prm->eig_iters >= 1, GMG_E_INVALID_ARG, "eig_iters");
+    GMG_REQUIRE(prm->coarse_solver == GMG_COARSE_CHOLESKY || prm->coarse_solver == GMG_COARSE_CHEBYSHEV,
+                GMG_E_INVALID_ARG, "coarse_solver");
     auto h = std::make_unique<gmg_hierarchy>();
     h->prm = *prm;
     h->topo = gmg::make_topology(f->f, p->p, prm->k);
@@ -473,6 +476,17 @@ gmg_status gmg_level_diagonal(gmg_hierarchy* h, int level, double* diag, void* s
     NEED(diag);
     need_level(h, level);
     gmg::device_level_diagonal(need_dev(h), level, diag, s);
+  });
+}
+
+gmg_status gmg_get_coarse_chebyshev(const gmg_hierarchy* h, double* lo, double* hi, int* degree) {
+  return guard([&] {
+    NEED(h);
+    NEED(lo);
+    NEED(hi);
+    NEED(degree);
+    GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "hierarchy has no device data (GMG_HOST_ONLY)");
+    gmg::device_coarse_chebyshev(h->dev, lo, hi, degree);
   });
 }
 

@@ -62,6 +62,8 @@ struct DeviceHierarchy {
   // mixed precision (GMG_MIXED_PRECISION): the V-cycle runs on fp32 copies
   // of the MG-layout buffers; CG and the setup stay fp64
   bool mixed = false;
+  bool coarse_cheb = false;     // GMG_COARSE_CHEBYSHEV instead of dense Cholesky
+  double coarse_lo = 0, coarse_hi = 0;
   float *D32 = nullptr, *X32 = nullptr, *T32 = nullptr, *DV32 = nullptr;
   double *cx = nullptr, *cr = nullptr, *cp = nullptr, *cq = nullptr, *cz = nullptr;
   double *sbuf = nullptr, *rbuf = nullptr;
@@ -251,7 +253,8 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
 template <typename T>
 static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, bool x_zero, cudaStream_t s) {
   DevLevel& v = d->lv[l];
-  const int m = d->m;
+  const int m = (int)v.c1.size();     // degree d->m on levels >= 1, the coarse degree on level 0
+  if (m == 0) return;
   if (x_zero) {
     k_cheb<T, false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else {
@@ -267,7 +270,11 @@ static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, boo
 }
 
 template <typename T>
-static void coarse(DeviceHierarchy* d, const T* d0, T* x0, cudaStream_t s) {
+static void coarse(DeviceHierarchy* d, T* d0, T* x0, T* t0, T* dv0, cudaStream_t s) {
+  if (d->coarse_cheb) {                 // collective: every rank joins the level-0 exchanges
+    smooth(d, 0, d0, x0, t0, dv0, true, s);
+    return;
+  }
   if (d->nS0 == 0) return;
   dev::coarse_solve<T><<<1, 256, 0, s>>>(d->nS0, d->coarse_idx, d->coarse_inv, d0, x0);
   d->launches++;
@@ -287,7 +294,7 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
     k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
     export_add(d, l - 1, gc, s);
   }
-  coarse(d, D + d->lv[0].off, X + d->lv[0].off, s);                         // 4: coarse solve (rank 0)
+  coarse(d, D + d->lv[0].off, X + d->lv[0].off, Tb + d->lv[0].off, DV + d->lv[0].off, s);   // 4: coarse solve
   for (int l = 1; l <= L; ++l) {
     DevLevel& v = d->lv[l];
     T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
@@ -359,22 +366,31 @@ static double host_dot(DeviceHierarchy* d, i64 n, const double* a, const double*
   return d->hscal[7];
 }
 
-static void set_cheb(DeviceHierarchy* d, int l) {
-  DevLevel& v = d->lv[l];
-  v.c1.assign(d->m, 0.0);
-  v.c2.assign(d->m, 0.0);
-  if (!(v.lam > 0)) return;
-  const double hi = d->hi * v.lam, lo = d->lo * v.lam;
-  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
-  double rho = 1.0 / sigma;
-  v.c1[0] = 0.0;
+// first-kind Chebyshev coefficients over [lo, hi], degree m (SURVEY c.1 step 9)
+static void set_cheb_range(DevLevel& v, double lo, double hi, int m) {
+  v.c1.assign(m, 0.0);
+  v.c2.assign(m, 0.0);
+  if (!(hi > 0)) return;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo);
   v.c2[0] = 1.0 / theta;
-  for (int j = 1; j < d->m; ++j) {
+  if (!(delta > 1e-14 * theta)) {        // one eigenvalue: the first step is exact
+    v.c1.resize(1);
+    v.c2.resize(1);
+    return;
+  }
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  for (int j = 1; j < m; ++j) {
     double rn = 1.0 / (2.0 * sigma - rho);
     v.c1[j] = rn * rho;
     v.c2[j] = 2.0 * rn / delta;
     rho = rn;
   }
+}
+
+static void set_cheb(DeviceHierarchy* d, int l) {
+  DevLevel& v = d->lv[l];
+  set_cheb_range(v, d->lo * v.lam, d->hi * v.lam, d->m);
 }
 
 // largest eigenvalue of a symmetric tridiagonal matrix (cyclic Jacobi on the
@@ -413,15 +429,23 @@ static double tridiag_max_eig(const std::vector<double>& a, const std::vector<do
   for (int i = 0; i < m; ++i) mx = std::max(mx, A[(size_t)i * m + i]);
   return mx;
 }
+static double tridiag_min_eig(std::vector<double> a, std::vector<double> b) {
+  for (auto& v : a) v = -v;
+  for (auto& v : b) v = -v;
+  return -tridiag_max_eig(a, b);
+}
 
 // CG (Jacobi preconditioned) on A^S x = v, v = (-5.5, ..., 5.5, -5.5, ...)
-// over the S DoFs in canonical order, min(eig_iters, n_S) iterations, Lanczos
-// tridiagonal from the CG coefficients, lambda = its largest eigenvalue.
-// Collective over ranks (global dots, same control flow everywhere).
-static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
+// over the S DoFs in canonical order, at most maxit iterations, stopping when the
+// unpreconditioned residual falls below tol ||r_0||; Lanczos tridiagonal from the
+// CG coefficients; its extreme eigenvalues.  Collective over ranks (global dots,
+// same control flow everywhere).
+static void lanczos_range(DeviceHierarchy* d, int l, int maxit, double tol, double* lo, double* hi,
+                          cudaStream_t s) {
   DevLevel& v = d->lv[l];
   const i64 n = v.n;
-  if (v.nS_global == 0) return 0.0;
+  *lo = *hi = 0.0;
+  if (v.nS_global == 0) return;
   double *r = d->X + v.off, *z = d->DV + v.off, *p = d->W + v.off, *q = d->Y + v.off;
   const int gr = (int)((n + 255) / 256);
   if (n > 0) {
@@ -433,8 +457,7 @@ static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
   double rz = host_dot(d, n, r, z, s);
   double r0 = std::sqrt(host_dot(d, n, r, r, s));
   std::vector<double> alphas, betas;
-  if (rz == 0.0 || r0 == 0.0) return 0.0;
-  const int maxit = (int)std::min<i64>(d->eig_iters, v.nS_global);
+  if (rz == 0.0 || r0 == 0.0) return;
   for (int it = 0; it < maxit; ++it) {
     if (n > 0) CK(cudaMemsetAsync(q, 0, n * sizeof(double), s));
     apply_full(d, l, p, q, s);
@@ -452,7 +475,7 @@ static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
     }
     double rz_new = host_dot(d, n, r, z, s);
     double rn = std::sqrt(host_dot(d, n, r, r, s));
-    if (rn <= 1e-10 * r0 || rz_new == 0.0) break;
+    if (rn <= tol * r0 || rz_new == 0.0) break;
     double beta = rz_new / rz;
     betas.push_back(beta);
     if (n > 0) {
@@ -467,7 +490,26 @@ static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
     a[j] = 1.0 / alphas[j] + (j > 0 ? betas[j - 1] / alphas[j - 1] : 0.0);
     if (j > 0) b[j - 1] = std::sqrt(betas[j - 1]) / alphas[j - 1];
   }
-  return tridiag_max_eig(a, b);
+  *hi = tridiag_max_eig(a, b);
+  *lo = tridiag_min_eig(a, b);
+}
+
+// lambda_bar of level l >= 1: min(eig_iters, n_S) iterations (reading R11)
+static double eigen_estimate(DeviceHierarchy* d, int l, cudaStream_t s) {
+  double lo, hi;
+  lanczos_range(d, l, (int)std::min<i64>(d->eig_iters, d->lv[l].nS_global), 1e-10, &lo, &hi, s);
+  return hi;
+}
+
+// P:890-895 coarse solver: Chebyshev over the full eigenvalue range of D^-1 A_0^S
+// (Lanczos of a CG run to relative unpreconditioned residual 1e-3) with the smallest
+// degree whose a priori bound 2 rho^m / (1 + rho^2m) is <= 1e-3 (reading R28).
+static int chebyshev_degree(double kappa, double eps) {
+  if (!(kappa > 1.0 + 1e-12)) return 1;
+  const double rho = (std::sqrt(kappa) - 1.0) / (std::sqrt(kappa) + 1.0);
+  int m = 1;
+  while (2.0 * std::pow(rho, m) / (1.0 + std::pow(rho, 2 * m)) > eps && m < 100000) ++m;
+  return m;
 }
 
 // ---------------------------------------------------------------- creation
@@ -490,6 +532,7 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     d->n0_global = n0_global;
     d->use_graph = !(prm.flags & GMG_NO_GRAPH) && (!d->comm || d->comm->capturable());
     d->mixed = (prm.flags & GMG_MIXED_PRECISION) != 0;
+    d->coarse_cheb = prm.coarse_solver == GMG_COARSE_CHEBYSHEV;
     if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
@@ -603,7 +646,7 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     GMG_REQUIRE(hbad == 0, GMG_E_ZERO_DIAG, "zero or negative diagonal on an S row");
     // coarse matrix A_0^S (all level-0 DoFs owned by rank 0): columns by a
     // collective apply of K_0 to unit vectors; dense Cholesky on rank 0
-    {
+    if (!d->coarse_cheb) {
       DevLevel& v0 = d->lv[0];
       const int n0 = (int)n0_global;
       d->nS0 = (int)v0.n_owned;
@@ -660,6 +703,12 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
     for (int l = 1; l <= Tp.L; ++l) {
       d->lv[l].lam = eigen_estimate(d, l, s);
       set_cheb(d, l);
+    }
+    if (d->coarse_cheb) {
+      DevLevel& v0 = d->lv[0];
+      lanczos_range(d, 0, (int)std::max<i64>(v0.nS_global, 1), 1e-3, &d->coarse_lo, &d->coarse_hi, s);
+      const int m0 = d->coarse_hi > 0 ? chebyshev_degree(d->coarse_hi / d->coarse_lo, 1e-3) : 0;
+      set_cheb_range(v0, d->coarse_lo, d->coarse_hi, m0);
     }
     // restore the work buffers to zero (T must be zero between applies)
     for (double* p : {d->X, d->T, d->DV, d->W, d->Y}) CK(cudaMemsetAsync(p, 0, N * sizeof(double), s));
@@ -885,6 +934,12 @@ void device_level_diagonal(DeviceHierarchy* d, int l, double* diag, void* stream
 }
 
 double device_get_eigen(const DeviceHierarchy* d, int l) { return d->lv[l].lam; }
+
+void device_coarse_chebyshev(const DeviceHierarchy* d, double* lo, double* hi, int* degree) {
+  *lo = d->coarse_lo;
+  *hi = d->coarse_hi;
+  *degree = d->coarse_cheb ? (int)d->lv[0].c1.size() : 0;
+}
 
 void device_set_eigen(DeviceHierarchy* d, int l, double lam) {
   d->lv[l].lam = lam;

@@ -27,6 +27,7 @@ void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* str
 void device_level_smooth(DeviceHierarchy* d, int level, const double* g, double* x, int x_zero, void* stream);
 void device_level_diagonal(DeviceHierarchy* d, int level, double* diag, void* stream);
 double device_get_eigen(const DeviceHierarchy* d, int level);
+void device_coarse_chebyshev(const DeviceHierarchy* d, double* lo, double* hi, int* degree);
 void device_set_eigen(DeviceHierarchy* d, int level, double lam);
 long long device_launches(const DeviceHierarchy* d);
 void device_launch_profile(const DeviceHierarchy* d, long long* per_vcycle, long long* per_leaf_apply);

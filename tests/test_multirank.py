@@ -165,7 +165,7 @@ def _coef(cfg):
     return None
 
 
-def _local_group(cfg, p):
+def _local_group(cfg, p, **kw):
     import torch
     world = G.LocalWorld(p)
     lf = G.gmg_forest_generate(G.recipe_from_config(cfg))
@@ -176,7 +176,7 @@ def _local_group(cfg, p):
     def setup(r):
         def fn():
             torch.cuda.set_device(0)
-            hs[r] = G.gmg_setup(lf, part, k=cfg["k"], rank=r, comm=world, coef_level2=_coef(cfg))
+            hs[r] = G.gmg_setup(lf, part, k=cfg["k"], rank=r, comm=world, coef_level2=_coef(cfg), **kw)
         return fn
 
     _run_threads([setup(r) for r in range(p)])
@@ -194,15 +194,20 @@ def test_nccl_transport_loads():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,p", [("c1", 2), ("c1", 3), ("c3p2", 2), ("c3p2", 4), ("c2", 3), ("c4s", 3)])
+@pytest.mark.parametrize("name,p", [("c1", 2), ("c1", 3), ("c3p2", 2), ("c3p2", 4), ("c2", 3), ("c4s", 3),
+                                    ("brick8-cheb", 3), ("brick8-cheb", 5)])
 def test_local_ranks_equal_single_rank(name, p):
     import torch
+    kw = {}
     if name == "c4s":      # config-4 recipe at a small size (variable coefficient)
         cfg = config("c4")
         cfg.update(s=2, lmax=7)
+    elif name == "brick8-cheb":   # multi-cell coarse mesh, collective Chebyshev coarse solver
+        cfg = config("brick8")
+        kw = {"coarse": "chebyshev"}
     else:
         cfg = config(name)
-    _, _, h1 = G.build_config(cfg, coef_level2=_coef(cfg))
+    _, _, h1 = G.build_config(cfg, coef_level2=_coef(cfg), **kw)
     n = h1.info()["n_leaf_free"]
     canon1 = h1.leaf_dofs()[3]
     b_can = uniform_pm1(n)
@@ -218,7 +223,7 @@ def test_local_ranks_equal_single_rank(name, p):
     ref_s = np.empty(n)
     ref_s[canon1] = xs1.cpu().numpy()
 
-    world, lf, part, hs, streams = _local_group(cfg, p)
+    world, lf, part, hs, streams = _local_group(cfg, p, **kw)
     canon = hs[0].leaf_dofs()[3]
     res = [None] * p
 
