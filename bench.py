@@ -189,7 +189,7 @@ def run_ours(args):
         cfg = config(args.config)
     t0 = time.time()
     f = G.gmg_forest_generate(G.recipe_from_config(cfg))
-    part = G.gmg_partition(f, world)
+    part = G.gmg_partition(f, world, mode=args.partition)
     comm = None
     if world > 1:
         uid = [G.gmg_nccl_get_unique_id() if rank == 0 else None]
@@ -330,7 +330,9 @@ def run_ours(args):
                                 % (info["mg_vector_len"] * 8 / 1e6),
                           "parallelism": "single GPU" if world == 1 else
                           f"{world} ranks, SFC partition + first-child rule, NCCL ghost exchange",
-                          "partition_eta": model["eta"], "setup_s": round(setup_s, 2)},
+                          "partition": args.partition, "partition_eta": model["eta"],
+                          "ghost_children_ratio": sum(model["ghost_children"]) / max(sum(model["children"]), 1),
+                          "setup_s": round(setup_s, 2)},
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic,
                             "traffic_source": traffic_src if traffic is not None else None,
@@ -363,6 +365,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--cheb-degree", type=int, default=4)
+    ap.add_argument("--partition", default="first_child", choices=["first_child", "per_level"],
+                    help="level ownership: first-child rule (P:604, default) or per-level SFC balance (P:597)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
                     help="fp64 V-cycle (default, BASELINE) or fp32 V-cycle inside the fp64 CG (P:897)")
     ap.add_argument("--profile", action="store_true", help="cudaProfilerStart/Stop around one V-cycle")

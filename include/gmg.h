@@ -125,6 +125,16 @@ gmg_status gmg_export_leaves(const gmg_forest *f, int32_t *leaf_tree, int8_t *le
  * of its subtree.  Pure integer work, no communication.
  * Errors: INVALID_ARG when n_ranks < 1. */
 gmg_status gmg_partition(const gmg_forest *f, int n_ranks, gmg_partitioning **out);
+/* mode GMG_PARTITION_FIRST_CHILD: as gmg_partition.  GMG_PARTITION_PER_LEVEL: the
+ * alternative the paper contrasts with (reading R29):
+ * every level is partitioned on its own along the SFC, families (the 2^d children
+ * of one parent; single cells on level 0) kept whole: the family starting at cell
+ * index c of the N_l cells of level l goes to rank floor(n_ranks c / N_l).  Leaves
+ * keep the leaf-interval owners for the leaf vectors; level owners balance every
+ * level (eta ~ 1) at the price of more ghost children (transfer communication). */
+#define GMG_PARTITION_FIRST_CHILD 0
+#define GMG_PARTITION_PER_LEVEL 1
+gmg_status gmg_partition_mode(const gmg_forest *f, int n_ranks, int mode, gmg_partitioning **out);
 gmg_status gmg_partition_destroy(gmg_partitioning *p);
 
 #define GMG_MAX_LEVELS 64

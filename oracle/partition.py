@@ -127,3 +127,26 @@ def ghost_children(cells: list[LevelCells]) -> tuple[np.ndarray, np.ndarray]:
         ghosts[l] = int((ch.owner != par.owner[idx]).sum())
         total[l] = ch.gc.shape[0]
     return ghosts, total
+
+
+def per_level_owners(cells: list[LevelCells], p: int) -> list[LevelCells]:
+    """The alternative to the first-child rule that P:597 contrasts with (SURVEY
+    §8(f) row 4, reading R29): each level partitioned on its own along
+    the SFC, families (cells with a common parent; single cells on level 0) kept
+    whole.  Written as a plain loop: a family whose first cell has index c among
+    the N_l cells of level l goes to rank floor(p c / N_l)."""
+    out = []
+    for l, lc in enumerate(cells):
+        n = lc.gc.shape[0]
+        owner = np.empty(n, dtype=np.int64)
+        c = 0
+        while c < n:
+            e = c + 1
+            if l > 0:
+                parent = tuple(lc.gc[c] >> 1)
+                while e < n and tuple(lc.gc[e] >> 1) == parent:
+                    e += 1
+            owner[c:e] = (p * c) // n
+            c = e
+        out.append(LevelCells(lc.level, lc.gc, lc.key, lc.is_leaf, owner))
+    return out

@@ -106,6 +106,7 @@ _SIGS = {
     "gmg_forest_info": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int)], C.c_int),
     "gmg_export_leaves": ([_vp, _vp, _vp, _vp], C.c_int),
     "gmg_partition": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
+    "gmg_partition_mode": ([_vp, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "gmg_partition_destroy": ([_vp], C.c_int),
     "gmg_partition_model": ([_vp, C.c_int64, C.POINTER(Model)], C.c_int),
     "gmg_export_tallies": ([_vp, _vp], C.c_int),
@@ -284,9 +285,14 @@ class Partitioning:
         return key, own, leaf
 
 
-def gmg_partition(forest: Forest, n_ranks: int) -> Partitioning:
+PARTITION_MODES = {"first_child": 0, "per_level": 1}
+
+
+def gmg_partition(forest: Forest, n_ranks: int, mode: str = "first_child") -> Partitioning:
+    """SFC partition with the first-child rule or, mode="per_level",
+    every level balanced on its own (P:597 alternative, reading R29)."""
     h = _vp()
-    _check(_lib.gmg_partition(forest.h, n_ranks, C.byref(h)))
+    _check(_lib.gmg_partition_mode(forest.h, n_ranks, PARTITION_MODES[mode], C.byref(h)))
     return Partitioning(h, forest, n_ranks)
 
 

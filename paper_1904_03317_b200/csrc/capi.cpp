@@ -138,6 +138,17 @@ gmg_status gmg_partition(const gmg_forest* f, int n_ranks, gmg_partitioning** ou
   });
 }
 
+gmg_status gmg_partition_mode(const gmg_forest* f, int n_ranks, int mode, gmg_partitioning** out) {
+  return guard([&] {
+    NEED(f);
+    NEED(out);
+    auto p = std::make_unique<gmg_partitioning>();
+    p->forest = f;
+    p->p = gmg::make_partition(f->f, n_ranks, mode);
+    *out = p.release();
+  });
+}
+
 gmg_status gmg_partition_destroy(gmg_partitioning* p) {
   delete p;
   return GMG_OK;

@@ -59,11 +59,12 @@ struct LevelCells {
 struct Partition {
   const Forest* f = nullptr;
   int n_ranks = 1;
+  int mode = GMG_PARTITION_FIRST_CHILD;
   std::vector<i32> leaf_owner;
   std::vector<LevelCells> levels;
 };
 
-Partition make_partition(const Forest& f, int n_ranks);
+Partition make_partition(const Forest& f, int n_ranks, int mode = GMG_PARTITION_FIRST_CHILD);
 gmg_model partition_model(const Partition& p, i64 W0_override);
 
 // ------------------------------------------------------------------ topology

@@ -11,11 +11,14 @@
 
 namespace gmg {
 
-Partition make_partition(const Forest& f, int n_ranks) {
+Partition make_partition(const Forest& f, int n_ranks, int mode) {
   GMG_REQUIRE(n_ranks >= 1, GMG_E_INVALID_ARG, "n_ranks must be >= 1");
+  GMG_REQUIRE(mode == GMG_PARTITION_FIRST_CHILD || mode == GMG_PARTITION_PER_LEVEL, GMG_E_INVALID_ARG,
+              "partition mode");
   Partition p;
   p.f = &f;
   p.n_ranks = n_ranks;
+  p.mode = mode;
   const i64 N = f.n_leaves();
   p.leaf_owner.resize(N);
   {
@@ -59,6 +62,21 @@ Partition make_partition(const Forest& f, int n_ranks) {
       auto it = std::lower_bound(lk.begin(), lk.end(), pk);
       GMG_REQUIRE(it != lk.end() && *it == pk, GMG_E_STATE, "first leaf of subtree not found");
       lc.owner[c] = p.leaf_owner[it - lk.begin()];
+    }
+    if (mode == GMG_PARTITION_PER_LEVEL) {
+      // P:597 alternative (reading R29): every level partitioned on its own along the
+      // SFC, whole families (children of one parent; single cells on level 0) kept
+      // together: the family starting at cell index c (of N_l) goes to rank
+      // floor(n_ranks * c / N_l).
+      const i64 n = (i64)lc.key.size();
+      for (i64 c = 0; c < n;) {
+        i64 e = c + 1;
+        if (l > 0)
+          while (e < n && (lc.key[e] >> d) == (lc.key[c] >> d)) ++e;
+        const i32 r = (i32)((__int128)n_ranks * c / n);
+        for (i64 q = c; q < e; ++q) lc.owner[q] = r;
+        c = e;
+      }
     }
   }
   return p;

@@ -188,10 +188,12 @@ Topology make_topology(const Forest& f, const Partition& p, int k) {
           for (int c = 0; c < nch; ++c)
             if ((pt.childmask[a] & (1u << c)) && cells.leaf[fi * nch + c]) fl |= F_LEAF;
           oflag[o] = fl;
-          // DoF owner = min owner of the families (= of their parents, first-child
-          // rule) whose patch contains the node (R25): the rank that computes a
-          // family owns at least one DoF-containing family of each DoF it owns
-          oown[o] = par.owner[t.fam_parent[fi]];
+          // DoF owner = min owner of the families whose patch contains the node
+          // (R25); a family belongs to the owner of its cells (= its parent's owner
+          // under the first-child rule; its own rank under per-level
+          // partitioning, R29): the rank that computes a family owns at least one
+          // DoF-containing family of each DoF it owns
+          oown[o] = cells.owner[fi * nch];
         }
       }
     }
