@@ -657,6 +657,21 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
     __syncwarp();
     if (tt + GW < nfam) row_fetch<D, K>(xfer, fam_list, tt + GW, lane, nxt);
     const int* rw = srow[w];
+    // one memory round trip per family: the parent's values and the owned fine
+    // values (read-modify-write below) are requested together, before the passes
+    constexpr int NIT = (NP + 31) / 32;
+    int vi[NIT];
+    T old[NIT];
+#pragma unroll
+    for (int q = 0; q < NIT; ++q) {
+      const int a = lane + 32 * q;
+      vi[q] = a < NP ? rw[a] : -1;    // < 0: not owned / Dirichlet
+      old[q] = 0;
+      if (vi[q] >= 0) {
+        if (MODE == XFER_SET_E) old[q] = (cls_fine[vi[q]] & 1) ? T(1) : T(0);
+        else old[q] = xf[vi[q]];
+      }
+    }
     if (lane < NC) {
       const int ci = rw[NP + lane];
       b0[w][lane] = ci >= 0 ? __ldg(xc + ci) : T(0);
@@ -678,19 +693,6 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
       fine = b0[w];
     }
     __syncwarp();
-    constexpr int NIT = (NP + 31) / 32;
-    int vi[NIT];
-    T old[NIT];
-#pragma unroll
-    for (int q = 0; q < NIT; ++q) {   // all loads first: one memory round trip per family
-      const int a = lane + 32 * q;
-      vi[q] = a < NP ? rw[a] : -1;    // < 0: not owned / Dirichlet
-      old[q] = 0;
-      if (vi[q] >= 0) {
-        if (MODE == XFER_SET_E) old[q] = (cls_fine[vi[q]] & 1) ? T(1) : T(0);
-        else old[q] = xf[vi[q]];
-      }
-    }
 #pragma unroll
     for (int q = 0; q < NIT; ++q) {
       const int a = lane + 32 * q;
