@@ -16,6 +16,7 @@
 #include "comm.hpp"
 #include "device.hpp"
 #include "kernels.cuh"
+#include "plan.hpp"
 
 namespace gmg {
 
@@ -37,6 +38,8 @@ struct DevLevel {
   float* Dinv32 = nullptr;          // the same in fp32 (mixed-precision V-cycle)
   int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
+  i64 n_r1 = 0;                     // device order (plan.hpp): rows [0, n_r1) finished by the fused apply
+  int* perm = nullptr;              // rank-local level index -> device index (API boundary)
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
   double h = 1, scale = 1;          // scale = h^(d-2)
@@ -247,6 +250,39 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
   d->launches++;
 }
 
+// One Chebyshev step j >= 1 (or the first from a nonzero x): t = K x with the
+// rows of R1 finished inside the operator kernel (fam_tensor_apply<TM>), the rest
+// by the streaming pass over [n_r1, n_pad).  Falls back to operator + full-level
+// streaming step where the level has no R1 (2D, coefficient levels, level 0).
+template <typename T, int TM, bool RDV, bool WDV>
+static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, double c1, double c2,
+                            cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  import_ghosts(d, l, x, s);
+  if (v.n_r1 > 0) {
+    const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
+    const int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
+    if (d->k == 2)
+      dev::fam_tensor_apply<3, 2, T, TM><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
+    else
+      dev::fam_tensor_apply<3, 1, T, TM><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
+    d->launches++;
+    export_add(d, l, t, s);
+    const i64 n = v.n_pad - v.n_r1;
+    if (n > 0) {
+      dev::cheb_range<T, RDV, WDV><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
+          v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2);
+      d->launches++;
+    }
+  } else {
+    k_apply(d, l, nullptr, v.n_cells, (const T*)x, t, s);
+    export_add(d, l, t, s);
+    k_cheb<T, true, RDV, WDV, false>(d, v, g, t, dv, x, c1, c2, s);
+  }
+}
+
 // Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
 // first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
 // x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows and ghosts keeps those entries fixed).
@@ -257,15 +293,14 @@ static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, boo
   if (m == 0) return;
   if (x_zero) {
     k_cheb<T, false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+  } else if (m == 1) {
+    cheb_step_fused<T, dev::TA_CHEB_00, false, false>(d, l, g, x, t, dv, 0.0, v.c2[0], s);
   } else {
-    apply_full(d, l, x, t, s);
-    if (m == 1) k_cheb<T, true, false, false, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
-    else k_cheb<T, true, false, true, false>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    cheb_step_fused<T, dev::TA_CHEB_01, false, true>(d, l, g, x, t, dv, 0.0, v.c2[0], s);
   }
   for (int j = 1; j < m; ++j) {
-    apply_full(d, l, x, t, s);
-    if (j == m - 1) k_cheb<T, true, true, false, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
-    else k_cheb<T, true, true, true, false>(d, v, g, t, dv, x, v.c1[j], v.c2[j], s);
+    if (j == m - 1) cheb_step_fused<T, dev::TA_CHEB_10, true, false>(d, l, g, x, t, dv, v.c1[j], v.c2[j], s);
+    else cheb_step_fused<T, dev::TA_CHEB_11, true, true>(d, l, g, x, t, dv, v.c1[j], v.c2[j], s);
   }
 }
 
@@ -513,10 +548,11 @@ static int chebyshev_degree(double kappa, double eps) {
 }
 
 // ---------------------------------------------------------------- creation
-DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::unique_ptr<Comm> comm,
+DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique_ptr<Comm> comm,
                                i64 n0_global) {
   auto* d = new DeviceHierarchy();
   try {
+    const DevicePlan plan = plan_device_order(Tp);   // device order of the level vectors (rewrites Tp)
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
@@ -571,6 +607,8 @@ DeviceHierarchy* device_create(const LocalTopo& Tp, const gmg_params& prm, std::
         v.xfer = d->upload(t.xfer);
       }
       v.leaf_cells = d->upload(t.leaf_cells);
+      v.n_r1 = plan.n_r1[l];
+      v.perm = d->upload(plan.perm[l]);
       if (!t.cell_coef.empty()) v.coef = d->upload(t.cell_coef);
       if (!t.fam_coef.empty()) v.fcoef = d->upload(t.fam_coef);
       if (!t.cell_elem.empty()) v.elem = d->upload(t.cell_elem);
@@ -860,17 +898,40 @@ static void need_single(const DeviceHierarchy* d) {
   GMG_REQUIRE(!d->comm, GMG_E_STATE, "single-operator entry points are defined for n_ranks == 1");
 }
 
+// The single-operator entry points take level vectors in the rank-local level
+// order (= global order for one rank) and permute to the device order
+// (plan.hpp) at the boundary, through the W / Y work buffers.
+static void to_dev(DeviceHierarchy* d, int l, const double* src, double* dst, cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  CK(cudaMemsetAsync(dst, 0, v.n_pad * sizeof(double), s));
+  if (v.n) {
+    dev::permute_in<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.perm, src, dst);
+    d->launches++;
+  }
+}
+static void from_dev(DeviceHierarchy* d, int l, const double* src, double* dst, cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  if (v.n) {
+    dev::permute_out<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.perm, src, dst);
+    d->launches++;
+  }
+}
+
 void device_level_apply(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
   need_single(d);
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
-  if (v.n) CK(cudaMemsetAsync(y, 0, v.n * sizeof(double), s));
-  k_apply(d, l, nullptr, v.n_cells, x, y, s);
+  double *xp = d->W + v.off, *yp = d->Y + v.off;
+  to_dev(d, l, x, xp, s);
+  CK(cudaMemsetAsync(yp, 0, v.n_pad * sizeof(double), s));
+  k_apply(d, l, nullptr, v.n_cells, (const double*)xp, yp, s);
+  from_dev(d, l, yp, y, s);
   CK(cudaPeekAtLastError());
 }
 
 void device_level_apply_kernel(DeviceHierarchy* d, int l, const double* x, double* y, void* stream) {
-  // rank-local kernel only (vectors of the local length n_owned + n_ghost), no exchange
+  // rank-local kernel only (vectors of the local length n_owned + n_ghost in the
+  // device order), no exchange
   DevLevel& v = d->lv[l];
   k_apply(d, l, nullptr, v.n_cells, x, y, (cudaStream_t)stream);
   CK(cudaPeekAtLastError());
@@ -884,13 +945,23 @@ void device_level_apply_kernel_f32(DeviceHierarchy* d, int l, const float* x, fl
 
 void device_restrict(DeviceHierarchy* d, int l, const double* r, double* dc, void* stream) {
   need_single(d);
-  k_restrict<dev::RES_PLAIN, double>(d, l, nullptr, d->lv[l].n_fam, r, nullptr, dc, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  double *rp = d->W + d->lv[l].off, *cp = d->Y + d->lv[l - 1].off;
+  to_dev(d, l, r, rp, s);
+  to_dev(d, l - 1, dc, cp, s);
+  k_restrict<dev::RES_PLAIN, double>(d, l, nullptr, d->lv[l].n_fam, rp, nullptr, cp, s);
+  from_dev(d, l - 1, cp, dc, s);
   CK(cudaPeekAtLastError());
 }
 
 void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, void* stream) {
   need_single(d);
-  k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, xc, xf, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  double *cp = d->W + d->lv[l - 1].off, *fp = d->Y + d->lv[l].off;
+  to_dev(d, l - 1, xc, cp, s);
+  to_dev(d, l, xf, fp, s);
+  k_prolongate<dev::XFER_ADD>(d, l, nullptr, d->lv[l].n_fam, (const double*)cp, fp, s);
+  from_dev(d, l, fp, xf, s);
   CK(cudaPeekAtLastError());
 }
 
@@ -912,13 +983,13 @@ void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, 
   cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   GMG_REQUIRE(l >= 1, GMG_E_INVALID_ARG, "no smoother on level 0");
-  // padded internal copies (the vector kernels stream the padded segment)
   double* gg = d->W + v.off;
   double* xx = d->Y + v.off;
-  CK(cudaMemcpyAsync(gg, g, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (!x_zero) CK(cudaMemcpyAsync(xx, x, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  smooth(d, l, gg, xx, d->T + v.off, d->DV + v.off, x_zero != 0, s);
-  CK(cudaMemcpyAsync(x, xx, v.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  to_dev(d, l, g, gg, s);
+  if (x_zero) CK(cudaMemsetAsync(xx, 0, v.n_pad * sizeof(double), s));
+  else to_dev(d, l, x, xx, s);
+  smooth(d, l, (const double*)gg, xx, d->T + v.off, d->DV + v.off, x_zero != 0, s);
+  from_dev(d, l, xx, x, s);
   CK(cudaMemsetAsync(gg, 0, v.n_pad * sizeof(double), s));
   CK(cudaMemsetAsync(xx, 0, v.n_pad * sizeof(double), s));
   CK(cudaPeekAtLastError());
@@ -926,10 +997,13 @@ void device_level_smooth(DeviceHierarchy* d, int l, const double* g, double* x, 
 
 void device_level_diagonal(DeviceHierarchy* d, int l, double* diag, void* stream) {
   need_single(d);
+  cudaStream_t s = (cudaStream_t)stream;
   DevLevel& v = d->lv[l];
   if (v.n == 0) return;
-  dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v.n, v.cls, v.Dinv, diag);
+  double* yp = d->Y + v.off;
+  dev::recip_s<<<(int)((v.n + 255) / 256), 256, 0, s>>>(v.n, v.cls, v.Dinv, yp);
   d->launches++;
+  from_dev(d, l, yp, diag, s);
   CK(cudaPeekAtLastError());
 }
 

@@ -9,8 +9,9 @@ namespace gmg {
 struct DeviceHierarchy;
 struct Comm;
 
+// T is rewritten in the device order (plan.hpp).
 // comm: nullptr for a single rank; n0_global: number of level-0 DoFs (all owned by rank 0)
-DeviceHierarchy* device_create(const LocalTopo& T, const gmg_params& prm, std::unique_ptr<Comm> comm,
+DeviceHierarchy* device_create(LocalTopo& T, const gmg_params& prm, std::unique_ptr<Comm> comm,
                                i64 n0_global);
 void device_destroy(DeviceHierarchy* d);
 

@@ -286,10 +286,20 @@ template <> struct PatchLayout<2, float> {
   static constexpr int ax = 5, ay = 1, az = 25, bx = 1, by = 25, bz = 5, size = 125;
 };
 
-template <int D, int K, typename T>
+// Epilogue modes of fam_tensor_apply: TA_APPLY y += K x (patch-interior rows
+// stored, others reduced); TA_CHEB_* in addition finish the Chebyshev-Jacobi
+// step on the interior rows of R1 (plan.hpp: only this family
+// touches them): dv = c1 dv + c2 D^-1 (g - K x), x += dv, with x_j taken from
+// the gather; those rows never reach y.  Suffix: READ_DV / WRITE_DV.
+enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4 };
+
+template <int D, int K, typename T, int TM = TA_APPLY>
 __global__ void __launch_bounds__(32 * TENSOR_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
-                 const T* __restrict__ x, T* __restrict__ y) {
+                 const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
+                 const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
+                 double c1_ = 0, double c2_ = 0) {
+  constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10, WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11;
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
   using LY = PatchLayout<K, T>;
   constexpr int NS = D == 3 && LY::size > NP ? LY::size : NP;
@@ -302,6 +312,8 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   T out[NP1];
   int ob = 0, os = 0;   // output line: base and stride in the patch
   int gi[NP1];           // 3D: the z-line DoFs of this lane, reused by the scatter
+  T ukeep[NP1];          // 3D: the gathered x values (x_j of the fused Chebyshev rows)
+  T pg[NP1 - 2], pd[NP1 - 2], pv[NP1 - 2];   // 3D fused modes: g, D^-1, dv of the interior rows
   if constexpr (D == 3) {
     constexpr int S2 = NP1 * NP1;
     if (lane < NL) {     // z lines: lane = (px, py), gathered straight into registers
@@ -310,6 +322,22 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       T u[NP1];
 #pragma unroll
       for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
+      if (TM != TA_APPLY) {   // requested with the gather: one memory round trip for the epilogue too
+        const int px = lane % NP1, py = lane / NP1;
+        const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
+#pragma unroll
+        for (int z = 1; z < 2 * K; ++z) {
+          const int i = gi[z];
+          pg[z - 1] = pd[z - 1] = pv[z - 1] = T(0);
+          if (inner && i >= 0 && i < n_r1) {
+            pg[z - 1] = __ldg(g + i);
+            pd[z - 1] = __ldg(Dinv + i);
+            if (RDV) pv[z - 1] = dv[i];
+          }
+        }
+      }
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         T t1 = 0, t2 = 0;
@@ -436,8 +464,17 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
         const int i = gi[z];
         if (i < 0) continue;
         const T v = s0[w][z * S2 + lane];
-        if (inner && z > 0 && z < 2 * K) y[i] = v;      // only this family touches the node
-        else atomicAdd(y + i, v);
+        if (TM != TA_APPLY && inner && z > 0 && z < 2 * K && i < n_r1) {
+          // complete row of an R1 node: Chebyshev step right here
+          T dd = (T)c2_ * pd[z - 1] * (pg[z - 1] - v);
+          if (RDV) dd = fma((T)c1_, pv[z - 1], dd);
+          if (WDV) dv[i] = dd;
+          xw[i] = ukeep[z] + dd;
+        } else if (inner && z > 0 && z < 2 * K) {
+          y[i] = v;                                      // only this family touches the node
+        } else {
+          atomicAdd(y + i, v);
+        }
       }
     }
   } else if (lane < NL) {
@@ -575,6 +612,37 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
   }
   if (WRITE_DV) dv[i] = V2{dx, dy};
   x[i] = V2{X.x + dx, X.y + dy};
+}
+
+// The Chebyshev step on [a, n) only (the rows not finished by the fused apply):
+// scalar form of cheb_step<T, READ_T = 1, ..., X_ZERO = 0>.
+template <typename T, bool READ_DV, bool WRITE_DV>
+__global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __restrict__ g,
+                                                     const T* __restrict__ Dinv, T* __restrict__ t,
+                                                     T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_) {
+  const long i = a + (long)blockIdx.x * VEC_NT + threadIdx.x;
+  if (i >= n) return;
+  const T G = g[i], Tv = t[i], Di = Dinv[i];
+  T V = 0;
+  if (READ_DV) V = dv[i];
+  const T X = x[i];
+  t[i] = Tv - Tv;                       // data-dependent reset (see cheb_step)
+  T dd = (T)c2_ * Di * (G - Tv);
+  if (READ_DV) dd = fma((T)c1_, V, dd);
+  if (WRITE_DV) dv[i] = dd;
+  x[i] = X + dd;
+}
+
+// dst[perm[i]] = src[i] (level order -> device order, plan.hpp) and the inverse
+__global__ void permute_in(long n, const int* __restrict__ perm, const double* __restrict__ src,
+                           double* __restrict__ dst) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[perm[i]] = src[i];
+}
+__global__ void permute_out(long n, const int* __restrict__ perm, const double* __restrict__ src,
+                            double* __restrict__ dst) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
 }
 
 // ------------------------------------------------------------- transfers

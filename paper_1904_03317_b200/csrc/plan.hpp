@@ -1,0 +1,32 @@
+// Device order of the rank-local level vectors (host, integer).
+//
+// On levels with families the owned DoFs are renumbered on the device as
+//     [ R1 | rest of the owned DoFs | ghosts ]
+//   R1  the interior nodes of the family patches ((2k+1)^d patch positions with
+//       every coordinate in 1 .. 2k-1) that no other rank needs: only their own
+//       family touches them, so the level-operator kernel holds their complete
+//       row and finishes the Chebyshev step on them in its epilogue
+//       (kernels.cuh, fam_tensor_apply<..., CHEB>); grouped by family (SFC
+//       order), z-major inside the family, so each z plane of a family is one
+//       contiguous run;
+//   the rest keep their (owner, Morton) order and are finished by the streaming
+//   Chebyshev pass over [n_r1, n_pad).
+// Level 0 keeps the identity order.  The renumbering is internal to the device
+// layer: integer exports use the global order of the paper's numbering
+// and the single-operator entry points permute at the boundary.
+#pragma once
+
+#include "forest.hpp"
+
+namespace gmg {
+
+struct DevicePlan {
+  std::vector<std::vector<i32>> perm;    // per level: rank-local index -> device index
+  std::vector<i64> n_r1;                 // per level: R1 = device indices [0, n_r1)
+};
+
+// Computes the device order from T's tables and rewrites T in place (every
+// local DoF index of every table is mapped through perm).
+DevicePlan plan_device_order(LocalTopo& T);
+
+}  // namespace gmg
