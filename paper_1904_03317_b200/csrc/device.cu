@@ -239,13 +239,13 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
   d->launches++;
 }
 
-template <typename T, bool RT, bool RDV, bool WDV, bool XZ>
+template <typename T, bool RT, bool RDV, bool WDV, bool XZ, bool DVX = false>
 static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* x, double c1, double c2,
                    cudaStream_t s) {
   if (v.n_pad == 0) return;
   using V2 = typename dev::Vec2<T>::type;
   // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
-  dev::cheb_step<T, RT, RDV, WDV, XZ><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
+  dev::cheb_step<T, RT, RDV, WDV, XZ, DVX><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
       (const V2*)g, (const V2*)MG<T>::Dinv(v), (V2*)t, (V2*)dv, (V2*)x, c1, c2);
   d->launches++;
 }
@@ -254,7 +254,7 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
 // rows of R1 finished inside the operator kernel (fam_tensor_apply<TM>), the rest
 // by the streaming pass over [n_r1, n_pad).  Falls back to operator + full-level
 // streaming step where the level has no R1 (2D, coefficient levels, level 0).
-template <typename T, int TM, bool RDV, bool WDV>
+template <typename T, int TM, bool RDV, bool WDV, bool DVX = false>
 static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, double c1, double c2,
                             cudaStream_t s) {
   DevLevel& v = d->lv[l];
@@ -272,14 +272,14 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     export_add(d, l, t, s);
     const i64 n = v.n_pad - v.n_r1;
     if (n > 0) {
-      dev::cheb_range<T, RDV, WDV><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
+      dev::cheb_range<T, RDV, WDV, DVX><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
           v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2);
       d->launches++;
     }
   } else {
     k_apply(d, l, nullptr, v.n_cells, (const T*)x, t, s);
     export_add(d, l, t, s);
-    k_cheb<T, true, RDV, WDV, false>(d, v, g, t, dv, x, c1, c2, s);
+    k_cheb<T, true, RDV, WDV, false, DVX>(d, v, g, t, dv, x, c1, c2, s);
   }
 }
 
@@ -291,14 +291,20 @@ static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, boo
   DevLevel& v = d->lv[l];
   const int m = (int)v.c1.size();     // degree d->m on levels >= 1, the coarse degree on level 0
   if (m == 0) return;
-  if (x_zero) {
+  int j0 = 1;
+  if (x_zero && m > 1) {
+    // x_1 = dv_0 = c2_0 D^-1 g: only x is stored, the next step reads dv_0 from x
+    k_cheb<T, false, false, false, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    cheb_step_fused<T, dev::TA_CHEB_X1, true, true, true>(d, l, g, x, t, dv, v.c1[1], v.c2[1], s);
+    j0 = 2;
+  } else if (x_zero) {
     k_cheb<T, false, false, true, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
   } else if (m == 1) {
     cheb_step_fused<T, dev::TA_CHEB_00, false, false>(d, l, g, x, t, dv, 0.0, v.c2[0], s);
   } else {
     cheb_step_fused<T, dev::TA_CHEB_01, false, true>(d, l, g, x, t, dv, 0.0, v.c2[0], s);
   }
-  for (int j = 1; j < m; ++j) {
+  for (int j = j0; j < m; ++j) {
     if (j == m - 1) cheb_step_fused<T, dev::TA_CHEB_10, true, false>(d, l, g, x, t, dv, v.c1[j], v.c2[j], s);
     else cheb_step_fused<T, dev::TA_CHEB_11, true, true>(d, l, g, x, t, dv, v.c1[j], v.c2[j], s);
   }

@@ -291,7 +291,9 @@ template <> struct PatchLayout<2, float> {
 // step on the interior rows of R1 (plan.hpp: only this family
 // touches them): dv = c1 dv + c2 D^-1 (g - K x), x += dv, with x_j taken from
 // the gather; those rows never reach y.  Suffix: READ_DV / WRITE_DV.
-enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4 };
+// TA_CHEB_X1: the step after the first one from x = 0, where dv_0 = x_1 is not
+// stored and is read from x (from the gather's registers in the epilogue).
+enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5 };
 
 template <int D, int K, typename T, int TM = TA_APPLY>
 __global__ void __launch_bounds__(32 * TENSOR_WARPS)
@@ -299,7 +301,9 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
                  double c1_ = 0, double c2_ = 0) {
-  constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10, WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11;
+  constexpr bool DVX = TM == TA_CHEB_X1;
+  constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
+  constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX;
   constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
   using LY = PatchLayout<K, T>;
   constexpr int NS = D == 3 && LY::size > NP ? LY::size : NP;
@@ -334,7 +338,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
           if (inner && i >= 0 && i < n_r1) {
             pg[z - 1] = __ldg(g + i);
             pd[z - 1] = __ldg(Dinv + i);
-            if (RDV) pv[z - 1] = dv[i];
+            if (RDV && !DVX) pv[z - 1] = dv[i];
           }
         }
       }
@@ -467,7 +471,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
         if (TM != TA_APPLY && inner && z > 0 && z < 2 * K && i < n_r1) {
           // complete row of an R1 node: Chebyshev step right here
           T dd = (T)c2_ * pd[z - 1] * (pg[z - 1] - v);
-          if (RDV) dd = fma((T)c1_, pv[z - 1], dd);
+          if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z - 1], dd);
           if (WDV) dv[i] = dd;
           xw[i] = ukeep[z] + dd;
         } else if (inner && z > 0 && z < 2 * K) {
@@ -586,7 +590,7 @@ template <typename T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
-template <typename S, bool READ_T, bool READ_DV, bool WRITE_DV, bool X_ZERO>
+template <typename S, bool READ_T, bool READ_DV, bool WRITE_DV, bool X_ZERO, bool DV_IS_X = false>
 __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type* __restrict__ g,
                                                     const typename Vec2<S>::type* __restrict__ Dinv,
                                                     typename Vec2<S>::type* __restrict__ t,
@@ -599,8 +603,8 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
   V2 T = {S(0), S(0)}, V = T, X = T;
   if (READ_T) T = t[i];
   const V2 Di = Dinv[i];
-  if (READ_DV) V = dv[i];
   if (!X_ZERO) X = x[i];
+  if (READ_DV) V = DV_IS_X ? X : dv[i];
   // reset of the accumulator: the stored zero is made data-dependent on the loaded
   // value so that the store cannot be issued while the load of the same address is
   // in flight (that ordering costs 2.25x on B200: tools/microbench8.cu)
@@ -616,16 +620,16 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
 
 // The Chebyshev step on [a, n) only (the rows not finished by the fused apply):
 // scalar form of cheb_step<T, READ_T = 1, ..., X_ZERO = 0>.
-template <typename T, bool READ_DV, bool WRITE_DV>
+template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false>
 __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __restrict__ g,
                                                      const T* __restrict__ Dinv, T* __restrict__ t,
                                                      T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_) {
   const long i = a + (long)blockIdx.x * VEC_NT + threadIdx.x;
   if (i >= n) return;
   const T G = g[i], Tv = t[i], Di = Dinv[i];
-  T V = 0;
-  if (READ_DV) V = dv[i];
   const T X = x[i];
+  T V = 0;
+  if (READ_DV) V = DV_IS_X ? X : dv[i];      // DV_IS_X: dv_0 = x_1 after the first step from 0
   t[i] = Tv - Tv;                       // data-dependent reset (see cheb_step)
   T dd = (T)c2_ * Di * (G - Tv);
   if (READ_DV) dd = fma((T)c1_, V, dd);
