@@ -71,8 +71,8 @@ struct DeviceHierarchy {
   double *cx = nullptr, *cr = nullptr, *cp = nullptr, *cq = nullptr, *cz = nullptr;
   double *sbuf = nullptr, *rbuf = nullptr;
   unsigned char* lam_mg = nullptr;
-  long long* mg_to_leaf = nullptr;
-  long long* leaf_to_mg = nullptr;
+  int* mg_to_leaf = nullptr;        // int32: the MG layout stays below 2^31 entries (checked)
+  int* leaf_to_mg = nullptr;
   double* partial = nullptr;
   int nred = 0;
   double* scal = nullptr;       // device scalars
@@ -642,13 +642,14 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     d->rbuf = d->alloc<double>(xmax);
     // lambda mask and leaf <-> MG maps (owned leaf DoFs of this rank)
     std::vector<unsigned char> lam(N, 0);
-    std::vector<long long> m2l(N, -1), l2m(Tp.n_leaf_owned);
+    GMG_REQUIRE(N < ((i64)1 << 31), GMG_E_INVALID_ARG, "MG layout exceeds 2^31 entries on one rank");
+    std::vector<int> m2l(N, -1), l2m(Tp.n_leaf_owned);
     for (int l = 0; l <= Tp.L; ++l)
       for (i64 i = 0; i < Tp.lv[l].n_local(); ++i) lam[d->lv[l].off + i] = Tp.lv[l].lam[i];
     for (i64 g = 0; g < Tp.n_leaf_owned; ++g) {
       i64 m = d->lv[Tp.leaf_level[g]].off + Tp.leaf_local[g];
-      l2m[g] = m;
-      m2l[m] = g;
+      l2m[g] = (int)m;
+      m2l[m] = (int)g;
     }
     d->n_leaf = Tp.n_leaf_owned;
     d->lam_mg = d->upload(lam);

@@ -907,18 +907,18 @@ __global__ void cast_vec(long n, const double* __restrict__ in, T* __restrict__ 
 
 // MG layout <- leaf order: out[m] = (inv[m] >= 0 ? in[inv[m]] : 0)
 template <typename T>
-__global__ void gather_to_mg(long n, const long long* __restrict__ inv, const double* __restrict__ in,
+__global__ void gather_to_mg(long n, const int* __restrict__ inv, const double* __restrict__ in,
                              T* __restrict__ out) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long stride = (long)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    long long s = inv[i];
+    const int s = inv[i];
     out[i] = s >= 0 ? (T)in[s] : T(0);
   }
 }
 // leaf order <- MG layout
 template <typename T>
-__global__ void gather_from_mg(long n, const long long* __restrict__ perm, const T* __restrict__ in,
+__global__ void gather_from_mg(long n, const int* __restrict__ perm, const T* __restrict__ in,
                                double* __restrict__ out) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long stride = (long)gridDim.x * blockDim.x;
