@@ -361,3 +361,58 @@ def test_more_ranks_than_leaves_local_ranks():
     for fo, no, xl in res:
         xv[canon[fo:fo + no]] = xl
     assert rel(xv, ref) < 1e-13
+
+
+# ---------------------------------------------------------------- random adaptive forests
+# Seeded random refinement (a few leaves per pass, closed to 2:1 balance after each
+# pass) in 2D/3D, Q1/Q2, one or two trees: every level operator, the V-cycle and
+# the CG count against the oracle, fp64 and mixed precision.
+RANDOM = [(2, 1, 11), (2, 2, 12), (3, 1, 13), (3, 2, 14), (3, 2, 15), (2, 2, 16)]
+
+
+def _random_forest(d, seed, trees):
+    rng = np.random.RandomState(seed)
+    f = F.coarse_forest(d, trees)
+    f = F.refine(f, np.ones(f.n_leaves, dtype=bool))
+    for _ in range(6):
+        m = np.zeros(f.n_leaves, dtype=bool)
+        m[rng.randint(0, f.n_leaves, size=1 + f.n_leaves // 8)] = True
+        f = F.close(F.refine(f, m))
+        if f.n_leaves > (2500 if d == 2 else 1500):
+            break
+    return f
+
+
+@pytest.mark.parametrize("d,k,seed", RANDOM, ids=[f"{d}d-k{k}-s{s}" for d, k, s in RANDOM])
+def test_random_forest_vcycle_cg(d, k, seed):
+    trees = [(0,) * d, (1,) + (0,) * (d - 1)] if seed % 2 == 0 else [(0,) * d]
+    of = _random_forest(d, seed, trees)
+    tree = of.tree_index()
+    tpos = of.gc >> of.level[:, None]
+    loc = of.gc - (tpos << of.level[:, None])
+    lf = G.gmg_forest_create(d, [tuple(t) for t in of.trees], tree.astype(np.int32), of.level.astype(np.int8),
+                             F.morton(loc, 32).astype(np.uint64))
+    oh = mg.build(of, k)
+    n = oh.leaf.n_free
+    b = uniform_pm1(n, STREAM_PROBE, offset=seed)
+    for mixed in (False, True):
+        h = G.gmg_setup(lf, G.gmg_partition(lf, 1), k=k, mixed=mixed)
+        if not mixed:
+            for l, lev in enumerate(oh.levels):
+                if lev.space.n == 0:
+                    continue
+                xv = uniform_pm1(lev.space.n, STREAM_PROBE, offset=100 * l)
+                y = torch.zeros(lev.space.n, device="cuda", dtype=torch.float64)
+                h.level_apply(l, dev(xv), y)
+                assert rel(y.cpu().numpy(), lev.K @ xv) < OP_TOL, l
+        for l in range(1, oh.L + 1):
+            h.set_eigen(l, oh.levels[l].lam)
+        x = torch.zeros(n, device="cuda", dtype=torch.float64)
+        h.vcycle(dev(b), x)
+        assert rel(x.cpu().numpy(), mg.vcycle(oh, b)) < (MIXED_VC_TOL if mixed else VC_TOL)
+        bb = torch.zeros(n, device="cuda", dtype=torch.float64)
+        h.rhs_constant(1.0, bb)
+        xs = torch.zeros(n, device="cuda", dtype=torch.float64)
+        it, relres, _ = h.solve_cg(bb, xs, rtol=1e-8)
+        _, it_ref, _, _ = mg.pcg(oh, oh.b_leaf, rtol=1e-8)
+        assert abs(it - it_ref) <= 1 and relres <= 1e-8, (mixed, it, it_ref)
