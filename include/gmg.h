@@ -244,6 +244,10 @@ typedef struct {
   int64_t mg_vector_len;     /* sum of the level vector lengths */
 } gmg_info;
 gmg_status gmg_hierarchy_info(const gmg_hierarchy *h, gmg_info *out);
+/* Leaf vectors of this rank: n_owned free leaf DoFs, the global
+ * indices [first, first + n_owned) of the global leaf order, n_global in total.
+ * Any pointer may be NULL. */
+gmg_status gmg_leaf_layout(const gmg_hierarchy *h, int64_t *n_owned, int64_t *n_global, int64_t *first);
 
 /* Level DoFs of `level` in global order: Morton key, class (0 = S, 1 = E),
  * owner, canonical index (position in the Morton order = the p = 1 numbering). */

@@ -251,6 +251,15 @@ gmg_status gmg_hierarchy_destroy(gmg_hierarchy* h) {
   return guard([&] { delete h; });
 }
 
+gmg_status gmg_leaf_layout(const gmg_hierarchy* h, int64_t* n_owned, int64_t* n_global, int64_t* first) {
+  return guard([&] {
+    NEED(h);
+    if (n_owned) *n_owned = h->local.n_leaf_owned;
+    if (n_global) *n_global = h->local.n_leaf_global;
+    if (first) *first = h->local.leaf_first;
+  });
+}
+
 gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
   return guard([&] {
     NEED(h);
