@@ -36,7 +36,7 @@ struct DevLevel {
   unsigned char* cls = nullptr;     // bit0 = E
   double* Dinv = nullptr;           // n_pad entries, 0 on E rows, ghosts and padding
   float* Dinv32 = nullptr;          // the same in fp32 (mixed-precision V-cycle)
-  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam] (cell-form family apply)
+  int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam], only for the cell-form family apply (fam_apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   i64 n_r1 = 0;                     // device order (plan.hpp): rows [0, n_r1) finished by the fused apply
   int* perm = nullptr;              // rank-local level index -> device index (API boundary)
@@ -81,7 +81,6 @@ struct DeviceHierarchy {
   double* coarse_inv = nullptr;
   int* coarse_idx = nullptr;
   bool use_graph = true;
-  bool xfer_warp = true;        // warp-per-family transfers (GMG_XFER=thread: thread per family)
   bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
@@ -603,14 +602,15 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       std::vector<unsigned char> cls(v.n);
       for (i64 i = 0; i < v.n; ++i) cls[i] = t.cls[i] == CLS_E ? 1 : 0;
       v.cls = d->upload(cls);
-      {
-        // patch table AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
+      v.xfer = d->upload(t.xfer);
+      if (!d->tensor_apply || (!t.cell_coef.empty() && t.fam_coef.empty())) {
+        // cell-form family apply (config-4 level 2, or GMG_APPLY=cell): patch table
+        // AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
         const size_t np = t.n_fam ? t.fam_dofs.size() / (size_t)t.n_fam : 0;
         std::vector<int> fs(t.fam_dofs.size());
         for (size_t f = 0; f < (size_t)t.n_fam; ++f)
           for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.fam_dofs[f * np + a];
         v.fam_dofs = d->upload(fs);
-        v.xfer = d->upload(t.xfer);
       }
       v.leaf_cells = d->upload(t.leaf_cells);
       v.n_r1 = plan.n_r1[l];
