@@ -101,3 +101,25 @@ def test_ghost_children_ratio_small_and_sublinear():
     # larger problem, same p: the ratio shrinks (surface / volume)
     _, r64_big = _eta_ratio(G.gmg_forest_sequence(2, "annulus", 12), 64)
     assert r64_big < r64
+
+
+def test_config3_partition_model_matches_survey_values():
+    """Exact first-child model on the full config-3 forest (5.3M leaves) against the
+    values SURVEY §8(c.3) lists (independent computation): eta at p = 1/2/4/8,
+    W = W_sync, one octant of level-10 cells per rank at p = 8."""
+    import json
+    import os
+    from gmg_inputs import config
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config_counts.json")))
+    c3 = gold["c3_partition"]
+    lf = G.gmg_forest_generate(G.recipe_from_config(config("c3")))
+    for p, eta in c3["eta"].items():
+        part = G.gmg_partition(lf, int(p))
+        m = part.model()
+        assert Fraction(*m["eta"]) == Fraction(*eta), p
+        assert m["N"] == gold["c3"]["N_l"]
+        if p in c3["W"]:
+            assert m["W"] == c3["W"][p] == m["W_sync"]
+        if p == "8":
+            t = part.tallies()
+            assert list(t[10]) == [c3["p8_level10_cells_per_rank"]] * 8
