@@ -365,8 +365,8 @@ def run_ours(args):
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic,
                             "traffic_source": traffic_src if traffic is not None else None,
-                            "kernel": "fam_tensor_apply<3,2,%s> (level operator), finest level"
-                                      % ("float" if mixed else "double"),
+                            "kernel": ("fam_tensor_apply<3,%d,%s>" if cfg["dim"] == 3 else "fam_tensor_apply2d<%d,%s>")
+                                      % (cfg["k"], "float" if mixed else "double") + " (level operator), finest level",
                             "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,
                             "share_of_step": share, "peak_source": peak_src},
                "cpu_baseline": cpu,

@@ -190,9 +190,20 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* 
   } else if (full && (v.coef == nullptr || v.fcoef != nullptr) && d->tensor_apply) {
     const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
     const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
-    int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
-    DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
-                                  (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y)));
+    if (d->dim == 2) {   // several families per warp (fam_tensor_apply2d)
+      const int fpw = 32 / (2 * d->k + 1), per_block = fpw * dev::TENSOR_WARPS;
+      const int grid = (int)((v.n_fam + per_block - 1) / per_block);
+      if (d->k == 2)
+        dev::fam_tensor_apply2d<2, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>((int)v.n_fam, v.xfer, np + nn,
+                                                                               v.fcoef, v.scale, x, y);
+      else
+        dev::fam_tensor_apply2d<1, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>((int)v.n_fam, v.xfer, np + nn,
+                                                                               v.fcoef, v.scale, x, y);
+    } else {
+      int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
+      DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+                                    (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y)));
+    }
   } else if (full) {                              // per-cell coefficients inside a family (config 4, level 2)
     DISPATCH_DK(d->dim, d->k, {
       constexpr int FPB = dev::FamCfg<D_, K_>::FPB;

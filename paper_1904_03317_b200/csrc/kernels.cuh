@@ -495,6 +495,67 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   }
 }
 
+// 2D form of fam_tensor_apply: a (2k+1)^2 patch has only 2k+1 lines, so one warp
+// packs FPW = 32 / (2k+1) families (6 for Q2, 10 for Q1) instead of leaving
+// 27 (29) lanes idle.  Lines along x first (gathered into registers), one
+// transposition through shared memory, lines along y; interior patch nodes
+// stored, the others reduced.
+template <int K, typename T>
+__global__ void __launch_bounds__(32 * TENSOR_WARPS)
+fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef,
+                   double scale_, const T* __restrict__ x, T* __restrict__ y) {
+  constexpr int NP1 = 2 * K + 1, NP = NP1 * NP1, FPW = 32 / NP1;
+  __shared__ T s0[TENSOR_WARPS][FPW][NP], s1[TENSOR_WARPS][FPW][NP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = lane / NP1, line = lane % NP1;
+  const long f = ((long)blockIdx.x * TENSOR_WARPS + w) * FPW + j;
+  const bool active = j < FPW && f < nfam;
+  const int* rp = xfer + (active ? f : 0) * (long)row;
+  const T scale = (T)(active && fcoef ? scale_ * __ldg(fcoef + f) : scale_);
+  if (active) {        // x lines: line = py, gathered straight into registers
+    const int b = line * NP1;
+    T u[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) {
+      const int gi = decode_dof(__ldg(rp + b + q));
+      u[q] = gi >= 0 ? __ldg(x + gi) : T(0);
+    }
+#pragma unroll
+    for (int xx = 0; xx < NP1; ++xx) {
+      T a = 0, bb = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Kt<K>(xx, q) != 0.0) a = fma((T)Kt<K>(xx, q), u[q], a);
+        if (Mt<K>(xx, q) != 0.0) bb = fma((T)Mt<K>(xx, q), u[q], bb);
+      }
+      s0[w][j][b + xx] = a;
+      s1[w][j][b + xx] = bb;
+    }
+  }
+  __syncwarp();
+  if (active) {        // y lines: line = px
+    T a[NP1], bb[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) {
+      a[q] = s0[w][j][line + q * NP1];
+      bb[q] = s1[w][j][line + q * NP1];
+    }
+#pragma unroll
+    for (int yy = 0; yy < NP1; ++yy) {
+      T o = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Mt<K>(yy, q) != 0.0) o = fma((T)Mt<K>(yy, q), a[q], o);
+        if (Kt<K>(yy, q) != 0.0) o = fma((T)Kt<K>(yy, q), bb[q], o);
+      }
+      const int i = decode_dof(__ldg(rp + line + yy * NP1));
+      if (i < 0) continue;
+      if (line > 0 && line < 2 * K && yy > 0 && yy < 2 * K) y[i] = scale * o;   // only this family
+      else atomicAdd(y + i, scale * o);
+    }
+  }
+}
+
 // cell_dofs is SoA: dof of local node b of cell c at cell_dofs[b * ldc + c]
 template <int D, int K, typename T>
 __global__ void __launch_bounds__(128) cell_apply(int n, const int* __restrict__ list,
