@@ -173,6 +173,11 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- primitives
+template <int K>
+static int tensor_grid(i64 n_fam) {
+  return (int)((n_fam + dev::TensorCfg<K>::FPB - 1) / dev::TensorCfg<K>::FPB);
+}
+
 // y += K_l x over a cell list (leaf cells) or, list == nullptr, over all local
 // cells.  Full levels >= 1 run family-blocked (y must be zero on entry:
 // patch-interior nodes are stored, not added); level 0 and cell lists run
@@ -200,9 +205,12 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* 
         dev::fam_tensor_apply2d<1, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>((int)v.n_fam, v.xfer, np + nn,
                                                                                v.fcoef, v.scale, x, y);
     } else {
-      int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
-      DISPATCH_DK(d->dim, d->k, (dev::fam_tensor_apply<D_, K_, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
-                                    (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y)));
+      if (d->k == 2)
+        dev::fam_tensor_apply<2, T><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
+            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y);
+      else
+        dev::fam_tensor_apply<1, T><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
+            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y);
     }
   } else if (full) {                              // per-cell coefficients inside a family (config 4, level 2)
     DISPATCH_DK(d->dim, d->k, {
@@ -271,12 +279,11 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
   import_ghosts(d, l, x, s);
   if (v.n_r1 > 0) {
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
-    const int grid = (int)((v.n_fam + dev::TENSOR_WARPS - 1) / dev::TENSOR_WARPS);
     if (d->k == 2)
-      dev::fam_tensor_apply<3, 2, T, TM><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+      dev::fam_tensor_apply<2, T, TM><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
           (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
     else
-      dev::fam_tensor_apply<3, 1, T, TM><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>(
+      dev::fam_tensor_apply<1, T, TM><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
           (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
     d->launches++;
     export_add(d, l, t, s);

@@ -269,21 +269,37 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
 
 constexpr int TENSOR_WARPS = 8;
 
-// Transposition layouts of fam_tensor_apply (3D): A holds the z-pass result for
-// the y pass, B the y-pass result for the x pass; index = cx x + cy y + cz z.
-// Chosen by exhaustive search so that every pass's shared-memory accesses (25
-// lanes; fp64 served per 16-lane half-warp over 16 bank pairs, fp32 in one pass
-// over 32 banks) take the minimum number of wavefronts (tools/smem_layouts.py).
+// fam_tensor_apply (3D) runs one block of TG_WARPS warps over FPB = 32 TG_WARPS
+// / (2k+1)^2 families (5 for Q2, 14 for Q1), one thread per 1-D line of a
+// patch: 125 of 128 lanes busy instead of 25 of 32 with a warp per family.
+constexpr int TG_WARPS = 4;
+
+// Transposition layouts (per family slot of the block): A holds the z-pass
+// result for the y pass, B the y-pass result for the x pass (slot stride sab),
+// N the x-pass result for the scatter along z lines (slot stride sn); index =
+// cx x + cy y + cz z.  Chosen by exhaustive search so that every pass's
+// shared-memory accesses (fp64 served per 16-lane half-warp over 16 bank pairs,
+// fp32 in one pass over 32 banks; warps straddle two families) take the minimum
+// number of wavefronts (tools/smem_layouts.py): A and B reach the ideal (2
+// wavefronts per fp64 access of a warp, 1 per fp32 access); N cannot on every
+// pass (the x-pass and z-pass line numberings swap the roles of y), it takes 25 %
+// (fp64) / 38 % (fp32) more than the ideal on its two passes.
 template <int K, typename T> struct PatchLayout {   // K = 1: natural order (27 nodes)
   static constexpr int ax = 1, ay = 2 * K + 1, az = (2 * K + 1) * (2 * K + 1);
   static constexpr int bx = 1, by = 2 * K + 1, bz = (2 * K + 1) * (2 * K + 1);
-  static constexpr int size = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);
+  static constexpr int nx = 1, ny = 2 * K + 1, nz = (2 * K + 1) * (2 * K + 1);
+  static constexpr int sab = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), sn = sab;
 };
-template <> struct PatchLayout<2, double> {
-  static constexpr int ax = 5, ay = 9, az = 25, bx = 1, by = 33, bz = 5, size = 157;
+template <> struct PatchLayout<2, double> {   // wavefronts per 5 families: A 40+40, B 40+40, N 40+60
+  static constexpr int ax = 1, ay = 5, az = 37, bx = 1, by = 33, bz = 5, sab = 185;
+  static constexpr int nx = 1, ny = 5, nz = 25, sn = 125;
 };
-template <> struct PatchLayout<2, float> {
-  static constexpr int ax = 5, ay = 1, az = 25, bx = 1, by = 25, bz = 5, size = 125;
+template <> struct PatchLayout<2, float> {    // A 20+20, B 20+20, N 35+20
+  static constexpr int ax = 1, ay = 5, az = 37, bx = 1, by = 33, bz = 5, sab = 185;
+  static constexpr int nx = 1, ny = 5, nz = 39, sn = 185;
+};
+template <int K> struct TensorCfg {
+  static constexpr int NL = (2 * K + 1) * (2 * K + 1), FPB = 32 * TG_WARPS / NL;
 };
 
 // Epilogue modes of fam_tensor_apply: TA_APPLY y += K x (patch-interior rows
@@ -295,8 +311,8 @@ template <> struct PatchLayout<2, float> {
 // stored and is read from x (from the gather's registers in the epilogue).
 enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5 };
 
-template <int D, int K, typename T, int TM = TA_APPLY>
-__global__ void __launch_bounds__(32 * TENSOR_WARPS)
+template <int K, typename T, int TM = TA_APPLY>
+__global__ void __launch_bounds__(32 * TG_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
@@ -304,193 +320,134 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   constexpr bool DVX = TM == TA_CHEB_X1;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX;
-  constexpr int NP1 = 2 * K + 1, NP = Shape<D, K>::NP, NL = NP / NP1;
+  constexpr int NP1 = 2 * K + 1, S2 = NP1 * NP1, NL = TensorCfg<K>::NL, FPB = TensorCfg<K>::FPB;
   using LY = PatchLayout<K, T>;
-  constexpr int NS = D == 3 && LY::size > NP ? LY::size : NP;
-  __shared__ T s0[TENSOR_WARPS][NS], s1[TENSOR_WARPS][NS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * TENSOR_WARPS + w;
-  if (f >= nfam) return;
-  const int* rp = xfer + (long)f * row;
-  const T scale = (T)(fcoef ? scale_ * __ldg(fcoef + f) : scale_);   // config 4: one coefficient per family (levels >= 3)
-  T out[NP1];
-  int ob = 0, os = 0;   // output line: base and stride in the patch
-  int gi[NP1];           // 3D: the z-line DoFs of this lane, reused by the scatter
-  T ukeep[NP1];          // 3D: the gathered x values (x_j of the fused Chebyshev rows)
-  T pg[NP1 - 2], pd[NP1 - 2], pv[NP1 - 2];   // 3D fused modes: g, D^-1, dv of the interior rows
-  if constexpr (D == 3) {
-    constexpr int S2 = NP1 * NP1;
-    if (lane < NL) {     // z lines: lane = (px, py), gathered straight into registers
+  constexpr int NS = FPB * (LY::sab > LY::sn ? LY::sab : LY::sn);
+  __shared__ T s0[NS], s1[NS];
+  const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
+  const long f = (long)blockIdx.x * FPB + slot;
+  const bool act = slot < FPB && f < nfam;
+  const int* rp = xfer + (act ? f : 0) * (long)row;
+  T* const a0 = s0 + (act ? slot : 0) * LY::sab;
+  T* const a1 = s1 + (act ? slot : 0) * LY::sab;
+  T* const n0 = s0 + (act ? slot : 0) * LY::sn;
+  const T scale = (T)(act && fcoef ? scale_ * __ldg(fcoef + f) : scale_);   // config 4: one coefficient per family (levels >= 3)
+  int gi[NP1];           // the z-line DoFs of this lane, reused by the scatter
+  T ukeep[NP1];          // the gathered x values (x_j of the fused Chebyshev rows)
+  T pg[NP1 - 2], pd[NP1 - 2], pv[NP1 - 2];   // fused modes: g, D^-1, dv of the interior rows
+  if (act) {             // z lines: lane = (px, py), gathered straight into registers
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
-      T u[NP1];
+    for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
+    T u[NP1];
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+    for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
-      if (TM != TA_APPLY) {   // requested with the gather: one memory round trip for the epilogue too
-        const int px = lane % NP1, py = lane / NP1;
-        const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
-#pragma unroll
-        for (int z = 1; z < 2 * K; ++z) {
-          const int i = gi[z];
-          pg[z - 1] = pd[z - 1] = pv[z - 1] = T(0);
-          if (inner && i >= 0 && i < n_r1) {
-            pg[z - 1] = __ldg(g + i);
-            pd[z - 1] = __ldg(Dinv + i);
-            if (RDV && !DVX) pv[z - 1] = dv[i];
-          }
-        }
-      }
-#pragma unroll
-      for (int z = 0; z < NP1; ++z) {
-        T t1 = 0, t2 = 0;
-#pragma unroll
-        for (int q = 0; q < NP1; ++q) {
-          if (Mt<K>(z, q) != 0.0) t1 = fma((T)Mt<K>(z, q), u[q], t1);
-          if (Kt<K>(z, q) != 0.0) t2 = fma((T)Kt<K>(z, q), u[q], t2);
-        }
-        // transposition layout A (PatchLayout): minimum wavefronts for this store
-        // (lanes over x, y) and for the y-pass load (lanes over x, z)
-        const int ia = LY::ax * (lane % NP1) + LY::ay * (lane / NP1) + LY::az * z;
-        s0[w][ia] = t1;
-        s1[w][ia] = t2;
-      }
-    }
-    __syncwarp();
-    if (lane < NL) {     // y lines: lane = (px, pz)
-      const int px = lane % NP1, pz = lane / NP1;
-      const int ba = LY::ax * px + LY::az * pz, bb_ = LY::bx * px + LY::bz * pz;
-      T t1[NP1], t2[NP1];
-#pragma unroll
-      for (int q = 0; q < NP1; ++q) {
-        t1[q] = s0[w][ba + LY::ay * q];
-        t2[q] = s1[w][ba + LY::ay * q];
-      }
-      __syncwarp((1u << NL) - 1);   // layout B differs from A: all loads before any store
-#pragma unroll
-      for (int yy = 0; yy < NP1; ++yy) {
-        T a = 0, bb = 0;
-#pragma unroll
-        for (int q = 0; q < NP1; ++q) {
-          if (Mt<K>(yy, q) != 0.0) {
-            a = fma((T)Mt<K>(yy, q), t1[q], a);
-            bb = fma((T)Mt<K>(yy, q), t2[q], bb);
-          }
-          if (Kt<K>(yy, q) != 0.0) bb = fma((T)Kt<K>(yy, q), t1[q], bb);
-        }
-        // layout B (PatchLayout): minimum wavefronts for this store (lanes over x, z)
-        // and for the x-pass load (lanes over y, z)
-        s0[w][bb_ + LY::by * yy] = a;
-        s1[w][bb_ + LY::by * yy] = bb;
-      }
-    }
-    __syncwarp();
-    if (lane < NL) {     // x lines: lane = (py, pz)
-      ob = lane * NP1;
-      os = 1;
-      const int bx = LY::by * (lane % NP1) + LY::bz * (lane / NP1);
-      T a[NP1], bb[NP1];
-#pragma unroll
-      for (int q = 0; q < NP1; ++q) {
-        a[q] = s0[w][bx + LY::bx * q];
-        bb[q] = s1[w][bx + LY::bx * q];
-      }
-#pragma unroll
-      for (int xx = 0; xx < NP1; ++xx) {
-        T o = 0;
-#pragma unroll
-        for (int q = 0; q < NP1; ++q) {
-          if (Kt<K>(xx, q) != 0.0) o = fma((T)Kt<K>(xx, q), a[q], o);
-          if (Mt<K>(xx, q) != 0.0) o = fma((T)Mt<K>(xx, q), bb[q], o);
-        }
-        out[xx] = scale * o;
-      }
-    }
-  } else {
-    if (lane < NL) {     // x lines: lane = py, gathered straight into registers
-      const int b = lane * NP1;
-      T u[NP1];
-#pragma unroll
-      for (int q = 0; q < NP1; ++q) {
-        const int gi = decode_dof(__ldg(rp + b + q));
-        u[q] = gi >= 0 ? __ldg(x + gi) : T(0);
-      }
-#pragma unroll
-      for (int xx = 0; xx < NP1; ++xx) {
-        T a = 0, bb = 0;
-#pragma unroll
-        for (int q = 0; q < NP1; ++q) {
-          if (Kt<K>(xx, q) != 0.0) a = fma((T)Kt<K>(xx, q), u[q], a);
-          if (Mt<K>(xx, q) != 0.0) bb = fma((T)Mt<K>(xx, q), u[q], bb);
-        }
-        s0[w][b + xx] = a;
-        s1[w][b + xx] = bb;
-      }
-    }
-    __syncwarp();
-    if (lane < NL) {     // y lines: lane = px
-      ob = lane;
-      os = NP1;
-      T a[NP1], bb[NP1];
-#pragma unroll
-      for (int q = 0; q < NP1; ++q) {
-        a[q] = s0[w][lane + q * NP1];
-        bb[q] = s1[w][lane + q * NP1];
-      }
-#pragma unroll
-      for (int yy = 0; yy < NP1; ++yy) {
-        T o = 0;
-#pragma unroll
-        for (int q = 0; q < NP1; ++q) {
-          if (Mt<K>(yy, q) != 0.0) o = fma((T)Mt<K>(yy, q), a[q], o);
-          if (Kt<K>(yy, q) != 0.0) o = fma((T)Kt<K>(yy, q), bb[q], o);
-        }
-        out[yy] = scale * o;
-      }
-    }
-  }
-  if constexpr (D == 3) {
-    // x-line results -> smem (each lane rewrites the positions it just read), then the
-    // scatter runs along the z lines of the gather with the DoF indices still in registers
-    constexpr int S2 = NP1 * NP1;
-    __syncwarp();        // every lane has read layout B before the natural-layout stores
-    if (lane < NL) {
-#pragma unroll
-      for (int q = 0; q < NP1; ++q) s0[w][ob + q] = out[q];
-    }
-    __syncwarp();
-    if (lane < NL) {
+    for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
+    if (TM != TA_APPLY) {   // requested with the gather: one memory round trip for the epilogue too
       const int px = lane % NP1, py = lane / NP1;
       const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
 #pragma unroll
-      for (int z = 0; z < NP1; ++z) {
+      for (int z = 1; z < 2 * K; ++z) {
         const int i = gi[z];
-        if (i < 0) continue;
-        const T v = s0[w][z * S2 + lane];
-        if (TM != TA_APPLY && inner && z > 0 && z < 2 * K && i < n_r1) {
-          // complete row of an R1 node: Chebyshev step right here
-          T dd = (T)c2_ * pd[z - 1] * (pg[z - 1] - v);
-          if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z - 1], dd);
-          if (WDV) dv[i] = dd;
-          xw[i] = ukeep[z] + dd;
-        } else if (inner && z > 0 && z < 2 * K) {
-          y[i] = v;                                      // only this family touches the node
-        } else {
-          atomicAdd(y + i, v);
+        pg[z - 1] = pd[z - 1] = pv[z - 1] = T(0);
+        if (inner && i >= 0 && i < n_r1) {
+          pg[z - 1] = __ldg(g + i);
+          pd[z - 1] = __ldg(Dinv + i);
+          if (RDV && !DVX) pv[z - 1] = dv[i];
         }
       }
     }
-  } else if (lane < NL) {
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) {
+      T t1 = 0, t2 = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Mt<K>(z, q) != 0.0) t1 = fma((T)Mt<K>(z, q), u[q], t1);
+        if (Kt<K>(z, q) != 0.0) t2 = fma((T)Kt<K>(z, q), u[q], t2);
+      }
+      const int ia = LY::ax * (lane % NP1) + LY::ay * (lane / NP1) + LY::az * z;   // layout A
+      a0[ia] = t1;
+      a1[ia] = t2;
+    }
+  }
+  __syncthreads();
+  T t1[NP1], t2[NP1];
+  const int px = lane % NP1, pz = lane / NP1;   // y lines: lane = (px, pz)
+  if (act) {
+    const int ba = LY::ax * px + LY::az * pz;
 #pragma unroll
     for (int q = 0; q < NP1; ++q) {
-      const int a = ob + q * os;
-      const int i = decode_dof(__ldg(rp + a));
+      t1[q] = a0[ba + LY::ay * q];
+      t2[q] = a1[ba + LY::ay * q];
+    }
+  }
+  __syncthreads();       // layout B overwrites layout A
+  if (act) {
+    const int bb_ = LY::bx * px + LY::bz * pz;
+#pragma unroll
+    for (int yy = 0; yy < NP1; ++yy) {
+      T a = 0, bb = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Mt<K>(yy, q) != 0.0) {
+          a = fma((T)Mt<K>(yy, q), t1[q], a);
+          bb = fma((T)Mt<K>(yy, q), t2[q], bb);
+        }
+        if (Kt<K>(yy, q) != 0.0) bb = fma((T)Kt<K>(yy, q), t1[q], bb);
+      }
+      a0[bb_ + LY::by * yy] = a;   // layout B
+      a1[bb_ + LY::by * yy] = bb;
+    }
+  }
+  __syncthreads();
+  T out[NP1];
+  if (act) {             // x lines: lane = (py, pz)
+    const int bx = LY::by * (lane % NP1) + LY::bz * (lane / NP1);
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) {
+      t1[q] = a0[bx + LY::bx * q];
+      t2[q] = a1[bx + LY::bx * q];
+    }
+#pragma unroll
+    for (int xx = 0; xx < NP1; ++xx) {
+      T o = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Kt<K>(xx, q) != 0.0) o = fma((T)Kt<K>(xx, q), t1[q], o);
+        if (Mt<K>(xx, q) != 0.0) o = fma((T)Mt<K>(xx, q), t2[q], o);
+      }
+      out[xx] = scale * o;
+    }
+  }
+  // x-line results -> layout N, then the scatter runs along the z lines of the
+  // gather with the DoF indices still in registers
+  __syncthreads();       // every lane has read layout B
+  if (act) {
+    const int bn = LY::ny * (lane % NP1) + LY::nz * (lane / NP1);
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) n0[bn + LY::nx * q] = out[q];
+  }
+  __syncthreads();
+  if (act) {
+    const int py = lane / NP1;
+    const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
+    const int bn = LY::nx * px + LY::ny * py;
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) {
+      const int i = gi[z];
       if (i < 0) continue;
-      int ad[3] = {a % NP1, (a / NP1) % NP1, D == 3 ? a / (NP1 * NP1) : 1};
-      bool interior = ad[0] > 0 && ad[0] < 2 * K && ad[1] > 0 && ad[1] < 2 * K && (D == 2 || (ad[2] > 0 && ad[2] < 2 * K));
-      if (interior) y[i] = out[q];       // only this family touches the node
-      else atomicAdd(y + i, out[q]);
+      const T v = n0[bn + LY::nz * z];
+      if (TM != TA_APPLY && inner && z > 0 && z < 2 * K && i < n_r1) {
+        // complete row of an R1 node: Chebyshev step right here
+        T dd = (T)c2_ * pd[z - 1] * (pg[z - 1] - v);
+        if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z - 1], dd);
+        if (WDV) dv[i] = dd;
+        xw[i] = ukeep[z] + dd;
+      } else if (inner && z > 0 && z < 2 * K) {
+        y[i] = v;                                      // only this family touches the node
+      } else {
+        atomicAdd(y + i, v);
+      }
     }
   }
 }
