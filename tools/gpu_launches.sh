@@ -1,0 +1,8 @@
+# launch lists of one V-cycle (both precisions), ncu gpu__time_duration only
+for P in fp64 mixed; do
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --profile --precision $P"
+$CMD > gpurun_out/plain_$P.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file gpurun_out/launches_$P.csv $CMD > gpurun_out/ncu_launches_$P.log 2>&1
+echo launches_$P=$?
+done
