@@ -12,7 +12,7 @@ def load(path):
     for r in rows[hi + 1:]:
         v = float(r[h.index("Metric Value")].replace(",", ""))
         u = r[h.index("Metric Unit")]
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
         out.append((r[h.index("Kernel Name")].split("(")[0].replace("void gmg::dev::", ""), r[h.index("Grid Size")], v))
     return out
 
