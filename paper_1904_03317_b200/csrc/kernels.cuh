@@ -334,7 +334,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   const T scale = (T)(act && fcoef ? scale_ * __ldg(fcoef + f) : scale_);   // config 4: one coefficient per family (levels >= 3)
   int gi[NP1];           // the z-line DoFs of this lane, reused by the scatter
   T ukeep[NP1];          // the gathered x values (x_j of the fused Chebyshev rows)
-  T pg[NP1 - 2], pd[NP1 - 2], pv[NP1 - 2];   // fused modes: g, D^-1, dv of the interior rows
+  T pg[NP1], pd[NP1], pv[NP1];   // fused modes: g, D^-1, dv of the R1 rows
   if (act) {             // z lines: lane = (px, py), gathered straight into registers
 #pragma unroll
     for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
@@ -344,16 +344,14 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
     if (TM != TA_APPLY) {   // requested with the gather: one memory round trip for the epilogue too
-      const int px = lane % NP1, py = lane / NP1;
-      const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
 #pragma unroll
-      for (int z = 1; z < 2 * K; ++z) {
+      for (int z = 0; z < NP1; ++z) {
         const int i = gi[z];
-        pg[z - 1] = pd[z - 1] = pv[z - 1] = T(0);
-        if (inner && i >= 0 && i < n_r1) {
-          pg[z - 1] = __ldg(g + i);
-          pd[z - 1] = __ldg(Dinv + i);
-          if (RDV && !DVX) pv[z - 1] = dv[i];
+        pg[z] = pd[z] = pv[z] = T(0);
+        if (i >= 0 && i < n_r1) {
+          pg[z] = __ldg(g + i);
+          pd[z] = __ldg(Dinv + i);
+          if (RDV && !DVX) pv[z] = dv[i];
         }
       }
     }
@@ -437,13 +435,13 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       const int i = gi[z];
       if (i < 0) continue;
       const T v = n0[bn + LY::nz * z];
-      if (TM != TA_APPLY && inner && z > 0 && z < 2 * K && i < n_r1) {
+      if (TM != TA_APPLY && i < n_r1) {
         // complete row of an R1 node: Chebyshev step right here
-        T dd = (T)c2_ * pd[z - 1] * (pg[z - 1] - v);
-        if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z - 1], dd);
+        T dd = (T)c2_ * pd[z] * (pg[z] - v);
+        if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
         if (WDV) dv[i] = dd;
         xw[i] = ukeep[z] + dd;
-      } else if (inner && z > 0 && z < 2 * K) {
+      } else if (i < n_r1 || (inner && z > 0 && z < 2 * K)) {
         y[i] = v;                                      // only this family touches the node
       } else {
         atomicAdd(y + i, v);

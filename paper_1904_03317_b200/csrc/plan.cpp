@@ -43,12 +43,21 @@ DevicePlan plan_device_order(LocalTopo& T) {
     if (tensor) {
       std::vector<char> remote(no, 0);
       for (i32 s : v.send_idx) remote[s] = 1;
+      // number of local family patches touching each local DoF
+      std::vector<uint8_t> touch(n, 0);
       for (i64 f = 0; f < v.n_fam; ++f)
-        for (int a : inner) {
+        for (int a = 0; a < np; ++a) {
           const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
-          GMG_REQUIRE(g >= 0, GMG_E_STATE, "interior patch node without a DoF");
-          if (g < no && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
+          if (g >= 0 && touch[g] < 255) ++touch[g];
         }
+      for (i64 f = 0; f < v.n_fam; ++f) {
+        for (int a : inner)
+          GMG_REQUIRE(dec(v.fam_dofs[(size_t)f * np + a]) >= 0, GMG_E_STATE, "interior patch node without a DoF");
+        for (int a = 0; a < np; ++a) {
+          const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
+          if (g >= 0 && g < no && touch[g] == 1 && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
+        }
+      }
     }
     P.n_r1[l] = pos;
     for (i64 i = 0; i < no; ++i)
