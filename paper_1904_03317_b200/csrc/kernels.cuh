@@ -309,6 +309,10 @@ template <int K> struct TensorCfg {
 // the gather; those rows never reach y.  Suffix: READ_DV / WRITE_DV.
 // TA_CHEB_X1: the step after the first one from x = 0, where dv_0 = x_1 is not
 // stored and is read from x (from the gather's registers in the epilogue).
+#ifndef TA_EARLY_LOADS_DEFAULT
+#define TA_EARLY_LOADS_DEFAULT 0
+#endif
+constexpr bool TA_EARLY_LOADS = TA_EARLY_LOADS_DEFAULT;
 enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5 };
 
 template <int K, typename T, int TM = TA_APPLY>
@@ -343,7 +347,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
-    if (TM != TA_APPLY) {   // requested with the gather: one memory round trip for the epilogue too
+    if (TM != TA_APPLY && TA_EARLY_LOADS) {   // requested with the gather: one memory round trip
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         const int i = gi[z];
@@ -424,6 +428,18 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     const int bn = LY::ny * (lane % NP1) + LY::nz * (lane / NP1);
 #pragma unroll
     for (int q = 0; q < NP1; ++q) n0[bn + LY::nx * q] = out[q];
+  }
+  if (TM != TA_APPLY && !TA_EARLY_LOADS && act) {   // the epilogue's loads after the passes (fewer live registers)
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) {
+      const int i = gi[z];
+      pg[z] = pd[z] = pv[z] = T(0);
+      if (i >= 0 && i < n_r1) {
+        pg[z] = __ldg(g + i);
+        pd[z] = __ldg(Dinv + i);
+        if (RDV && !DVX) pv[z] = dv[i];
+      }
+    }
   }
   __syncthreads();
   if (act) {
