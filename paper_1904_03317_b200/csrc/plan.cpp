@@ -58,8 +58,14 @@ DevicePlan plan_device_order(LocalTopo& T) {
           if (g >= 0 && g < no && touch[g] == 1 && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
         }
       }
+      P.n_r1[l] = pos;
+      // the rest in the order the family patches first reach them (patch order)
+      for (i64 f = 0; f < v.n_fam; ++f)
+        for (int a = 0; a < np; ++a) {
+          const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
+          if (g >= 0 && g < no && perm[g] < 0) perm[g] = (i32)pos++;
+        }
     }
-    P.n_r1[l] = pos;
     for (i64 i = 0; i < no; ++i)
       if (perm[i] < 0) perm[i] = (i32)pos++;
     GMG_REQUIRE(pos == no, GMG_E_STATE, "device order is not a permutation");
