@@ -274,26 +274,28 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
 // streaming step where the level has no R1 (2D, coefficient levels, level 0).
 template <typename T, int TM, bool RDV, bool WDV, bool DVX = false>
 static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, double c1, double c2,
-                            cudaStream_t s) {
+                            cudaStream_t s, const T* xc = nullptr) {
+  constexpr bool PRO = TM == dev::TA_CHEB_P01;   // x + P x_{l-1} (xc) fused in; only called where n_r1 > 0
   DevLevel& v = d->lv[l];
   import_ghosts(d, l, x, s);
   if (v.n_r1 > 0) {
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
     if (d->k == 2)
       dev::fam_tensor_apply<2, T, TM><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
+          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);
     else
       dev::fam_tensor_apply<1, T, TM><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2);
+          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);
     d->launches++;
     export_add(d, l, t, s);
     const i64 n = v.n_pad - v.n_r1;
     if (n > 0) {
-      dev::cheb_range<T, RDV, WDV, DVX><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
-          v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2);
+      dev::cheb_range<T, RDV, WDV, DVX, PRO><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
+          v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2, v.n_owned);
       d->launches++;
     }
   } else {
+    if (PRO) throw Error(GMG_E_STATE, "fused prolongation on a level without R1");
     k_apply(d, l, nullptr, v.n_cells, (const T*)x, t, s);
     export_add(d, l, t, s);
     k_cheb<T, true, RDV, WDV, false, DVX>(d, v, g, t, dv, x, c1, c2, s);
@@ -304,12 +306,15 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
 // first-kind recurrence: r_j = D^-1 (g - K x_j), dv_j = c1_j dv_{j-1} + c2_j r_j,
 // x_{j+1} = x_j + dv_j; D^-1 = 0 on E rows and ghosts keeps those entries fixed).
 template <typename T>
-static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, bool x_zero, cudaStream_t s) {
+static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, bool x_zero, cudaStream_t s,
+                   const T* xc = nullptr) {
   DevLevel& v = d->lv[l];
   const int m = (int)v.c1.size();     // degree d->m on levels >= 1, the coarse degree on level 0
   if (m == 0) return;
   int j0 = 1;
-  if (x_zero && m > 1) {
+  if (xc) {                            // post-smoothing with x + P x_{l-1} fused into step 0 (prolong_fusable)
+    cheb_step_fused<T, dev::TA_CHEB_P01, false, true>(d, l, g, x, t, dv, 0.0, v.c2[0], s, xc);
+  } else if (x_zero && m > 1) {
     // x_1 = dv_0 = c2_0 D^-1 g: only x is stored, the next step reads dv_0 from x
     k_cheb<T, false, false, false, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
     cheb_step_fused<T, dev::TA_CHEB_X1, true, true, true>(d, l, g, x, t, dv, v.c1[1], v.c2[1], s);
@@ -338,6 +343,17 @@ static void coarse(DeviceHierarchy* d, T* d0, T* x0, T* t0, T* dv0, cudaStream_t
   d->launches++;
 }
 
+// The prolongation can ride on the first post-smoothing step where that step runs
+// the fused operator kernel (R1 present, degree >= 2; GMG_FUSE_PROLONG=0 turns
+// it off for comparison).
+static bool prolong_fusable(DeviceHierarchy* d, int l) {
+  static const bool on = [] {
+    const char* e = std::getenv("GMG_FUSE_PROLONG");
+    return !(e && e[0] == '0');
+  }();
+  return on && d->lv[l].n_r1 > 0 && d->lv[l].c1.size() > 1;
+}
+
 // The V-cycle on the MG-layout buffers D (defects, copy_to_mg done), X (out).
 template <typename T>
 static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
@@ -358,8 +374,12 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
     T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
     T* xc = X + d->lv[l - 1].off;
     import_ghosts(d, l - 1, xc, s);
-    k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, xc, x, s);         // 5: x += P x_{l-1}
-    smooth(d, l, g, x, t, dv, false, s);                                    // 6: post-smooth
+    if (prolong_fusable(d, l)) {
+      smooth(d, l, g, x, t, dv, false, s, (const T*)xc);                    // 5 + 6 in one pass over the level
+    } else {
+      k_prolongate<dev::XFER_ADD>(d, l, nullptr, v.n_fam, xc, x, s);       // 5: x += P x_{l-1}
+      smooth(d, l, g, x, t, dv, false, s);                                  // 6: post-smooth
+    }
   }
 }
 

@@ -269,6 +269,33 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
 
 constexpr int TENSOR_WARPS = 8;
 
+// one 1-D pass over `lines` lines of a 3-index array: in(i, q, o) -> out(i, p, o),
+// out = sum_q M(p, q) in, with M = P (UP: q < N, p < NP1) or P^T (!UP)
+template <int K, bool UP, int NI, int NO, typename T>
+__device__ __forceinline__ void xfer_pass(int lane, const T* in, T* out, int si_in, int sq_in, int so_in,
+                                          int si_out, int sp_out, int so_out) {
+  constexpr int N = K + 1, NP1 = 2 * K + 1;
+  constexpr int NQ = UP ? N : NP1, NPo = UP ? NP1 : N;
+  for (int L = lane; L < NI * NO; L += 32) {
+    const int i = L / NO, o = L % NO;
+    T v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = in[i * si_in + q * sq_in + o * so_in];
+#pragma unroll
+    for (int p = 0; p < NPo; ++p) {
+      T s = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const double m = UP ? Q<K>::P(p, q) : Q<K>::P(q, p);
+        if (m != 0.0) s = fma((T)m, v[q], s);
+      }
+      out[i * si_out + p * sp_out + o * so_out] = s;
+    }
+  }
+}
+
 // fam_tensor_apply (3D) runs one block of TG_WARPS warps over FPB = 32 TG_WARPS
 // / (2k+1)^2 families (5 for Q2, 14 for Q1), one thread per 1-D line of a
 // patch: 125 of 128 lanes busy instead of 25 of 32 with a warp per family.
@@ -313,21 +340,32 @@ template <int K> struct TensorCfg {
 #define TA_EARLY_LOADS_DEFAULT 0
 #endif
 constexpr bool TA_EARLY_LOADS = TA_EARLY_LOADS_DEFAULT;
-enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5 };
+// TA_CHEB_P01: the prolongation x += P x_{l-1} fused into the first step of the
+// post-smoothing (TA_CHEB_01 on x + P x_{l-1}).  Every family computes P x_{l-1}
+// on its whole patch from its parent's values: a fine node on a face, edge or
+// corner shared with a family of another parent gets the same value bit for bit
+// from either parent (the 1-D weights across the shared coordinate are exact
+// picks, the others are the same weights on the same coarse values in the same
+// order), so the gathered x + P x_{l-1} equals what warp_prolongate writes.  R1
+// rows are finished here; for the other rows the transfer-owner family leaves
+// P x_{l-1} in dv (dead before this step) and cheb_range<..., PRO> adds it.
+enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5,
+             TA_CHEB_P01 = 6 };
 
 template <int K, typename T, int TM = TA_APPLY>
 __global__ void __launch_bounds__(32 * TG_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                 double c1_ = 0, double c2_ = 0) {
-  constexpr bool DVX = TM == TA_CHEB_X1;
+                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr) {
+  constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
-  constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX;
+  constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   constexpr int NP1 = 2 * K + 1, S2 = NP1 * NP1, NL = TensorCfg<K>::NL, FPB = TensorCfg<K>::FPB;
   using LY = PatchLayout<K, T>;
   constexpr int NS = FPB * (LY::sab > LY::sn ? LY::sab : LY::sn);
   __shared__ T s0[NS], s1[NS];
+  __shared__ T cb[PRO ? FPB : 1][(K + 1) * (K + 1) * (K + 1) + 1];   // PRO: the parents' values
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
   const long f = (long)blockIdx.x * FPB + slot;
   const bool act = slot < FPB && f < nfam;
@@ -339,12 +377,71 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   int gi[NP1];           // the z-line DoFs of this lane, reused by the scatter
   T ukeep[NP1];          // the gathered x values (x_j of the fused Chebyshev rows)
   T pg[NP1], pd[NP1], pv[NP1];   // fused modes: g, D^-1, dv of the R1 rows
+  T inc[PRO ? NP1 : 1];          // PRO: (P x_{l-1}) on the z line
+  int own = 0;                   // PRO: bit z = the family is the row's transfer owner
+  if constexpr (PRO) {
+    // P x_{l-1} on this thread's z line, in registers: the parent's values are
+    // staged once per family, then (P (x) P (x) P) restricted to (px, py, *) in
+    // warp_prolongate's order (x, then y, then z; fma chains over ascending
+    // coarse index; a zero weight adds an exact 0), so the result is its
+    // bit pattern
+    constexpr int N = K + 1, NC = N * N * N, NPT = NP1 * NP1 * NP1;
+    if (act) {
+      for (int c = lane; c < NC; c += NL) {    // 27 values, 25 lines
+        const int ci = __ldg(rp + NPT + c);
+        cb[slot][c] = ci >= 0 ? __ldg(xc + ci) : T(0);
+      }
+    }
+    __syncthreads();
+    if (act) {
+      const int px = lane % NP1, py = lane / NP1;
+      T wx[N], wy[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        wx[a] = wy[a] = T(0);
+#pragma unroll
+        for (int p = 0; p < NP1; ++p) {
+          if (px == p) wx[a] = (T)Q<K>::P(p, a);
+          if (py == p) wy[a] = (T)Q<K>::P(p, a);
+        }
+      }
+      T w[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        w[c] = T(0);
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+          T sx = T(0);
+#pragma unroll
+          for (int a = 0; a < N; ++a) sx = fma(wx[a], cb[slot][a + N * b + N * N * c], sx);
+          w[c] = fma(wy[b], sx, w[c]);
+        }
+      }
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) {
+        T sz = T(0);
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          if (Q<K>::P(z, c) != 0.0) sz = fma((T)Q<K>::P(z, c), w[c], sz);
+        inc[z] = sz;
+      }
+    }
+  }
   if (act) {             // z lines: lane = (px, py), gathered straight into registers
 #pragma unroll
-    for (int z = 0; z < NP1; ++z) gi[z] = decode_dof(__ldg(rp + z * S2 + lane));
+    for (int z = 0; z < NP1; ++z) {
+      const int e = __ldg(rp + z * S2 + lane);
+      gi[z] = decode_dof(e);
+      if (PRO && e >= 0) own |= 1 << z;
+    }
     T u[NP1];
 #pragma unroll
-    for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+    for (int z = 0; z < NP1; ++z) {
+      u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+      if constexpr (PRO) {
+        if (gi[z] >= 0) u[z] = u[z] + inc[z];    // = warp_prolongate's old + fine
+      }
+    }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
     if (TM != TA_APPLY && TA_EARLY_LOADS) {   // requested with the gather: one memory round trip
@@ -457,10 +554,10 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
         if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
         if (WDV) dv[i] = dd;
         xw[i] = ukeep[z] + dd;
-      } else if (i < n_r1 || (inner && z > 0 && z < 2 * K)) {
-        y[i] = v;                                      // only this family touches the node
       } else {
-        atomicAdd(y + i, v);
+        if (PRO && ((own >> z) & 1)) dv[i] = inc[z];  // P x_{l-1} of a streamed row (cheb_range<PRO>)
+        if (i < n_r1 || (inner && z > 0 && z < 2 * K)) y[i] = v;   // only this family touches the node
+        else atomicAdd(y + i, v);
       }
     }
   }
@@ -652,14 +749,16 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
 
 // The Chebyshev step on [a, n) only (the rows not finished by the fused apply):
 // scalar form of cheb_step<T, READ_T = 1, ..., X_ZERO = 0>.
-template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false>
+template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false, bool PRO = false>
 __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __restrict__ g,
                                                      const T* __restrict__ Dinv, T* __restrict__ t,
-                                                     T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_) {
+                                                     T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_,
+                                                     long n_own = 0) {
   const long i = a + (long)blockIdx.x * VEC_NT + threadIdx.x;
   if (i >= n) return;
   const T G = g[i], Tv = t[i], Di = Dinv[i];
-  const T X = x[i];
+  T X = x[i];
+  if (PRO && i < n_own) X = X + dv[i];   // x + P x_{l-1} (fam_tensor_apply<TA_CHEB_P01> left it in dv)
   T V = 0;
   if (READ_DV) V = DV_IS_X ? X : dv[i];      // DV_IS_X: dv_0 = x_1 after the first step from 0
   t[i] = Tv - Tv;                       // data-dependent reset (see cheb_step)
@@ -697,33 +796,6 @@ enum : int { XFER_ADD = 0, XFER_SET_E = 1 };
 enum : int { RES_PLAIN = 0, RES_VCYCLE = 1, RES_EONLY = 2 };
 
 constexpr int XFER_WARPS = 4;
-
-// one 1-D pass over `lines` lines of a 3-index array: in(i, q, o) -> out(i, p, o),
-// out = sum_q M(p, q) in, with M = P (UP: q < N, p < NP1) or P^T (!UP)
-template <int K, bool UP, int NI, int NO, typename T>
-__device__ __forceinline__ void xfer_pass(int lane, const T* in, T* out, int si_in, int sq_in, int so_in,
-                                          int si_out, int sp_out, int so_out) {
-  constexpr int N = K + 1, NP1 = 2 * K + 1;
-  constexpr int NQ = UP ? N : NP1, NPo = UP ? NP1 : N;
-  for (int L = lane; L < NI * NO; L += 32) {
-    const int i = L / NO, o = L % NO;
-    T v[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) v[q] = in[i * si_in + q * sq_in + o * so_in];
-#pragma unroll
-    for (int p = 0; p < NPo; ++p) {
-      T s = 0;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const double m = UP ? Q<K>::P(p, q) : Q<K>::P(q, p);
-        if (m != 0.0) s = fma((T)m, v[q], s);
-      }
-      out[i * si_out + p * sp_out + o * so_out] = s;
-    }
-  }
-}
 
 template <int D, int K>
 struct XferShape {
