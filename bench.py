@@ -368,7 +368,11 @@ def run_ours(args):
                             "kernel": ("fam_tensor_apply<3,%d,%s>" if cfg["dim"] == 3 else "fam_tensor_apply2d<%d,%s>")
                                       % (cfg["k"], "float" if mixed else "double") + " (level operator), finest level",
                             "algorithmic_bytes_per_launch": alg_bytes, "launch_s": t_apply,
-                            "share_of_step": share, "peak_source": peak_src},
+                            "share_of_step": share,
+                            "share_definition": "8 finest-level operator passes per V-cycle x this kernel's "
+                                                "launch time / step time (the fused variants of those "
+                                                "passes do more work: profiles/r01_launches_*.txt)",
+                            "peak_source": peak_src},
                "cpu_baseline": cpu,
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * info["n_leaf_free"],
                        "d2h_bytes_per_step": 8 * info["n_leaf_free"], "steps": e2e_steps,
