@@ -242,6 +242,11 @@ typedef struct {
   int64_t level_S[GMG_MAX_LEVELS], level_E[GMG_MAX_LEVELS], level_B[GMG_MAX_LEVELS];
   int64_t level_leaf_cells[GMG_MAX_LEVELS];
   int64_t mg_vector_len;     /* sum of the level vector lengths */
+  /* this rank's rows the level-operator kernel finishes itself (device order R1,
+   * csrc/plan.hpp: owned rows exactly one local family patch touches and no
+   * other rank needs); 0 on levels without the family-tensor kernel and for
+   * GMG_HOST_ONLY hierarchies */
+  int64_t level_r1[GMG_MAX_LEVELS];
 } gmg_info;
 gmg_status gmg_hierarchy_info(const gmg_hierarchy *h, gmg_info *out);
 /* Leaf vectors of this rank: n_owned free leaf DoFs, the global

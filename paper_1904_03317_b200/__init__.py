@@ -91,7 +91,8 @@ class Info(C.Structure):
                 ("level_dofs", C.c_int64 * MAX_LEVELS), ("level_cells", C.c_int64 * MAX_LEVELS),
                 ("level_families", C.c_int64 * MAX_LEVELS), ("level_S", C.c_int64 * MAX_LEVELS),
                 ("level_E", C.c_int64 * MAX_LEVELS), ("level_B", C.c_int64 * MAX_LEVELS),
-                ("level_leaf_cells", C.c_int64 * MAX_LEVELS), ("mg_vector_len", C.c_int64)]
+                ("level_leaf_cells", C.c_int64 * MAX_LEVELS), ("mg_vector_len", C.c_int64),
+                ("level_r1", C.c_int64 * MAX_LEVELS)]
 
 
 _vp = C.c_void_p
@@ -319,7 +320,7 @@ class Hierarchy:
         nl = i.n_levels
         out = {f: getattr(i, f) for f, _ in Info._fields_ if not f.startswith("level_")}
         for f in ("level_dofs", "level_cells", "level_families", "level_S", "level_E", "level_B",
-                  "level_leaf_cells"):
+                  "level_leaf_cells", "level_r1"):
             out[f] = list(getattr(i, f)[:nl])
         return out
 

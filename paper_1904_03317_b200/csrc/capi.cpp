@@ -287,6 +287,7 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
       o->level_E[l] = t.nE;
       o->level_B[l] = t.nB;
       o->level_leaf_cells[l] = (gmg::i64)t.leaf_cells.size();
+      o->level_r1[l] = h->dev ? gmg::device_level_r1(h->dev, l) : 0;
       mg += (t.n_dofs + 511) / 512 * 512;   // device segment padding (kernels.cuh VEC_PAD)
     }
     o->mg_vector_len = mg;

@@ -816,6 +816,10 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
   return d;
 }
 
+long long device_level_r1(const DeviceHierarchy* d, int level) {
+  return d && level >= 0 && level < (int)d->lv.size() ? (long long)d->lv[level].n_r1 : 0;
+}
+
 void device_destroy(DeviceHierarchy* d) {
   if (!d) return;
   cudaDeviceSynchronize();
