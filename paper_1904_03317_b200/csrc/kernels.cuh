@@ -379,6 +379,17 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   T pg[NP1], pd[NP1], pv[NP1];   // fused modes: g, D^-1, dv of the R1 rows
   T inc[PRO ? NP1 : 1];          // PRO: (P x_{l-1}) on the z line
   int own = 0;                   // PRO: bit z = the family is the row's transfer owner
+  T u[NP1];
+  if (act) {             // z lines: lane = (px, py), gathered straight into registers
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) {
+      const int e = __ldg(rp + z * S2 + lane);
+      gi[z] = decode_dof(e);
+      if (PRO && e >= 0) own |= 1 << z;
+    }
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+  }
   if constexpr (PRO) {
     // P x_{l-1} on this thread's z line, in registers: the parent's values are
     // staged once per family, then (P (x) P (x) P) restricted to (px, py, *) in
@@ -427,20 +438,11 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
     }
   }
-  if (act) {             // z lines: lane = (px, py), gathered straight into registers
+  if (act) {
+    if constexpr (PRO) {   // the gather above is in flight while P x_{l-1} is formed
 #pragma unroll
-    for (int z = 0; z < NP1; ++z) {
-      const int e = __ldg(rp + z * S2 + lane);
-      gi[z] = decode_dof(e);
-      if (PRO && e >= 0) own |= 1 << z;
-    }
-    T u[NP1];
-#pragma unroll
-    for (int z = 0; z < NP1; ++z) {
-      u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
-      if constexpr (PRO) {
+      for (int z = 0; z < NP1; ++z)
         if (gi[z] >= 0) u[z] = u[z] + inc[z];    // = warp_prolongate's old + fine
-      }
     }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
