@@ -336,10 +336,15 @@ template <int K> struct TensorCfg {
 // the gather; those rows never reach y.  Suffix: READ_DV / WRITE_DV.
 // TA_CHEB_X1: the step after the first one from x = 0, where dv_0 = x_1 is not
 // stored and is read from x (from the gather's registers in the epilogue).
-#ifndef TA_EARLY_LOADS_DEFAULT
-#define TA_EARLY_LOADS_DEFAULT 0
+// Where the fused epilogue requests g, D^-1, dv of its R1 rows: 0 with the x
+// gather (80 registers), 1 after the z pass, 2 after the last pass (56).
+#ifndef TA_LOAD_AT_DEFAULT
+#define TA_LOAD_AT_DEFAULT 2
 #endif
-constexpr bool TA_EARLY_LOADS = TA_EARLY_LOADS_DEFAULT;
+constexpr int TA_LOAD_AT = TA_LOAD_AT_DEFAULT;
+#ifndef TA_MIN_BLOCKS
+#define TA_MIN_BLOCKS 1
+#endif
 // TA_CHEB_P01: the prolongation x += P x_{l-1} fused into the first step of the
 // post-smoothing (TA_CHEB_01 on x + P x_{l-1}).  Every family computes P x_{l-1}
 // on its whole patch from its parent's values: a fine node on a face, edge or
@@ -353,7 +358,7 @@ enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CH
              TA_CHEB_P01 = 6 };
 
 template <int K, typename T, int TM = TA_APPLY>
-__global__ void __launch_bounds__(32 * TG_WARPS)
+__global__ void __launch_bounds__(32 * TG_WARPS, TM == TA_APPLY ? 1 : TA_MIN_BLOCKS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
@@ -446,7 +451,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
-    if (TM != TA_APPLY && TA_EARLY_LOADS) {   // requested with the gather: one memory round trip
+    if (TM != TA_APPLY && TA_LOAD_AT == 0) {   // requested with the gather: one memory round trip
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         const int i = gi[z];
@@ -469,6 +474,18 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       const int ia = LY::ax * (lane % NP1) + LY::ay * (lane / NP1) + LY::az * z;   // layout A
       a0[ia] = t1;
       a1[ia] = t2;
+    }
+    if (TM != TA_APPLY && TA_LOAD_AT == 1) {   // in flight across the y and x passes
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) {
+        const int i = gi[z];
+        pg[z] = pd[z] = pv[z] = T(0);
+        if (i >= 0 && i < n_r1) {
+          pg[z] = __ldg(g + i);
+          pd[z] = __ldg(Dinv + i);
+          if (RDV && !DVX) pv[z] = dv[i];
+        }
+      }
     }
   }
   __syncthreads();
@@ -528,7 +545,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
 #pragma unroll
     for (int q = 0; q < NP1; ++q) n0[bn + LY::nx * q] = out[q];
   }
-  if (TM != TA_APPLY && !TA_EARLY_LOADS && act) {   // the epilogue's loads after the passes (fewer live registers)
+  if (TM != TA_APPLY && TA_LOAD_AT == 2 && act) {   // the epilogue's loads after the passes (fewer live registers)
 #pragma unroll
     for (int z = 0; z < NP1; ++z) {
       const int i = gi[z];
