@@ -342,9 +342,7 @@ template <int K> struct TensorCfg {
 #define TA_LOAD_AT_DEFAULT 2
 #endif
 constexpr int TA_LOAD_AT = TA_LOAD_AT_DEFAULT;
-#ifndef TA_MIN_BLOCKS
-#define TA_MIN_BLOCKS 1
-#endif
+
 // TA_CHEB_P01: the prolongation x += P x_{l-1} fused into the first step of the
 // post-smoothing (TA_CHEB_01 on x + P x_{l-1}).  Every family computes P x_{l-1}
 // on its whole patch from its parent's values: a fine node on a face, edge or
@@ -358,7 +356,7 @@ enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CH
              TA_CHEB_P01 = 6 };
 
 template <int K, typename T, int TM = TA_APPLY>
-__global__ void __launch_bounds__(32 * TG_WARPS, TM == TA_APPLY ? 1 : TA_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * TG_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
