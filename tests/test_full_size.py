@@ -1,5 +1,5 @@
-"""Config 3 at its full size (49.8M leaf DoFs, 11 levels), in the launch
-configuration bench.py times (gmg_setup defaults: CUDA graph, degree-4
+"""Configs 3 (49.8M leaf DoFs, 11 levels) and 4 (107M leaf nodes, 20 levels,
+variable coefficient) at their full sizes, in the launch configuration bench.py times (gmg_setup defaults: CUDA graph, degree-4
 Chebyshev, family-tensor operator kernels, device order with R1).
 
 The oracle cannot assemble this hierarchy in seconds, so the checks are
@@ -21,7 +21,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_1904_03317_b200 as G  # noqa: E402
-from gmg_inputs import config, uniform_pm1, STREAM_PROBE  # noqa: E402
+from gmg_inputs import config, uniform_pm1, log_uniform_coef, STREAM_PROBE  # noqa: E402
 from oracle import fem  # noqa: E402
 
 OP_TOL = 1e-12
@@ -139,3 +139,65 @@ def test_c3_mixed_precision_vcycle(h64):
     hm.vcycle(b, x32)
     err = float((x32 - x64).abs().max() / x64.abs().max())
     assert 1e-9 < err < MIXED_VC_TOL, err
+
+
+# ---------------------------------------------------------------- config 4, full size
+# 107M leaf nodes, 20 levels, a log-uniform per level-2 cell (R15, R20): sampled
+# rows of the level operator on a coefficient level against a(cell) times the
+# oracle element matrix, and the preconditioner / CG properties.
+_h4 = {}
+
+
+def hier4():
+    if "h" not in _h4:
+        cfg = config("c4")
+        coef = log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+        f = G.gmg_forest_generate(G.recipe_from_config(cfg))
+        part = G.gmg_partition(f, 1)
+        _h4["h"] = (G.gmg_setup(f, part, k=cfg["k"], coef_level2=coef), part, coef)
+    return _h4["h"]
+
+
+@pytest.mark.parametrize("which", ["finest", "middle"])
+def test_c4_level_apply_sampled_rows(which):
+    h, part, coef = hier4()
+    info = h.info()
+    L = info["n_levels"] - 1
+    l = L if which == "finest" else 10
+    n = info["level_dofs"][l]
+    x = uniform_pm1(n, STREAM_PROBE, offset=23)
+    y = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.level_apply(l, dev(x), y)
+    y = y.cpu().numpy()
+    cd = h.cell_dofs(l)
+    keys, _, _ = part.level_cells(l)
+    keys2, _, _ = part.level_cells(2)
+    a_cell = coef[np.searchsorted(keys2, keys >> np.uint64(3 * (l - 2)))]   # R15: the level-2 ancestor's a
+    rows = np.random.default_rng(190403317 + l).choice(n, size=min(N_SAMPLE, n), replace=False)
+    Ke = fem.element_laplace(info["dim"], info["k"], 2.0 ** -l)
+    cells, bs = np.nonzero(np.isin(cd, rows))
+    xc = np.where(cd[cells] >= 0, x[np.maximum(cd[cells], 0)], 0.0)
+    contrib = a_cell[cells] * np.einsum("ij,ij->i", Ke[bs], xc)
+    ref = np.zeros(n)
+    np.add.at(ref, cd[cells, bs], contrib)
+    err = np.abs(y[rows] - ref[rows]).max() / np.abs(ref[rows]).max()
+    assert err < OP_TOL, (l, err)
+
+
+def test_c4_vcycle_symmetric_and_cg():
+    h, _, _ = hier4()
+    n = h.info()["n_leaf_free"]
+    b1, b2 = dev(uniform_pm1(n)), dev(uniform_pm1(n, STREAM_PROBE))
+    v1, v2 = torch.zeros_like(b1), torch.zeros_like(b1)
+    h.vcycle(b1, v1)
+    h.vcycle(b2, v2)
+    assert abs(dot(v1, b2) - dot(b1, v2)) <= VC_TOL * float(v1.norm() * b2.norm())
+    assert dot(v1, b1) > 0 and dot(v2, b2) > 0
+    b = torch.zeros(n, device="cuda", dtype=torch.float64)
+    h.rhs_constant(1.0, b)
+    x = torch.zeros_like(b)
+    it, relres, _ = h.solve_cg(b, x, rtol=1e-8)
+    assert relres <= 1e-8 and 1 <= it <= 15, (it, relres)
+    r = torch.zeros_like(b)
+    h.leaf_apply(x, r)
+    assert float((b - r).norm() / b.norm()) <= 1.01e-8
