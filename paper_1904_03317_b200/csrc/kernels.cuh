@@ -329,11 +329,12 @@ template <int K> struct TensorCfg {
   static constexpr int NL = (2 * K + 1) * (2 * K + 1), FPB = 32 * TG_WARPS / NL;
 };
 
-// Epilogue modes of fam_tensor_apply: TA_APPLY y += K x (patch-interior rows
-// stored, others reduced); TA_CHEB_* in addition finish the Chebyshev-Jacobi
-// step on the interior rows of R1 (plan.hpp: only this family
-// touches them): dv = c1 dv + c2 D^-1 (g - K x), x += dv, with x_j taken from
-// the gather; those rows never reach y.  Suffix: READ_DV / WRITE_DV.
+// Epilogue modes of fam_tensor_apply: TA_APPLY y += K x (rows only this
+// family touches -- R1 rows, rows < n_r1, and patch-interior nodes -- stored,
+// the others reduced at L2); TA_CHEB_* in addition finish the Chebyshev-Jacobi
+// step on the R1 rows (plan.hpp): dv = c1 dv + c2 D^-1 (g - K x),
+// x += dv, with x_j taken from the gather; those rows never reach y.  Suffix:
+// READ_DV / WRITE_DV.
 // TA_CHEB_X1: the step after the first one from x = 0, where dv_0 = x_1 is not
 // stored and is read from x (from the gather's registers in the epilogue).
 // Where the fused epilogue requests g, D^-1, dv of its R1 rows: 0 with the x
