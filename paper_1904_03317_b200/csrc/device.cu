@@ -235,13 +235,23 @@ static void apply_full(DeviceHierarchy* d, int l, T* x, T* t, cudaStream_t s) {
   export_add(d, l, t, s);
 }
 
+// The transfer kernels are persistent (grid-stride over families): launch one
+// resident wave, not more -- with a second partial wave the late blocks hold the
+// same share of families and finish a third of a block's time after the rest.
+template <typename Kern>
+static int xfer_grid(DeviceHierarchy* d, i64 nf, Kern kern) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * dev::XFER_WARPS, 0));
+  return (int)std::max<i64>(1, std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS,
+                                             (i64)std::max(per_sm, 1) * d->sms));
+}
+
 template <int MODE, typename T>
 static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const T* vin, T* t, T* dc,
                        cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
-  DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE, T><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+  DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE, T><<<xfer_grid(d, nf, dev::warp_restrict<D_, K_, MODE, T>), 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, vin, t, dc)));
   d->launches++;
 }
@@ -251,8 +261,7 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
                          cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
-  const int grid = (int)std::min<i64>((nf + dev::XFER_WARPS - 1) / dev::XFER_WARPS, (i64)d->sms * 16);
-  DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE, T><<<grid, 32 * dev::XFER_WARPS, 0, s>>>(
+  DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE, T><<<xfer_grid(d, nf, dev::warp_prolongate<D_, K_, MODE, T>), 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, xc, xf)));
   d->launches++;
 }
