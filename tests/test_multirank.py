@@ -253,3 +253,57 @@ def test_local_ranks_equal_single_rank(name, p):
         assert it == it1
     assert np.abs(xv - ref_x).max() <= 1e-12 * np.abs(ref_x).max()
     assert np.abs(xsv - ref_s).max() <= 1e-9 * np.abs(ref_s).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,p", [("c3p2", 3), ("c4s", 2)])
+def test_local_ranks_mixed_precision(name, p):
+    """The fp32 V-cycle (R13) sharded over p local ranks (fp64 wire format for the
+    ghost values) equals the single-rank fp32 V-cycle up to fp32 rounding (the
+    reductions of shared rows add in a different order), and its CG converges in
+    the same number of iterations."""
+    import torch
+    if name == "c4s":
+        cfg = config("c4")
+        cfg.update(s=2, lmax=7)
+    else:
+        cfg = config(name)
+    _, _, h1 = G.build_config(cfg, coef_level2=_coef(cfg), mixed=True)
+    n = h1.info()["n_leaf_free"]
+    canon1 = h1.leaf_dofs()[3]
+    b_can = uniform_pm1(n)
+    b1 = torch.tensor(b_can[canon1], device="cuda", dtype=torch.float64)
+    x1 = torch.zeros_like(b1)
+    h1.vcycle(b1, x1)
+    rhs1 = torch.zeros_like(b1)
+    h1.rhs_constant(1.0, rhs1)
+    it1, _, _ = h1.solve_cg(rhs1, torch.zeros_like(b1), rtol=1e-8)
+    ref_x = np.empty(n)
+    ref_x[canon1] = x1.cpu().numpy()
+
+    world, lf, part, hs, streams = _local_group(cfg, p, mixed=True)
+    canon = hs[0].leaf_dofs()[3]
+    res = [None] * p
+
+    def work(r):
+        def fn():
+            torch.cuda.set_device(0)
+            info = hs[r].info()
+            fo, no = info["first_owned"], info["n_owned"]
+            with torch.cuda.stream(streams[r]):
+                b = torch.tensor(b_can[canon[fo:fo + no]], device="cuda", dtype=torch.float64)
+                x = torch.zeros_like(b)
+                hs[r].vcycle(b, x, stream=streams[r].cuda_stream)
+                rhs = torch.zeros_like(b)
+                hs[r].rhs_constant(1.0, rhs, stream=streams[r].cuda_stream)
+                it, _, _ = hs[r].solve_cg(rhs, torch.zeros_like(b), rtol=1e-8, stream=streams[r].cuda_stream)
+                streams[r].synchronize()
+            res[r] = (fo, no, x.cpu().numpy(), it)
+        return fn
+
+    _run_threads([work(r) for r in range(p)])
+    xv = np.empty(n)
+    for fo, no, x, it in res:
+        xv[canon[fo:fo + no]] = x
+        assert abs(it - it1) <= 1
+    assert np.abs(xv - ref_x).max() <= 2e-5 * np.abs(ref_x).max()
