@@ -173,6 +173,9 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- primitives
+// grid of the four-entries-per-thread copy kernels (gather_to_mg / gather_from_mg)
+static int grid4(i64 n) { return (int)std::max<i64>(1, (n + 1023) / 1024); }
+
 template <int K>
 static int tensor_grid(i64 n_fam) {
   return (int)((n_fam + dev::TensorCfg<K>::FPB - 1) / dev::TensorCfg<K>::FPB);
@@ -843,13 +846,13 @@ void device_destroy(DeviceHierarchy* d) {
 void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int gr = d->vgrid(d->N);
-  if (d->mixed) dev::gather_to_mg<float><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32);   // copy_to_mg
-  else dev::gather_to_mg<double><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);
+  if (d->mixed) dev::gather_to_mg<float><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32);   // copy_to_mg
+  else dev::gather_to_mg<double><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);
   d->launches++;
   run_vcycle_mg(d, s);
   if (d->n_leaf) {                                                                              // copy_from_mg
-    if (d->mixed) dev::gather_from_mg<float><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X32, x);
-    else dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);
+    if (d->mixed) dev::gather_from_mg<float><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X32, x);
+    else dev::gather_from_mg<double><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
@@ -882,7 +885,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
   const i64 N = d->N;
   const int gr = d->vgrid(N);
   // r = b (MG layout), x = 0
-  dev::gather_to_mg<double><<<gr, 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
+  dev::gather_to_mg<double><<<grid4(N), 256, 0, s>>>(N, d->mg_to_leaf, b, d->cr);
   CK(cudaMemsetAsync(d->cx, 0, N * sizeof(double), s));
   d->launches++;
   double nb = std::sqrt(host_dot(d, N, d->cr, d->cr, s));
@@ -918,7 +921,7 @@ int device_solve_cg(DeviceHierarchy* d, const double* b, double* x, double rtol,
     if (it > max_it) it = max_it;
   }
   if (d->n_leaf) {
-    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
+    dev::gather_from_mg<double><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cx, x);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
@@ -946,7 +949,7 @@ void device_rhs_constant(DeviceHierarchy* d, double f, double* b, void* stream) 
   }
   export_add(d, 0, d->Y + d->lv[0].off, s);
   if (d->n_leaf) {
-    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
+    dev::gather_from_mg<double><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->Y, b);
     d->launches++;
   }
   CK(cudaPeekAtLastError());
@@ -1026,11 +1029,11 @@ void device_prolongate(DeviceHierarchy* d, int l, const double* xc, double* xf, 
 void device_leaf_apply(DeviceHierarchy* d, const double* u, double* v, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int gr = d->vgrid(d->N);
-  dev::gather_to_mg<double><<<gr, 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
+  dev::gather_to_mg<double><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, u, d->cp);
   d->launches++;
   leaf_apply_mg(d, d->cp, d->cq, d->partial, s);
   if (d->n_leaf) {
-    dev::gather_from_mg<double><<<d->vgrid(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
+    dev::gather_from_mg<double><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->cq, v);
     d->launches++;
   }
   CK(cudaPeekAtLastError());

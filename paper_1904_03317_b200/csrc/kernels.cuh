@@ -1028,23 +1028,53 @@ __global__ void cast_vec(long n, const double* __restrict__ in, T* __restrict__ 
 }
 
 // MG layout <- leaf order: out[m] = (inv[m] >= 0 ? in[inv[m]] : 0)
+// Four consecutive entries per thread: the four index loads are one 16-byte load
+// and the four gathers are in flight together (one element per thread and
+// iteration left these latency bound).  Callers launch ceil(n / 1024) blocks of
+// 256 threads.
 template <typename T>
-__global__ void gather_to_mg(long n, const int* __restrict__ inv, const double* __restrict__ in,
-                             T* __restrict__ out) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long stride = (long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) {
-    const int s = inv[i];
-    out[i] = s >= 0 ? (T)in[s] : T(0);
+__device__ __forceinline__ void store4(T* p, T a, T b, T c, T d, bool vec) {
+  if (vec) {
+    if constexpr (sizeof(T) == 8) {
+      reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+      reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+    } else {
+      *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+    }
+  } else {
+    p[0] = a; p[1] = b; p[2] = c; p[3] = d;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_to_mg(long n, const int* __restrict__ inv, const double* __restrict__ in,
+                                                    T* __restrict__ out) {
+  const long i0 = ((long)blockIdx.x * 256 + threadIdx.x) * 4;
+  if (i0 + 3 < n) {
+    const int4 s = *reinterpret_cast<const int4*>(inv + i0);   // inv: device allocation, i0 % 4 == 0
+    const T a = s.x >= 0 ? (T)__ldg(in + s.x) : T(0), b = s.y >= 0 ? (T)__ldg(in + s.y) : T(0);
+    const T c = s.z >= 0 ? (T)__ldg(in + s.z) : T(0), d = s.w >= 0 ? (T)__ldg(in + s.w) : T(0);
+    store4(out + i0, a, b, c, d, true);                        // MG layout: device allocation
+  } else {
+    for (long i = i0; i < n; ++i) {
+      const int s = inv[i];
+      out[i] = s >= 0 ? (T)in[s] : T(0);
+    }
   }
 }
 // leaf order <- MG layout
 template <typename T>
-__global__ void gather_from_mg(long n, const int* __restrict__ perm, const T* __restrict__ in,
-                               double* __restrict__ out) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long stride = (long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) out[i] = (double)in[perm[i]];
+__global__ void __launch_bounds__(256) gather_from_mg(long n, const int* __restrict__ perm, const T* __restrict__ in,
+                                                      double* __restrict__ out) {
+  const long i0 = ((long)blockIdx.x * 256 + threadIdx.x) * 4;
+  if (i0 + 3 < n) {
+    const int4 s = *reinterpret_cast<const int4*>(perm + i0);
+    const double a = (double)__ldg(in + s.x), b = (double)__ldg(in + s.y);
+    const double c = (double)__ldg(in + s.z), d = (double)__ldg(in + s.w);
+    store4(out + i0, a, b, c, d, ((unsigned long long)out & 15) == 0);   // out: the caller's leaf vector
+  } else {
+    for (long i = i0; i < n; ++i) out[i] = (double)in[perm[i]];
+  }
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
