@@ -429,8 +429,13 @@ static void leaf_apply_mg(DeviceHierarchy* d, const double* p, double* q, double
   }
   import_ghosts(d, L, d->W + d->lv[L].off, s);
   CK(cudaMemsetAsync(d->Y, 0, d->N * sizeof(double), s));
-  for (int l = 0; l <= L; ++l)
-    k_apply(d, l, d->lv[l].leaf_cells, d->lv[l].n_leaf, d->W + d->lv[l].off, d->Y + d->lv[l].off, s);
+  for (int l = 0; l <= L; ++l) {
+    // a level whose cells are all leaves (c3's finest) runs the family-patch
+    // operator over the whole level instead of the thread-per-cell list kernel
+    const DevLevel& v = d->lv[l];
+    const bool all = l > 0 && v.n_fam > 0 && v.n_leaf == v.n_cells;
+    k_apply(d, l, all ? nullptr : v.leaf_cells, all ? v.n_cells : v.n_leaf, d->W + v.off, d->Y + v.off, s);
+  }
   for (int l = L; l >= 1; --l) {
     export_add(d, l, d->Y + d->lv[l].off, s);
     k_restrict<dev::RES_EONLY, double>(d, l, d->lv[l].edge_fams, d->lv[l].n_edge, d->Y + d->lv[l].off, nullptr,
