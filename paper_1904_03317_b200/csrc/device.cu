@@ -176,6 +176,17 @@ static void allreduce(DeviceHierarchy* d, double* buf, int n, cudaStream_t s) {
 // grid of the four-entries-per-thread copy kernels (gather_to_mg / gather_from_mg)
 static int grid4(i64 n) { return (int)std::max<i64>(1, (n + 1023) / 1024); }
 
+// resident blocks of a fam_tensor_apply instantiation on the whole GPU (the
+// prefetch distance of its patch rows)
+template <int K, typename T, int TM>
+static int tensor_wave(DeviceHierarchy* d) {
+  static const int per_sm = [] {
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::fam_tensor_apply<K, T, TM>, 32 * dev::TG_WARPS, 0));
+    return std::max(nb, 1);
+  }();
+  return per_sm * d->sms;
+}
 template <int K>
 static int tensor_grid(i64 n_fam) {
   return (int)((n_fam + dev::TensorCfg<K>::FPB - 1) / dev::TensorCfg<K>::FPB);
@@ -210,7 +221,8 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* 
     } else {
       if (d->k == 2)
         dev::fam_tensor_apply<2, T><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y);
+            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y, 0, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0,
+            nullptr, tensor_wave<2, T, dev::TA_APPLY>(d));
       else
         dev::fam_tensor_apply<1, T><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
             (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y);
@@ -294,7 +306,8 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
     if (d->k == 2)
       dev::fam_tensor_apply<2, T, TM><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);
+          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc,
+          tensor_wave<2, T, TM>(d));
     else
       dev::fam_tensor_apply<1, T, TM><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
           (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(32 * TG_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr) {
+                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
@@ -373,6 +373,12 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
   const long f = (long)blockIdx.x * FPB + slot;
   const bool act = slot < FPB && f < nfam;
+  if (pf > 0) {   // the patch rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
+    const long fb = ((long)blockIdx.x + pf) * FPB;
+    const long bytes = (long)FPB * row * 4, off = (long)threadIdx.x * 128;
+    if (fb < nfam && off < bytes && fb * row * 4 + off < (long)nfam * row * 4)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(xfer + fb * (long)row) + off));
+  }
   const int* rp = xfer + (act ? f : 0) * (long)row;
   T* const a0 = s0 + (act ? slot : 0) * LY::sab;
   T* const a1 = s1 + (act ? slot : 0) * LY::sab;
