@@ -168,7 +168,12 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
  * E_l = D_l \ B_l on the closure of a leaf of level < l (refinement edge),
  * S_l = the rest (smoothed).  Level vectors hold the S u E DoFs in
  * global order (owner, Morton key of the node's finest-lattice coordinates);
- * owner of a node = min owner of the level cells having it as a node.
+ * owner of a level-l node (l >= 1) = min, over the level-l cells having it as a
+ * node, of the rank that computes the cell's family (the owner of the family's
+ * first child = its parent's owner under the first-child rule P:604; the
+ * family's rank under GMG_PARTITION_PER_LEVEL); every level-0 node is owned by
+ * rank 0 (coarse handoff).  P:519-521 leaves interface ownership open; this rule
+ * (reading R25) makes every owned DoF part of a family its owner computes.
  * Free leaf DoFs (non-hanging, non-Dirichlet) are numbered (owner, key) with
  * owner = the level owner at lambda(n) = max{ l : n in S_l }.
  */
@@ -179,6 +184,7 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
                                  fp64 interface (conversion at copy_to/from_mg) */
 #define GMG_LOCAL_RANKS 4u    /* all n_ranks ranks live in this process (one host thread and
                                  stream each, same GPU); params.nccl_comm is a gmg_local_world */
+#define GMG_HOST_RANKS 16u    /* ranks are processes joined by a gmg_host_world, passed as params.nccl_comm */
 
 /* ------------------------------------------------------------------ communicators
  * Multi-rank runs (one rank per GPU, "processor" = MPI rank): each rank
@@ -198,6 +204,18 @@ gmg_status gmg_nccl_comm_destroy(void *comm);
  * waits on another). */
 gmg_status gmg_local_world_create(int n_ranks, void **world);
 gmg_status gmg_local_world_destroy(void *world);
+/* Host-staged transport for ranks that are separate processes (the multi-process
+ * path on a machine with fewer GPUs than ranks, e.g. bench.py --transport host):
+ * every rank calls gmg_host_world_create with the same POSIX shared-memory name
+ * ("/..."), n_ranks and its rank (collective: returns once all ranks have
+ * attached); slot_bytes bounds one rank's packed send data per exchange (larger
+ * exchanges fail with GMG_E_OOM).  Exchanges copy device -> shared host memory ->
+ * device with host barriers between; kernels never wait on each other; the
+ * V-cycle is not graph-captured.  Pass the handle as params.nccl_comm with
+ * GMG_HOST_RANKS.  Destroy is collective; rank 0 unlinks the segment.
+ * Errors: INVALID_ARG, STATE (shm_open failed, a rank missing for 600 s), OOM. */
+gmg_status gmg_host_world_create(const char *name, int n_ranks, int rank, size_t slot_bytes, void **world);
+gmg_status gmg_host_world_destroy(void *world);
 
 typedef struct {
   int k;                    /* Q_k degree, 1 or 2 */
@@ -207,11 +225,25 @@ typedef struct {
   const double *coef_level2;/* host [#level-2 cells] coefficient per level-2 cell in SFC
                                order (config 4), NULL = constant 1 */
   int rank, n_ranks;        /* this process' rank; must equal the partition's n_ranks */
-  void *nccl_comm;          /* ncclComm_t for n_ranks > 1 (not yet used), else NULL */
+  void *nccl_comm;          /* n_ranks > 1: the communicator -- an ncclComm_t
+                               from gmg_nccl_comm_init, a gmg_local_world with
+                               GMG_LOCAL_RANKS or a gmg_host_world with GMG_HOST_RANKS;
+                               NULL for p = 1.  It
+                               must outlive the hierarchy. */
   int device;               /* CUDA device ordinal; -1 = current */
   uint32_t flags;           /* GMG_HOST_ONLY | GMG_NO_GRAPH | GMG_MIXED_PRECISION | ... */
   int coarse_solver;        /* GMG_COARSE_CHOLESKY (default: dense Cholesky of A_0^S, P:331-334,
                                reading R12) or GMG_COARSE_CHEBYSHEV (reading R28) */
+  /* Device allocator hooks; NULL = cudaMalloc / cudaFree.  Every
+   * device buffer of the hierarchy (level vectors, index tables, scratch) is
+   * obtained through dev_alloc at gmg_setup on the hierarchy's device and given
+   * back through dev_free at gmg_hierarchy_destroy, both called from the calling
+   * thread with stream = NULL (the legacy stream: setup synchronises).  dev_alloc
+   * returns NULL on failure (-> GMG_E_OOM).  The Python binding passes the torch
+   * caching allocator. */
+  void *(*dev_alloc)(size_t bytes, void *stream, void *ctx);
+  void (*dev_free)(void *ptr, size_t bytes, void *stream, void *ctx);
+  void *alloc_ctx;
 } gmg_params;
 
 #define GMG_COARSE_CHOLESKY 0
@@ -274,9 +306,15 @@ gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_ce
                                 int64_t *dofs);
 
 /* ------------------------------------------------------------------ hot path
- * All vectors below are DEVICE fp64 arrays.  "leaf vector": length n_owned in
- * the rank's global leaf order.  "level vector": length level_dofs[level] in
- * global level order.  p = 1 only in this version (n_ranks > 1 -> STATE). */
+ * All vectors below are DEVICE fp64 arrays on the hierarchy's device, caller
+ * owned, contiguous.  "leaf vector": length n_owned (gmg_info) in the rank's
+ * global leaf order; the collective calls (gmg_vcycle, gmg_solve_cg,
+ * gmg_rhs_constant, gmg_leaf_apply) are made by every rank with its own part.
+ * "level vector": length level_dofs[level] in global level order -- the
+ * single-operator entry points gmg_level_apply, gmg_restrict, gmg_prolongate,
+ * gmg_level_smooth, gmg_level_diagonal are defined for n_ranks == 1 only
+ * (GMG_E_STATE otherwise); gmg_level_apply_kernel(_f32) runs the rank-local
+ * kernel of any rank. */
 
 /* One V-cycle (P:318-327 with local smoothing P:413-469), x = V(b), x0 = 0:
  * Chebyshev-Jacobi pre/post smoothing of degree m on S rows, residual with the
@@ -293,12 +331,14 @@ gmg_status gmg_vcycle(gmg_hierarchy *h, const double *b_dev, double *x_dev, void
 gmg_status gmg_solve_cg(gmg_hierarchy *h, const double *b_dev, double *x_dev, double rtol,
                         int max_it, int *iters, double *rel_res, void *cuda_stream);
 
-/* b_i = int f phi_i for constant f on the free leaf DoFs (hanging-node
- * condensed), leaf vector. */
+/* b_i = int_Omega f phi_i for constant f on the free leaf DoFs (the weak form
+ * of P:140-147; hanging-node condensed), leaf vector.  Collective. */
 gmg_status gmg_rhs_constant(gmg_hierarchy *h, double f, double *b_dev, void *cuda_stream);
 
 /* Single-operator entry points (parity checks, ncu runs). */
-/* y = K_l x over all cells of C_l on S u E rows (edge rows included). */
+/* y = K_l x over all cells of C_l on S u E rows (edge rows included): the level
+ * matrix A_l of P:337-347 applied matrix-free cell by cell; on the
+ * E rows this is the edge matrix -A^{ES} part of P:459-469.  p = 1 only. */
 gmg_status gmg_level_apply(gmg_hierarchy *h, int level, const double *x_dev, double *y_dev,
                            void *cuda_stream);
 /* The level-operator kernel alone (no memset, no exchange): y must be zero on
@@ -312,19 +352,25 @@ gmg_status gmg_level_apply_kernel(gmg_hierarchy *h, int level, const double *x_d
  * GMG_MIXED_PRECISION): x_dev, y_dev are float arrays of the rank-local length. */
 gmg_status gmg_level_apply_kernel_f32(gmg_hierarchy *h, int level, const float *x_dev, float *y_dev,
                                       void *cuda_stream);
-/* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1) */
+/* d_coarse += P_l^T r_fine  (level >= 1; coarse = level-1): the restriction
+ * R = P^T of P:286-295, cell-wise on the families of level l.  p = 1 only. */
 gmg_status gmg_restrict(gmg_hierarchy *h, int level, const double *r_fine_dev,
                         double *d_coarse_dev, void *cuda_stream);
-/* x_fine += P_l x_coarse on all fine rows (level >= 1) */
+/* x_fine += P_l x_coarse on all fine rows (level >= 1): the prolongation
+ * (embedding of V_{l-1} into V_l).  p = 1 only. */
 gmg_status gmg_prolongate(gmg_hierarchy *h, int level, const double *x_coarse_dev,
                           double *x_fine_dev, void *cuda_stream);
-/* v = A_leaf u (hanging-node condensed leaf operator), leaf vectors */
+/* v = A_leaf u: the leaf-mesh operator with hanging nodes eliminated
+ * (P:403-407), leaf vectors (the CG operator of P:1039-1041).  Collective. */
 gmg_status gmg_leaf_apply(gmg_hierarchy *h, const double *u_dev, double *v_dev,
                           void *cuda_stream);
-/* x^S = Cheb(A^S, g^S - A^{SE} x^E, x^S) on one level (x_is_zero: start from 0) */
+/* x^S = Cheb(A^S, g^S - A^{SE} x^E, x^S) on one level (x_is_zero: start from 0):
+ * the Chebyshev-Jacobi smoother of P:882-887 on the local-smoothing block
+ * system of P:413-426.  p = 1 only. */
 gmg_status gmg_level_smooth(gmg_hierarchy *h, int level, const double *g_dev, double *x_dev,
                             int x_is_zero, void *cuda_stream);
-/* diagonal of A_l^S on S rows, 0 on E rows (level vector) */
+/* diagonal of A_l^S on S rows, 0 on E rows (level vector): the Jacobi part of
+ * the smoother.  p = 1 only. */
 gmg_status gmg_level_diagonal(gmg_hierarchy *h, int level, double *diag_dev, void *cuda_stream);
 
 /* lambda_bar of D^{-1} A_l^S; set overrides it (parity decoupling). */

@@ -371,8 +371,11 @@ def vcycle(h: Hierarchy, b: np.ndarray) -> np.ndarray:
 
 
 def pcg(h: Hierarchy, b: np.ndarray, rtol: float = 1e-8, maxit: int = 200, precond=None):
-    """CG on the leaf system, x0 = 0, stop at the first k with
-    ||b - A x_k|| <= rtol ||b|| (unpreconditioned)."""
+    """CG on the leaf system, x0 = 0, stop at the first k whose residual norm
+    ||r_k|| <= rtol ||b|| (unpreconditioned 2-norm).  r_k is CG's
+    recursively updated residual r_k = r_{k-1} - alpha A p, equal to b - A x_k in
+    exact arithmetic; the tests check the true residual of the returned x
+    separately."""
     A = h.A_leaf
     M = (lambda r: vcycle(h, r)) if precond is None else precond
     x = np.zeros_like(b)

@@ -17,8 +17,12 @@ Definitions (§2.3; notation of SURVEY.md §0):
 All nodes live on one integer lattice: local node a of cell (l, G) sits at
 X = (k G + a) 2^(L - l), L the finest level.  The canonical order of a set of
 nodes is the Morton order of X (x fastest, reading R10); the global
-(rank-aware) order sorts by (owner, Morton), owner = min owner of the cells
-that have the node as one of their nodes (S:173-like rule, SURVEY c.1 step 4).
+(rank-aware) order sorts by (owner, Morton).  Owner of a level-l node (DESIGN.md
+reading R25; PAPER.md:519-521 leaves the interface rule open): level 0 -> rank
+0 (coarse handoff); l >= 1 -> min over the level-l cells that have the node of
+the owner of the cell's PARENT, i.e. of the rank that computes the cell's
+family (first-child rule).  Pinned by hand-derived values and a
+brute-force evaluation in tests/test_oracle_r2_pins.py.
 """
 from __future__ import annotations
 

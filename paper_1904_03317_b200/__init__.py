@@ -45,6 +45,8 @@ GMG_CLOSE_BALANCE = 1
 GMG_HOST_ONLY = 1
 GMG_NO_GRAPH = 2
 GMG_MIXED_PRECISION = 8
+GMG_LOCAL_RANKS = 4
+GMG_HOST_RANKS = 16
 MAX_LEVELS = 64
 
 
@@ -77,11 +79,16 @@ class Model(C.Structure):
                 ("ghost_children", C.c_int64 * MAX_LEVELS), ("children", C.c_int64 * MAX_LEVELS)]
 
 
+DEV_ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+DEV_FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
 class Params(C.Structure):
     _fields_ = [("k", C.c_int), ("cheb_degree", C.c_int), ("cheb_lo", C.c_double), ("cheb_hi", C.c_double),
                 ("eig_iters", C.c_int), ("coef_level2", C.POINTER(C.c_double)), ("rank", C.c_int),
                 ("n_ranks", C.c_int), ("nccl_comm", C.c_void_p), ("device", C.c_int), ("flags", C.c_uint32),
-                ("coarse_solver", C.c_int)]
+                ("coarse_solver", C.c_int), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
+                ("alloc_ctx", C.c_void_p)]
 
 
 class Info(C.Structure):
@@ -142,8 +149,10 @@ _SIGS = {
     "gmg_nccl_comm_destroy": ([_vp], C.c_int),
     "gmg_local_world_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
     "gmg_local_world_destroy": ([_vp], C.c_int),
+    "gmg_host_world_create": ([C.c_char_p, C.c_int, C.c_int, C.c_size_t, C.POINTER(_vp)], C.c_int),
+    "gmg_host_world_destroy": ([_vp], C.c_int),
+    "gmg_leaf_layout": ([_vp, _i64p, _i64p, _i64p], C.c_int),
 }
-GMG_LOCAL_RANKS = 4
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -159,6 +168,26 @@ def _ptr(a):
     if isinstance(a, np.ndarray):
         return a.ctypes.data_as(_vp)
     return _vp(a.data_ptr())
+
+
+def _vec(t, n, what, dtype=None):
+    """Device-vector argument check (before any pointer crosses the ABI): a
+    contiguous CUDA tensor of the hot path's dtype (fp64 unless stated) with at
+    least n entries.  Raises GmgError(GMG_E_INVALID_ARG) instead of letting a
+    kernel read or write out of bounds."""
+    import torch
+    dtype = torch.float64 if dtype is None else dtype
+    if not isinstance(t, torch.Tensor):
+        raise GmgError(1, f"{what}: expected a torch CUDA tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise GmgError(1, f"{what}: tensor is on {t.device}, expected a CUDA device")
+    if t.dtype != dtype:
+        raise GmgError(1, f"{what}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise GmgError(1, f"{what}: tensor is not contiguous")
+    if t.numel() < n:
+        raise GmgError(1, f"{what}: {t.numel()} entries, expected {n}")
+    return _vp(t.data_ptr())
 
 
 def _stream(stream):
@@ -304,15 +333,34 @@ def gmg_params_default() -> Params:
 
 
 class Hierarchy:
-    def __init__(self, handle, part, coef=None):
+    """Owns a gmg_hierarchy.  Keeps the partition (and through it the forest),
+    the coefficient array, the communicator and the allocator callbacks alive
+    for as long as the hierarchy exists: the library holds raw pointers to them."""
+
+    def __init__(self, handle, part, coef=None, comm=None, alloc=None):
         self.h = handle
         self.part = part
         self._coef = coef
+        self.comm = comm
+        self._alloc = alloc
+        i = self.info()
+        self.n_owned = i["n_owned"]
+        self._dim, self._k = i["dim"], i["k"]
+        self._level_dofs = i["level_dofs"]
+        self._n_ranks = i["n_ranks"]
 
     def __del__(self):
         if getattr(self, "h", None):
             _lib.gmg_hierarchy_destroy(self.h)
             self.h = None
+
+    def close(self):
+        """Destroy the hierarchy now (collective for multi-rank hierarchies)."""
+        self.__del__()
+
+    def _local_len(self, level):
+        fo, no, gh = self.rank_level(level)
+        return no + len(gh)
 
     def info(self) -> dict:
         i = Info()
@@ -364,44 +412,52 @@ class Hierarchy:
 
     # ---------- hot path (device tensors)
     def vcycle(self, b, x, stream=None):
-        _check(_lib.gmg_vcycle(self.h, _ptr(b), _ptr(x), _stream(stream)))
+        _check(_lib.gmg_vcycle(self.h, _vec(b, self.n_owned, "b"), _vec(x, self.n_owned, "x"), _stream(stream)))
 
     def solve_cg(self, b, x, rtol=1e-8, max_it=200, stream=None, raise_on_fail=True):
         it = C.c_int()
         rel = C.c_double()
-        code = _lib.gmg_solve_cg(self.h, _ptr(b), _ptr(x), rtol, max_it, C.byref(it), C.byref(rel),
-                                 _stream(stream))
+        code = _lib.gmg_solve_cg(self.h, _vec(b, self.n_owned, "b"), _vec(x, self.n_owned, "x"), rtol, max_it,
+                                 C.byref(it), C.byref(rel), _stream(stream))
         if code != GMG_OK and (raise_on_fail or code != 9):
             _check(code)
         return it.value, rel.value, code
 
     def rhs_constant(self, f, b, stream=None):
-        _check(_lib.gmg_rhs_constant(self.h, f, _ptr(b), _stream(stream)))
+        _check(_lib.gmg_rhs_constant(self.h, f, _vec(b, self.n_owned, "b"), _stream(stream)))
 
     def level_apply(self, level, x, y, stream=None):
-        _check(_lib.gmg_level_apply(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
+        n = self._level_dofs[level]
+        _check(_lib.gmg_level_apply(self.h, level, _vec(x, n, "x"), _vec(y, n, "y"), _stream(stream)))
 
     def level_apply_kernel(self, level, x, y, stream=None):
         """Rank-local kernel only (timing); fp64 tensors, or fp32 tensors for the
         operator of the mixed-precision V-cycle."""
         import torch
-        fn = _lib.gmg_level_apply_kernel_f32 if x.dtype == torch.float32 else _lib.gmg_level_apply_kernel
-        _check(fn(self.h, level, _ptr(x), _ptr(y), _stream(stream)))
+        f32 = isinstance(x, torch.Tensor) and x.dtype == torch.float32
+        fn = _lib.gmg_level_apply_kernel_f32 if f32 else _lib.gmg_level_apply_kernel
+        n = self._local_len(level)
+        dt = torch.float32 if f32 else torch.float64
+        _check(fn(self.h, level, _vec(x, n, "x", dt), _vec(y, n, "y", dt), _stream(stream)))
 
     def restrict(self, level, r, dc, stream=None):
-        _check(_lib.gmg_restrict(self.h, level, _ptr(r), _ptr(dc), _stream(stream)))
+        _check(_lib.gmg_restrict(self.h, level, _vec(r, self._level_dofs[level], "r"),
+                                 _vec(dc, self._level_dofs[level - 1] if level >= 1 else 0, "dc"), _stream(stream)))
 
     def prolongate(self, level, xc, xf, stream=None):
-        _check(_lib.gmg_prolongate(self.h, level, _ptr(xc), _ptr(xf), _stream(stream)))
+        _check(_lib.gmg_prolongate(self.h, level, _vec(xc, self._level_dofs[level - 1] if level >= 1 else 0, "xc"),
+                                   _vec(xf, self._level_dofs[level], "xf"), _stream(stream)))
 
     def leaf_apply(self, u, v, stream=None):
-        _check(_lib.gmg_leaf_apply(self.h, _ptr(u), _ptr(v), _stream(stream)))
+        _check(_lib.gmg_leaf_apply(self.h, _vec(u, self.n_owned, "u"), _vec(v, self.n_owned, "v"), _stream(stream)))
 
     def level_smooth(self, level, g, x, x_is_zero, stream=None):
-        _check(_lib.gmg_level_smooth(self.h, level, _ptr(g), _ptr(x), int(bool(x_is_zero)), _stream(stream)))
+        n = self._level_dofs[level]
+        _check(_lib.gmg_level_smooth(self.h, level, _vec(g, n, "g"), _vec(x, n, "x"), int(bool(x_is_zero)),
+                                     _stream(stream)))
 
     def level_diagonal(self, level, diag, stream=None):
-        _check(_lib.gmg_level_diagonal(self.h, level, _ptr(diag), _stream(stream)))
+        _check(_lib.gmg_level_diagonal(self.h, level, _vec(diag, self._level_dofs[level], "diag"), _stream(stream)))
 
     def coarse_chebyshev(self):
         """(lambda_min, lambda_max, degree) of the Chebyshev coarse solver (degree 0: Cholesky)."""
@@ -442,6 +498,48 @@ class LocalWorld:
             self.h = None
 
 
+class HostWorld:
+    """Ranks as separate processes joined through POSIX shared memory
+    (gmg_host_world, host-staged exchanges; the multi-process path on a machine
+    with fewer GPUs than ranks).  Collective create and destroy."""
+
+    def __init__(self, name: str, n_ranks: int, rank: int, slot_bytes: int = 256 << 20):
+        self.h = _vp()
+        _check(_lib.gmg_host_world_create(name.encode(), n_ranks, rank, slot_bytes, C.byref(self.h)))
+        self.n, self.rank = n_ranks, rank
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            _check(_lib.gmg_host_world_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def torch_allocator(device: int | None = None):
+    """(dev_alloc, dev_free) ctypes callbacks over the torch caching allocator
+    (gmg_params.dev_alloc / dev_free).  Keep the returned pair alive as long as
+    the hierarchy (Hierarchy does)."""
+    import torch
+
+    dev = torch.cuda.current_device() if device is None or device < 0 else device
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), dev, 0)
+        except Exception:
+            return None
+
+    def _free(ptr, nbytes, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return DEV_ALLOC(_alloc), DEV_FREE(_free)
+
+
 def gmg_nccl_get_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.gmg_nccl_get_unique_id(buf))
@@ -461,8 +559,10 @@ class NcclComm:
 
 def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
               coef_level2=None, graph=True, device=-1, comm=None, mixed=False,
-              coarse="cholesky") -> Hierarchy:
-    """comm: None (one rank), a LocalWorld (ranks as threads) or an NcclComm."""
+              coarse="cholesky", allocator=None) -> Hierarchy:
+    """comm: None (one rank), a LocalWorld (ranks as threads), a HostWorld (ranks
+    as processes, host-staged) or an NcclComm.  allocator: None (cudaMalloc) or
+    "torch" (the torch caching allocator through gmg_params.dev_alloc/dev_free)."""
     p = gmg_params_default()
     p.k = k
     p.cheb_degree = cheb_degree
@@ -475,15 +575,24 @@ def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_deg
     if isinstance(comm, LocalWorld):
         p.flags |= GMG_LOCAL_RANKS
         p.nccl_comm = comm.h
+    elif isinstance(comm, HostWorld):
+        p.flags |= GMG_HOST_RANKS
+        p.nccl_comm = comm.h
     elif comm is not None:
         p.nccl_comm = comm.h
     coef = None
     if coef_level2 is not None:
         coef = np.ascontiguousarray(coef_level2, dtype=np.float64)
         p.coef_level2 = coef.ctypes.data_as(C.POINTER(C.c_double))
+    alloc = None
+    if allocator == "torch" and not host_only:
+        alloc = torch_allocator(device)
+        p.dev_alloc, p.dev_free = alloc
+    elif allocator not in (None, "cuda", "torch"):
+        raise ValueError(f"allocator {allocator!r}")
     h = _vp()
     _check(_lib.gmg_setup(forest.h, part.h, C.byref(p), C.byref(h)))
-    return Hierarchy(h, part, coef)
+    return Hierarchy(h, part, coef, comm=comm, alloc=alloc)
 
 
 def build_config(cfg: dict, n_ranks=1, host_only=False, passes=-1, **kw):

@@ -64,7 +64,7 @@ void need_level(const gmg_hierarchy* h, int level) {
 extern "C" {
 
 const char* gmg_last_error(void) { return g_err.c_str(); }
-int gmg_abi_version(void) { return 1; }
+int gmg_abi_version(void) { return 2; }
 
 gmg_status gmg_forest_create(int dim, int n_trees, const int32_t* tree_xyz, int64_t n_leaves,
                              const int32_t* leaf_tree, const int8_t* leaf_level, const uint64_t* leaf_morton,
@@ -205,6 +205,9 @@ void gmg_params_default(gmg_params* p) {
   p->device = -1;
   p->flags = 0;
   p->coarse_solver = GMG_COARSE_CHOLESKY;
+  p->dev_alloc = nullptr;
+  p->dev_free = nullptr;
+  p->alloc_ctx = nullptr;
 }
 
 gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_params* prm, gmg_hierarchy** out) {
@@ -230,7 +233,12 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
       std::unique_ptr<gmg::Comm> comm;
       if (prm->n_ranks > 1) {
         GMG_REQUIRE(prm->nccl_comm != nullptr, GMG_E_INVALID_ARG, "n_ranks > 1 needs a communicator");
-        if (prm->flags & GMG_LOCAL_RANKS) {
+        if (prm->flags & GMG_HOST_RANKS) {
+          auto* w = static_cast<gmg::HostWorld*>(prm->nccl_comm);
+          GMG_REQUIRE(w->n == prm->n_ranks && w->rank == prm->rank, GMG_E_INVALID_ARG,
+                      "host world rank/size != params");
+          comm = std::make_unique<gmg::HostComm>(w);
+        } else if (prm->flags & GMG_LOCAL_RANKS) {
           auto* w = static_cast<gmg::LocalWorld*>(prm->nccl_comm);
           GMG_REQUIRE(w->n == prm->n_ranks, GMG_E_INVALID_ARG, "local world size != n_ranks");
           comm = std::make_unique<gmg::ThreadComm>(w, prm->rank);
@@ -288,9 +296,10 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
       o->level_B[l] = t.nB;
       o->level_leaf_cells[l] = (gmg::i64)t.leaf_cells.size();
       o->level_r1[l] = h->dev ? gmg::device_level_r1(h->dev, l) : 0;
-      mg += (t.n_dofs + 511) / 512 * 512;   // device segment padding (kernels.cuh VEC_PAD)
+      // this rank's level vector (owned + ghosts), padded like the device segments (kernels.cuh VEC_PAD)
+      mg += (h->local.lv[l].n_local() + 511) / 512 * 512;
     }
-    o->mg_vector_len = mg;
+    o->mg_vector_len = h->dev ? gmg::device_mg_len(h->dev) : mg;
   });
 }
 
@@ -371,6 +380,18 @@ gmg_status gmg_local_world_create(int n_ranks, void** world) {
 
 gmg_status gmg_local_world_destroy(void* world) {
   return guard([&] { delete static_cast<gmg::LocalWorld*>(world); });
+}
+
+gmg_status gmg_host_world_create(const char* name, int n_ranks, int rank, size_t slot_bytes, void** world) {
+  return guard([&] {
+    NEED(name);
+    NEED(world);
+    *world = new gmg::HostWorld(name, n_ranks, rank, slot_bytes);
+  });
+}
+
+gmg_status gmg_host_world_destroy(void* world) {
+  return guard([&] { delete static_cast<gmg::HostWorld*>(world); });
 }
 
 gmg_status gmg_export_cell_dofs(const gmg_hierarchy* h, int level, int64_t* n_cells, int64_t* dofs) {

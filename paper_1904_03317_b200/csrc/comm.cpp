@@ -2,6 +2,15 @@
 #include "comm.hpp"
 
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <cerrno>
+#include <chrono>
 
 #include <cstdlib>
 #include <string>
@@ -81,6 +90,105 @@ void ThreadComm::allreduce(double* buf, int n, cudaStream_t s) {
   w->barrier();
   for (int i = 0; i < n; ++i) me.red[i] = sum[i];
   CKC(cudaMemcpyAsync(buf, me.red, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CKC(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------- processes (shared memory)
+namespace {
+struct ShmHdr {                       // zero-initialised by ftruncate: a valid initial state
+  std::atomic<long long> arrived;
+  std::atomic<long long> generation;
+};
+}  // namespace
+
+HostWorld::HostWorld(const char* nm, int n_, int r, size_t slot) : n(n_), rank(r), name(nm) {
+  GMG_REQUIRE(n_ >= 1 && r >= 0 && r < n_, GMG_E_INVALID_ARG, "host world rank/size");
+  GMG_REQUIRE(nm && nm[0] == '/', GMG_E_INVALID_ARG, "host world name must start with '/'");
+  slot_bytes = (std::max<size_t>(slot, 1 << 16) + 4095) / 4096 * 4096;
+  total = 4096 + slot_bytes * (size_t)n_;
+  const int fd = shm_open(nm, O_CREAT | O_RDWR, 0600);
+  GMG_REQUIRE(fd >= 0, GMG_E_STATE, std::string("shm_open ") + nm + ": " + std::strerror(errno));
+  struct stat st;
+  if (fstat(fd, &st) == 0 && (size_t)st.st_size < total && ftruncate(fd, (off_t)total) != 0) {
+    close(fd);
+    fail(GMG_E_OOM, std::string("ftruncate of the host world: ") + std::strerror(errno));
+  }
+  void* m = mmap(nullptr, total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  GMG_REQUIRE(m != MAP_FAILED, GMG_E_OOM, std::string("mmap of the host world: ") + std::strerror(errno));
+  base = (unsigned char*)m;
+  registered = cudaHostRegister(base, total, cudaHostRegisterDefault) == cudaSuccess;
+  if (!registered) cudaGetLastError();   // fall back to pageable copies
+  barrier();                             // every rank has mapped the segment
+}
+
+HostWorld::~HostWorld() {
+  if (!base) return;
+  try {
+    barrier();                           // nobody still reads a slot
+  } catch (...) {
+  }
+  if (registered) cudaHostUnregister(base);
+  munmap(base, total);
+  if (rank == 0) shm_unlink(name.c_str());
+}
+
+void HostWorld::barrier() {
+  auto* h = (ShmHdr*)base;
+  const long long gen = h->generation.load(std::memory_order_acquire);
+  if (h->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == n) {
+    h->arrived.store(0, std::memory_order_relaxed);
+    h->generation.fetch_add(1, std::memory_order_release);
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  long spins = 0;
+  while (h->generation.load(std::memory_order_acquire) == gen) {
+    if (++spins > 1000) {
+      sched_yield();
+      if ((spins & 0xffff) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+        fail(GMG_E_STATE, "host world barrier: a rank did not arrive within 600 s");
+    }
+  }
+}
+
+void HostComm::exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
+                        double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) {
+  const int me = w->rank;
+  i64* dir = w->dir(me);
+  for (int q = 0; q < w->n; ++q) dir[2 * q] = dir[2 * q + 1] = 0;
+  const i64 ns = soff.empty() ? 0 : soff.back();
+  GMG_REQUIRE((size_t)ns <= w->payload_cap(), GMG_E_OOM, "host world slot too small for an exchange");
+  for (size_t i = 0; i < peers.size(); ++i) {
+    dir[2 * peers[i]] = soff[i];
+    dir[2 * peers[i] + 1] = soff[i + 1] - soff[i];
+  }
+  if (ns) CKC(cudaMemcpyAsync(w->payload(me), sendbuf, ns * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  w->barrier();                       // every slot is written
+  for (size_t i = 0; i < peers.size(); ++i) {
+    const int q = peers[i];
+    const i64* od = w->dir(q);
+    const i64 cnt = od[2 * me + 1];
+    GMG_REQUIRE(cnt == roff[i + 1] - roff[i], GMG_E_STATE, "exchange count mismatch");
+    if (cnt)
+      CKC(cudaMemcpyAsync(recvbuf + roff[i], w->payload(q) + od[2 * me], cnt * sizeof(double),
+                          cudaMemcpyHostToDevice, s));
+  }
+  CKC(cudaStreamSynchronize(s));
+  w->barrier();                       // every slot is read: it may be rewritten
+}
+
+void HostComm::allreduce(double* buf, int cnt, cudaStream_t s) {
+  GMG_REQUIRE((size_t)cnt <= w->payload_cap(), GMG_E_INVALID_ARG, "allreduce size");
+  CKC(cudaMemcpyAsync(w->payload(w->rank), buf, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  w->barrier();
+  std::vector<double> sum(cnt, 0.0);
+  for (int q = 0; q < w->n; ++q)      // same order on every rank: identical sums
+    for (int i = 0; i < cnt; ++i) sum[i] += w->payload(q)[i];
+  w->barrier();
+  CKC(cudaMemcpyAsync(buf, sum.data(), cnt * sizeof(double), cudaMemcpyHostToDevice, s));
   CKC(cudaStreamSynchronize(s));
 }
 

@@ -12,6 +12,7 @@
 
 #include <condition_variable>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.hpp"
@@ -57,6 +58,40 @@ struct ThreadComm : Comm {
   LocalWorld* w;
   int r;
   int rank() const override { return r; }
+  int size() const override { return w->n; }
+  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
+                const std::vector<i64>& roff, cudaStream_t s) override;
+  void allreduce(double* buf, int n, cudaStream_t s) override;
+  bool capturable() const override { return false; }
+};
+
+// ---------------------------------------------------------------- processes, host-staged
+// n ranks as separate processes (any GPUs, e.g. all on one device): a POSIX
+// shared-memory segment holds a sense-free generation barrier and one slot per
+// rank; an exchange is D2H of the packed send buffer into the own slot (the
+// segment is cudaHostRegister'ed), a barrier, H2D of every peer's chunk from the
+// peer's slot, a stream synchronise and a second barrier.  Kernels never wait on
+// each other; not capturable.  A test transport for the multi-process path on a
+// one-GPU machine (bench.py --transport host), not a performance path.
+struct HostWorld {
+  HostWorld(const char* name, int n, int rank, size_t slot_bytes);
+  ~HostWorld();
+  int n, rank;
+  size_t slot_bytes = 0, total = 0;
+  std::string name;
+  unsigned char* base = nullptr;
+  bool registered = false;
+  void barrier();
+  // slot q: [directory: n x (offset, count) as i64][payload doubles]
+  i64* dir(int q) const { return (i64*)(base + 4096 + (size_t)q * slot_bytes); }
+  double* payload(int q) const { return (double*)(base + 4096 + (size_t)q * slot_bytes + 16 * (size_t)n); }
+  size_t payload_cap() const { return (slot_bytes - 16 * (size_t)n) / sizeof(double); }
+};
+
+struct HostComm : Comm {
+  explicit HostComm(HostWorld* w) : w(w) {}
+  HostWorld* w;
+  int rank() const override { return w->rank; }
   int size() const override { return w->n; }
   void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
                 const std::vector<i64>& roff, cudaStream_t s) override;

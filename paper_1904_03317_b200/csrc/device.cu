@@ -39,6 +39,7 @@ struct DevLevel {
   int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam], only for the cell-form family apply (fam_apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   i64 n_r1 = 0;                     // device order (plan.hpp): rows [0, n_r1) finished by the fused apply
+  bool fuse_pro = false;            // prolongation fused into the first post-smoothing step on EVERY rank
   int* perm = nullptr;              // rank-local level index -> device index (API boundary)
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
@@ -85,7 +86,11 @@ struct DeviceHierarchy {
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;
+  // caller's allocator hooks (gmg_params.dev_alloc / dev_free), else cudaMalloc / cudaFree
+  void* (*dev_alloc)(size_t, void*, void*) = nullptr;
+  void (*dev_free)(void*, size_t, void*, void*) = nullptr;
+  void* alloc_ctx = nullptr;
   int sms = 148;
   std::unique_ptr<Comm> comm;
 
@@ -93,9 +98,15 @@ struct DeviceHierarchy {
   T_* alloc(size_t n) {
     void* p = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(&p, n * sizeof(T_));
-    if (e != cudaSuccess) fail(GMG_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    allocs.push_back(p);
+    const size_t bytes = n * sizeof(T_);
+    if (dev_alloc) {
+      p = dev_alloc(bytes, nullptr, alloc_ctx);
+      if (!p) fail(GMG_E_OOM, "dev_alloc returned NULL for " + std::to_string(bytes) + " bytes");
+    } else {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) fail(GMG_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    allocs.emplace_back(p, bytes);
     return (T_*)p;
   }
   template <class T_>
@@ -370,13 +381,16 @@ static void coarse(DeviceHierarchy* d, T* d0, T* x0, T* t0, T* dv0, cudaStream_t
 
 // The prolongation can ride on the first post-smoothing step where that step runs
 // the fused operator kernel (R1 present, degree >= 2; GMG_FUSE_PROLONG=0 turns
-// it off for comparison).
+// it off for comparison).  The decision is collective (fuse_pro, set at setup):
+// the fused path imports x_l before adding P x_{l-1} (every rank adds it to its
+// ghosts itself), the separate path after, so ranks choosing differently would
+// exchange inconsistent ghost values.
 static bool prolong_fusable(DeviceHierarchy* d, int l) {
   static const bool on = [] {
     const char* e = std::getenv("GMG_FUSE_PROLONG");
     return !(e && e[0] == '0');
   }();
-  return on && d->lv[l].n_r1 > 0 && d->lv[l].c1.size() > 1;
+  return on && d->lv[l].fuse_pro && d->lv[l].c1.size() > 1;
 }
 
 // The V-cycle on the MG-layout buffers D (defects, copy_to_mg done), X (out).
@@ -631,6 +645,11 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     CK(cudaGetDevice(&dev_id));
     CK(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, dev_id));
     d->comm = std::move(comm);
+    GMG_REQUIRE((prm.dev_alloc == nullptr) == (prm.dev_free == nullptr), GMG_E_INVALID_ARG,
+                "dev_alloc and dev_free must be given together");
+    d->dev_alloc = prm.dev_alloc;
+    d->dev_free = prm.dev_free;
+    d->alloc_ctx = prm.alloc_ctx;
     d->dim = Tp.dim;
     d->k = Tp.k;
     d->L = Tp.L;
@@ -817,6 +836,18 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       d->lv[l].lam = eigen_estimate(d, l, s);
       set_cheb(d, l);
     }
+    // prolongation fusion per level, collectively: every rank has R1 rows there
+    {
+      const int nl = Tp.L + 1;
+      GMG_REQUIRE(nl <= 64 && nl <= d->nred, GMG_E_INVALID_ARG, "too many levels");
+      std::vector<double> miss(nl);
+      for (int l = 0; l < nl; ++l) miss[l] = d->lv[l].n_r1 > 0 ? 0.0 : 1.0;
+      CK(cudaMemcpyAsync(d->partial, miss.data(), nl * sizeof(double), cudaMemcpyHostToDevice, s));
+      allreduce(d, d->partial, nl, s);
+      CK(cudaMemcpyAsync(miss.data(), d->partial, nl * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int l = 0; l < nl; ++l) d->lv[l].fuse_pro = l > 0 && miss[l] == 0.0;
+    }
     if (d->coarse_cheb) {
       DevLevel& v0 = d->lv[0];
       lanczos_range(d, 0, (int)std::max<i64>(v0.nS_global, 1), 1e-3, &d->coarse_lo, &d->coarse_hi, s);
@@ -846,6 +877,8 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
   return d;
 }
 
+long long device_mg_len(const DeviceHierarchy* d) { return d ? (long long)d->N : 0; }
+
 long long device_level_r1(const DeviceHierarchy* d, int level) {
   return d && level >= 0 && level < (int)d->lv.size() ? (long long)d->lv[level].n_r1 : 0;
 }
@@ -854,7 +887,10 @@ void device_destroy(DeviceHierarchy* d) {
   if (!d) return;
   cudaDeviceSynchronize();
   if (d->vgraph) cudaGraphExecDestroy(d->vgraph);
-  for (void* p : d->allocs) cudaFree(p);
+  for (auto& a : d->allocs) {
+    if (d->dev_free) d->dev_free(a.first, a.second, nullptr, d->alloc_ctx);
+    else cudaFree(a.first);
+  }
   if (d->hscal) cudaFreeHost(d->hscal);
   if (d->cap) cudaStreamDestroy(d->cap);
   delete d;

@@ -31,6 +31,7 @@ double device_get_eigen(const DeviceHierarchy* d, int level);
 void device_coarse_chebyshev(const DeviceHierarchy* d, double* lo, double* hi, int* degree);
 void device_set_eigen(DeviceHierarchy* d, int level, double lam);
 long long device_launches(const DeviceHierarchy* d);
+long long device_mg_len(const DeviceHierarchy* d);
 long long device_level_r1(const DeviceHierarchy* d, int level);
 void device_launch_profile(const DeviceHierarchy* d, long long* per_vcycle, long long* per_leaf_apply);
 

@@ -33,8 +33,11 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     for (i64 g = 0; g < t.n_dofs; ++g) start[l][t.dof_owner[g] + 1]++;
     for (int q = 0; q < P; ++q) start[l][q + 1] += start[l][q];
   }
-  // the rank computing a family = the owner of its cells (all 2^d children share it; under
-  // the first-child rule this is the parent's owner)
+  // the rank computing a family = the owner of its first child: under the first-child
+  // rule the parent's owner; the other children may be owned elsewhere (ghost
+  // children) and are still computed here.  Under per-level partitioning
+  // (R29) families are kept whole and this is the family's rank.  Executed per-rank
+  // work therefore follows family owners, not the cell owners the N_{l,p} model counts.
   auto fam_owner = [&](int l, i64 fi) { return p.levels[l].owner[fi * nch]; };
   // ---------------- ghost sets of every rank (needed DoFs owned elsewhere)
   std::vector<std::vector<std::vector<i64>>> ghosts(L + 1, std::vector<std::vector<i64>>(P));

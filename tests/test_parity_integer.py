@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in sorted(decl) if not hasattr(lib, s)]
     assert not missing, missing
     assert set(G.EXPORTED) <= decl
-    assert lib.gmg_abi_version() == 1
+    assert lib.gmg_abi_version() == 2
 
 
 # ------------------------------------------------------------------ helpers
