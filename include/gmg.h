@@ -113,6 +113,11 @@ gmg_status gmg_forest_sequence(int dim, gmg_sequence kind, int L, gmg_forest **o
 gmg_status gmg_forest_destroy(gmg_forest *f);
 gmg_status gmg_forest_info(const gmg_forest *f, int *dim, int *n_trees, int64_t *n_leaves,
                            int *max_level);
+/* Number of distinct Q_k nodes of the leaves (hanging and Dirichlet nodes
+ * included: the "DoFs" of the configs, reading R22) without building the level
+ * topology (slab-wise key counting, bounded memory) -- sizes the config-5
+ * weak-scaling forests.  Errors: INVALID_ARG (k outside 1..4), DEPTH. */
+gmg_status gmg_forest_count_nodes(const gmg_forest *f, int k, int64_t *n_nodes);
 /* host arrays [n_leaves] (any may be NULL) */
 gmg_status gmg_export_leaves(const gmg_forest *f, int32_t *leaf_tree, int8_t *leaf_level,
                              uint64_t *leaf_morton);
@@ -379,6 +384,46 @@ gmg_status gmg_get_eigen(const gmg_hierarchy *h, int level, double *lambda_bar);
  * a priori degree (0 with the Cholesky coarse solver). */
 gmg_status gmg_get_coarse_chebyshev(const gmg_hierarchy *h, double *lo, double *hi, int *degree);
 gmg_status gmg_set_eigen(gmg_hierarchy *h, int level, double lambda_bar);
+
+/* Launch profiler (measurement): runs n_rep V-cycles x = V(b) eagerly
+ * (no CUDA graph; same kernels and arguments as the captured cycle) with every
+ * launch bracketed by CUDA events on cuda_stream, and aggregates per (kind,
+ * level): number of launches, summed kernel seconds, and the kernel's
+ * algorithmic bytes per launch (DESIGN.md §6 definitions: the level operator
+ * counts 2 vectors per level DoF + (k+1)^d int32 per cell; the fused
+ * Chebyshev kinds add the R1 rows' vectors; transfers count their vectors, the
+ * family's transfer row and the coarse read-modify-write) and the same with the
+ * index layout the kernel actually reads (bytes_layout).  Exchanges (GMG_K_EXCHANGE)
+ * include the transport.  Writes min(count, max_out) records to out and the
+ * number of distinct records to *n_out; synchronises the stream.  Collective. */
+typedef enum {
+  GMG_K_APPLY = 0,          /* fam_tensor_apply / cell kernels, plain y = K_l x */
+  GMG_K_CHEB_X1 = 1,        /* fused operator + Chebyshev step 1 after the start from 0 */
+  GMG_K_CHEB_11 = 2,        /* fused, middle steps (read and write dv) */
+  GMG_K_CHEB_10 = 3,        /* fused, last step (read dv) */
+  GMG_K_CHEB_01 = 4,        /* fused, first post-smoothing step without prolongation */
+  GMG_K_CHEB_00 = 5,        /* fused, degree 1 */
+  GMG_K_CHEB_P01 = 6,       /* fused, first post-smoothing step with x += P x_{l-1} */
+  GMG_K_CHEB_STREAM = 7,    /* streaming Chebyshev rows outside R1 (cheb_range) */
+  GMG_K_CHEB_STREAM_FULL = 8, /* streaming Chebyshev over a whole level (cheb_step) */
+  GMG_K_RESTRICT = 9,
+  GMG_K_PROLONGATE = 10,
+  GMG_K_COARSE = 11,
+  GMG_K_EXCHANGE = 12,
+  GMG_K_COPY_MG = 13,       /* copy_to_mg / copy_from_mg */
+  GMG_K_LEAF_APPLY = 14,
+  GMG_K_OTHER = 15
+} gmg_kernel_kind;
+typedef struct {
+  int kind;                 /* gmg_kernel_kind */
+  int level;                /* -1 for whole-vector kernels */
+  int64_t launches;
+  double seconds;           /* summed over the launches */
+  double bytes;             /* algorithmic bytes per launch */
+  double bytes_layout;      /* bytes per launch with the index layout actually read */
+} gmg_kernel_stat;
+gmg_status gmg_profile_vcycle(gmg_hierarchy *h, const double *b_dev, double *x_dev, int n_rep,
+                              gmg_kernel_stat *out, int max_out, int *n_out, void *cuda_stream);
 
 /* Kernel launches issued by the library since creation (evidence counter). */
 gmg_status gmg_launch_count(const gmg_hierarchy *h, int64_t *count);

@@ -43,6 +43,7 @@ import scipy.linalg as sla
 import scipy.sparse as sp
 
 from . import fem
+from .spmv import mv
 from .forest import Forest
 from .partition import level_cells, leaf_owners, LevelCells
 from .spaces import Lattice, LevelSpace, LeafSpace, level_space, leaf_space, leaf_level_sets, S_CLASS, E_CLASS
@@ -277,7 +278,7 @@ def chebyshev_range(lev: Level, g: np.ndarray, lam_lo: float, lam_hi: float, deg
     for j in range(degree):
         x = x + dvec
         if j < degree - 1:
-            r = r - Dinv * (A @ dvec)
+            r = r - Dinv * mv(A, dvec)
             rho_new = 1.0 / (2.0 * sigma - rho)
             dvec = rho_new * rho * dvec + (2.0 * rho_new / delta) * r
             rho = rho_new
@@ -303,13 +304,13 @@ def chebyshev(lev: Level, g: np.ndarray, x0: np.ndarray | None, degree: int) -> 
         r = Dinv * g
     else:
         x = x0.copy()
-        r = Dinv * (g - A @ x)
+        r = Dinv * (g - mv(A, x))
     rho = 1.0 / sigma
     dvec = r / theta
     for j in range(degree):
         x = x + dvec
         if j < degree - 1:
-            r = r - Dinv * (A @ dvec)
+            r = r - Dinv * mv(A, dvec)
             rho_new = 1.0 / (2.0 * sigma - rho)
             dvec = rho_new * rho * dvec + (2.0 * rho_new / delta) * r
             rho = rho_new
@@ -339,7 +340,7 @@ def vcycle_levels(h: Hierarchy, d: list) -> list:
             return
         xl = chebyshev(lev, d[l], None, h.degree)                    # 1
         SE = lev.S | lev.E
-        r = np.where(SE, d[l] - lev.K @ xl, 0.0)                     # 2
+        r = np.where(SE, d[l] - mv(lev.K, xl), 0.0)                  # 2
         d[l - 1] = d[l - 1] + lev.P.T @ r                            # 3
         V(l - 1)                                                     # 4
         xl = xl + np.where(SE, lev.P @ x[l - 1], 0.0)                # 5
@@ -388,7 +389,7 @@ def pcg(h: Hierarchy, b: np.ndarray, rtol: float = 1e-8, maxit: int = 200, preco
     p = z.copy()
     rz = float(r @ z)
     for it in range(1, maxit + 1):
-        q = A @ p
+        q = mv(A, p)
         alpha = rz / float(p @ q)
         x = x + alpha * p
         r = r - alpha * q

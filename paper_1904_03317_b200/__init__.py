@@ -102,6 +102,14 @@ class Info(C.Structure):
                 ("level_r1", C.c_int64 * MAX_LEVELS)]
 
 
+class KernelStat(C.Structure):
+    _fields_ = [("kind", C.c_int), ("level", C.c_int), ("launches", C.c_int64), ("seconds", C.c_double),
+                ("bytes", C.c_double), ("bytes_layout", C.c_double)]
+
+
+KERNEL_KINDS = ["apply", "cheb_x1", "cheb_11", "cheb_10", "cheb_01", "cheb_00", "cheb_p01", "cheb_stream",
+                "cheb_stream_full", "restrict", "prolongate", "coarse", "exchange", "copy_mg", "leaf_apply", "other"]
+
 _vp = C.c_void_p
 _i64p = C.POINTER(C.c_int64)
 _SIGS = {
@@ -152,6 +160,9 @@ _SIGS = {
     "gmg_host_world_create": ([C.c_char_p, C.c_int, C.c_int, C.c_size_t, C.POINTER(_vp)], C.c_int),
     "gmg_host_world_destroy": ([_vp], C.c_int),
     "gmg_leaf_layout": ([_vp, _i64p, _i64p, _i64p], C.c_int),
+    "gmg_forest_count_nodes": ([_vp, C.c_int, _i64p], C.c_int),
+    "gmg_profile_vcycle": ([_vp, _vp, _vp, C.c_int, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int), _vp],
+                           C.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -243,6 +254,12 @@ class Forest:
         d, t, n, L = C.c_int(), C.c_int(), C.c_int64(), C.c_int()
         _check(_lib.gmg_forest_info(self.h, C.byref(d), C.byref(t), C.byref(n), C.byref(L)))
         return dict(dim=d.value, n_trees=t.value, n_leaves=n.value, max_level=L.value)
+
+    def count_nodes(self, k):
+        """All leaf nodes of degree k (R22), without the level topology."""
+        n = C.c_int64()
+        _check(_lib.gmg_forest_count_nodes(self.h, k, C.byref(n)))
+        return n.value
 
     def leaves(self):
         n = self.info()["n_leaves"]
@@ -472,6 +489,18 @@ class Hierarchy:
 
     def set_eigen(self, level, lam):
         _check(_lib.gmg_set_eigen(self.h, level, float(lam)))
+
+    def profile_vcycle(self, b, x, n_rep=3, stream=None):
+        """Per (kernel kind, level) launch statistics of n_rep eager V-cycles
+        (gmg_profile_vcycle): dicts with kind, level, launches, seconds (summed),
+        bytes and bytes_layout per launch."""
+        cap = 4096
+        arr = (KernelStat * cap)()
+        n = C.c_int()
+        _check(_lib.gmg_profile_vcycle(self.h, _vec(b, self.n_owned, "b"), _vec(x, self.n_owned, "x"), int(n_rep),
+                                       arr, cap, C.byref(n), _stream(stream)))
+        return [dict(kind=KERNEL_KINDS[a.kind], level=a.level, launches=a.launches, seconds=a.seconds,
+                     bytes=a.bytes, bytes_layout=a.bytes_layout) for a in arr[:min(n.value, cap)]]
 
     def launch_count(self):
         v = C.c_int64()

@@ -382,6 +382,27 @@ gmg_status gmg_local_world_destroy(void* world) {
   return guard([&] { delete static_cast<gmg::LocalWorld*>(world); });
 }
 
+gmg_status gmg_forest_count_nodes(const gmg_forest* f, int k, int64_t* n_nodes) {
+  return guard([&] {
+    NEED(f);
+    NEED(n_nodes);
+    *n_nodes = gmg::count_leaf_nodes(f->f, k);
+  });
+}
+
+gmg_status gmg_profile_vcycle(gmg_hierarchy* h, const double* b, double* x, int n_rep, gmg_kernel_stat* out,
+                              int max_out, int* n_out, void* stream) {
+  return guard([&] {
+    NEED(h);
+    NEED(b);
+    NEED(x);
+    GMG_REQUIRE(n_rep >= 1 && max_out >= 0 && (out || max_out == 0), GMG_E_INVALID_ARG, "profile arguments");
+    GMG_REQUIRE(h->dev != nullptr, GMG_E_STATE, "hierarchy has no device data (GMG_HOST_ONLY)");
+    const int n = gmg::device_profile_vcycle(h->dev, b, x, n_rep, out, max_out, stream);
+    if (n_out) *n_out = n;
+  });
+}
+
 gmg_status gmg_host_world_create(const char* name, int n_ranks, int rank, size_t slot_bytes, void** world) {
   return guard([&] {
     NEED(name);

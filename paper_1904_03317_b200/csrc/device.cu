@@ -93,6 +93,24 @@ struct DeviceHierarchy {
   void* alloc_ctx = nullptr;
   int sms = 148;
   std::unique_ptr<Comm> comm;
+  // kernel profiler (gmg_profile_vcycle): when set, every launch site of the
+  // V-cycle brackets its kernel with two events on the launching stream
+  struct ProfRec {
+    int kind, level;
+    double bytes, bytes_layout;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec>* prof = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  cudaEvent_t ev() {
+    if (evnext == evpool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) fail(GMG_E_CUDA, "cudaEventCreate");
+      evpool.push_back(e);
+    }
+    return evpool[evnext++];
+  }
 
   template <class T_>
   T_* alloc(size_t n) {
@@ -131,6 +149,33 @@ struct DeviceHierarchy {
     else { constexpr int D_ = 3, K_ = 2; __VA_ARGS__; }             \
   } while (0)
 
+// ---------------------------------------------------------------- launch profiler
+// One record per bracketed launch: kind (gmg.h GMG_K_*), level, the kernel's
+// algorithmic bytes per launch (DESIGN.md §6 definitions) and the bytes of the
+// index layout it actually reads.
+struct Prof {
+  DeviceHierarchy* d;
+  cudaStream_t s;
+  int kind, level;
+  double bytes, layout;
+  cudaEvent_t a = nullptr;
+  Prof(DeviceHierarchy* d_, cudaStream_t s_, int kind_, int level_, double bytes_, double layout_ = -1)
+      : d(d_), s(s_), kind(kind_), level(level_), bytes(bytes_), layout(layout_ < 0 ? bytes_ : layout_) {
+    if (d->prof) {
+      a = d->ev();
+      CK(cudaEventRecord(a, s));
+    }
+  }
+  void end() {
+    if (d->prof && a) {
+      cudaEvent_t b = d->ev();
+      if (cudaEventRecord(b, s) == cudaSuccess) d->prof->push_back({kind, level, bytes, layout, a, b});
+    }
+    a = nullptr;
+  }
+  ~Prof() { end(); }
+};
+
 // ---------------------------------------------------------------- V-cycle buffers by precision
 template <typename T> struct MG;
 template <> struct MG<double> {
@@ -154,6 +199,7 @@ template <typename T>
 static void import_ghosts(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
+  Prof pr(d, s, GMG_K_EXCHANGE, l, (double)(v.n_send + v.n_recv) * (sizeof(T) + 4 + 8));
   if (v.n_send) {
     dev::pack<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, d->sbuf);
     d->launches++;
@@ -169,6 +215,7 @@ template <typename T>
 static void export_add(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
+  Prof pr(d, s, GMG_K_EXCHANGE, l, (double)(v.n_send + v.n_recv) * (2 * sizeof(T) + 4 + 8));
   if (v.n_recv) {
     dev::pack_zero<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, d->sbuf);
     d->launches++;
@@ -207,11 +254,27 @@ static int tensor_grid(i64 n_fam) {
 // cells.  Full levels >= 1 run family-blocked (y must be zero on entry:
 // patch-interior nodes are stored, not added); level 0 and cell lists run
 // thread-per-cell.
+static int nn_of(const DeviceHierarchy* d) { return d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1); }
+static int np_of(const DeviceHierarchy* d) {
+  return d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
+}
+// level operator: x read + y written per level DoF, (k+1)^d index entries
+// per cell; layout: the (2k+1)^d patch row per family the tensor kernel reads instead
+static double apply_bytes(const DeviceHierarchy* d, const DevLevel& v, size_t vb) {
+  return 2.0 * vb * (double)v.n + 4.0 * nn_of(d) * (double)v.n_cells;
+}
+static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t vb) {
+  return 2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam;
+}
+
 template <typename T>
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* x, T* y, cudaStream_t s) {
   if (n == 0) return;
   DevLevel& v = d->lv[l];
   const bool full = list == nullptr && l > 0 && v.n_fam > 0;
+  Prof pr(d, s, full || list == nullptr ? GMG_K_APPLY : GMG_K_LEAF_APPLY, l,
+          list == nullptr ? apply_bytes(d, v, sizeof(T)) : (2.0 * sizeof(T) + 4.0) * nn_of(d) * (double)n,
+          list == nullptr && full ? apply_layout(d, v, sizeof(T)) : -1.0);
   if (v.elem) {                                   // config 4, levels 0-1: explicit element matrices
     const int nt = 128;
     const int nn = d->dim == 3 ? (d->k + 1) * (d->k + 1) * (d->k + 1) : (d->k + 1) * (d->k + 1);
@@ -277,6 +340,12 @@ static void k_restrict(DeviceHierarchy* d, int l, const int* list, i64 nf, const
                        cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
+  // r = d - t read (two vectors, MODE RES_VCYCLE; one otherwise) and t reset per fine
+  // row, the family's xfer row, d_{l-1} read-modify-written per coarse row
+  const double fine_vecs = MODE == dev::RES_VCYCLE ? 3.0 : 1.0;
+  Prof pr(d, s, list ? GMG_K_OTHER : GMG_K_RESTRICT, l,
+          list ? 0.0 : fine_vecs * sizeof(T) * (double)f.n + 4.0 * (np_of(d) + nn_of(d)) * (double)nf +
+                        2.0 * sizeof(T) * (double)d->lv[l - 1].n);
   DISPATCH_DK(d->dim, d->k, (dev::warp_restrict<D_, K_, MODE, T><<<xfer_grid(d, nf, dev::warp_restrict<D_, K_, MODE, T>), 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, vin, t, dc)));
   d->launches++;
@@ -287,6 +356,9 @@ static void k_prolongate(DeviceHierarchy* d, int l, const int* list, i64 nf, con
                          cudaStream_t s) {
   if (nf == 0) return;
   DevLevel& f = d->lv[l];
+  Prof pr(d, s, list ? GMG_K_OTHER : GMG_K_PROLONGATE, l,
+          list ? 0.0 : 2.0 * sizeof(T) * (double)f.n + 4.0 * (np_of(d) + nn_of(d)) * (double)nf +
+                        sizeof(T) * (double)d->lv[l - 1].n);
   DISPATCH_DK(d->dim, d->k, (dev::warp_prolongate<D_, K_, MODE, T><<<xfer_grid(d, nf, dev::warp_prolongate<D_, K_, MODE, T>), 32 * dev::XFER_WARPS, 0, s>>>(
                                 (int)nf, list, f.xfer, f.cls, xc, xf)));
   d->launches++;
@@ -297,6 +369,9 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
                    cudaStream_t s) {
   if (v.n_pad == 0) return;
   using V2 = typename dev::Vec2<T>::type;
+  // per padded row: g, D^-1 (+ t, dv, x) read; x (+ dv, t) written
+  const int nvec = 3 + (RT ? 2 : 0) + (RDV && !DVX ? 1 : 0) + (!XZ ? 1 : 0) + (WDV ? 1 : 0);
+  Prof pr(d, s, GMG_K_CHEB_STREAM_FULL, (int)(&v - d->lv.data()), (double)nvec * sizeof(T) * (double)v.n_pad);
   // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
   dev::cheb_step<T, RT, RDV, WDV, XZ, DVX><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
       (const V2*)g, (const V2*)MG<T>::Dinv(v), (V2*)t, (V2*)dv, (V2*)x, c1, c2);
@@ -315,6 +390,18 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
   import_ghosts(d, l, x, s);
   if (v.n_r1 > 0) {
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
+    // the operator's x gather and index rows, t (reduced) on the rows outside R1,
+    // and on the R1 rows the Chebyshev vectors: g, D^-1 (+ dv) read, x (+ dv) written
+    const double vb = sizeof(T);
+    const int r1v = 3 + (RDV && !DVX ? 1 : 0) + (WDV ? 1 : 0);
+    double fb = vb * (double)v.n + vb * (double)(v.n - v.n_r1) + r1v * vb * (double)v.n_r1;
+    if (PRO) fb += vb * (double)d->lv[l - 1].n + vb * (double)(v.n_owned - v.n_r1);
+    const double idx = 4.0 * nn * (double)v.n_cells + (PRO ? 4.0 * nn * (double)v.n_fam : 0.0);
+    const double idx_layout = 4.0 * np * (double)v.n_fam + (PRO ? 4.0 * nn * (double)v.n_fam : 0.0);
+    const int kind = TM == dev::TA_CHEB_X1 ? GMG_K_CHEB_X1 : TM == dev::TA_CHEB_11 ? GMG_K_CHEB_11
+                   : TM == dev::TA_CHEB_10 ? GMG_K_CHEB_10 : TM == dev::TA_CHEB_P01 ? GMG_K_CHEB_P01
+                   : TM == dev::TA_CHEB_01 ? GMG_K_CHEB_01 : GMG_K_CHEB_00;
+    Prof pr(d, s, kind, l, fb + idx, fb + idx_layout);
     if (d->k == 2)
       dev::fam_tensor_apply<2, T, TM><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
           (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc,
@@ -323,9 +410,12 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
       dev::fam_tensor_apply<1, T, TM><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
           (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);
     d->launches++;
+    pr.end();
     export_add(d, l, t, s);
     const i64 n = v.n_pad - v.n_r1;
     if (n > 0) {
+      const int nvec = 6 + (RDV && !DVX ? 1 : 0) + (WDV ? 1 : 0) + (PRO ? 1 : 0);   // g D t x (+dv) | t x (+dv)
+      Prof pr2(d, s, GMG_K_CHEB_STREAM, l, (double)nvec * sizeof(T) * (double)n);
       dev::cheb_range<T, RDV, WDV, DVX, PRO><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
           v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2, v.n_owned);
       d->launches++;
@@ -375,6 +465,7 @@ static void coarse(DeviceHierarchy* d, T* d0, T* x0, T* t0, T* dv0, cudaStream_t
     return;
   }
   if (d->nS0 == 0) return;
+  Prof pr(d, s, GMG_K_COARSE, 0, (double)d->nS0 * d->nS0 * 8.0);
   dev::coarse_solve<T><<<1, 256, 0, s>>>(d->nS0, d->coarse_idx, d->coarse_inv, d0, x0);
   d->launches++;
 }
@@ -887,6 +978,7 @@ void device_destroy(DeviceHierarchy* d) {
   if (!d) return;
   cudaDeviceSynchronize();
   if (d->vgraph) cudaGraphExecDestroy(d->vgraph);
+  for (cudaEvent_t e : d->evpool) cudaEventDestroy(e);
   for (auto& a : d->allocs) {
     if (d->dev_free) d->dev_free(a.first, a.second, nullptr, d->alloc_ctx);
     else cudaFree(a.first);
@@ -899,12 +991,16 @@ void device_destroy(DeviceHierarchy* d) {
 // ---------------------------------------------------------------- API ops
 void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int gr = d->vgrid(d->N);
+  {
+  const size_t vb = d->mixed ? 4 : 8;
+  Prof pr(d, s, GMG_K_COPY_MG, -1, 8.0 * (double)d->n_leaf + (4.0 + vb) * (double)d->N);
   if (d->mixed) dev::gather_to_mg<float><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32);   // copy_to_mg
   else dev::gather_to_mg<double><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);
   d->launches++;
+  }
   run_vcycle_mg(d, s);
   if (d->n_leaf) {                                                                              // copy_from_mg
+    Prof pr(d, s, GMG_K_COPY_MG, -1, (4.0 + 8.0 + (d->mixed ? 4 : 8)) * (double)d->n_leaf);
     if (d->mixed) dev::gather_from_mg<float><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X32, x);
     else dev::gather_from_mg<double><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X, x);
     d->launches++;
@@ -1137,6 +1233,46 @@ void device_set_eigen(DeviceHierarchy* d, int l, double lam) {
     cudaGraphExecDestroy(d->vgraph);
     d->vgraph = nullptr;
   }
+}
+
+// gmg_profile_vcycle: n_rep eager V-cycles (no graph) with every launch bracketed
+// by events; per (kind, level): launches, summed seconds, bytes per launch.
+int device_profile_vcycle(DeviceHierarchy* d, const double* b, double* x, int n_rep, gmg_kernel_stat* out,
+                          int max_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<DeviceHierarchy::ProfRec> recs;
+  const bool graph = d->use_graph;
+  CK(cudaStreamSynchronize(s));
+  d->use_graph = false;
+  d->prof = &recs;
+  d->evnext = 0;
+  try {
+    for (int r = 0; r < n_rep; ++r) device_vcycle(d, b, x, stream);
+    CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    d->prof = nullptr;
+    d->use_graph = graph;
+    throw;
+  }
+  d->prof = nullptr;
+  d->use_graph = graph;
+  std::vector<gmg_kernel_stat> agg;
+  for (auto& r : recs) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    gmg_kernel_stat* e = nullptr;
+    for (auto& q : agg)
+      if (q.kind == r.kind && q.level == r.level) e = &q;
+    if (!e) {
+      agg.push_back(gmg_kernel_stat{r.kind, r.level, 0, 0.0, r.bytes, r.bytes_layout});
+      e = &agg.back();
+    }
+    e->launches += 1;
+    e->seconds += 1e-3 * ms;
+  }
+  const int n = (int)agg.size();
+  for (int i = 0; i < n && i < max_out; ++i) out[i] = agg[i];
+  return n;
 }
 
 long long device_launches(const DeviceHierarchy* d) { return d->launches; }

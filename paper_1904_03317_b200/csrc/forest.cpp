@@ -470,3 +470,54 @@ Forest forest_create(int dim, int n_trees, const int32_t* tree_xyz, i64 n_leaves
 }
 
 }  // namespace gmg
+
+namespace gmg {
+
+// Number of distinct Q_k nodes of all leaves (reading R22: "DoFs" = all leaf
+// nodes, hanging and Dirichlet included) without building the topology: the
+// finest node lattice is cut into slabs along x; each slab gathers the node keys
+// of the leaves meeting it that fall into its half-open x range, sorts and counts
+// the distinct ones.  Memory ~ (all node occurrences) / n_slabs, so config-5
+// forests of 0.25-1B nodes can be counted on a small host.
+i64 count_leaf_nodes(const Forest& f, int k) {
+  GMG_REQUIRE(k >= 1 && k <= 4, GMG_E_INVALID_ARG, "k");
+  const int d = f.dim, L = f.L;
+  const i64 X = (i64)k * f.ext[0] << L;                 // lattice points 0..X along x
+  const i64 n_leaves = f.n_leaves();
+  int nn = 1;
+  for (int j = 0; j < d; ++j) nn *= k + 1;
+  const i64 occ = n_leaves * nn;
+  const i64 target = 1 << 26;                           // ~64M keys (0.5 GB) per slab
+  i64 n_slabs = std::max<i64>(1, std::min<i64>(X + 1, (occ + target - 1) / target));
+  const i64 emax = std::max({f.ext[0], f.ext[1], f.ext[2]});
+  const int cbits = bits_for((u64)(k * emax) << L);
+  GMG_REQUIRE(cbits * d <= 64, GMG_E_DEPTH, "lattice keys exceed 64 bits");
+  i64 total = 0;
+  std::vector<u64> keys;
+  for (i64 sl = 0; sl < n_slabs; ++sl) {
+    const i64 x0 = (X + 1) * sl / n_slabs, x1 = (X + 1) * (sl + 1) / n_slabs;   // [x0, x1)
+    keys.clear();
+    for (i64 i = 0; i < n_leaves; ++i) {
+      const int l = f.level[i];
+      const i64 sh = L - l;
+      const i64 lo = ((i64)k * f.gc[i][0]) << sh, hi = lo + ((i64)k << sh);
+      if (hi < x0 || lo >= x1) continue;
+      for (int b = 0; b < nn; ++b) {
+        Vec3 P{0, 0, 0};
+        int r = b;
+        for (int j = 0; j < d; ++j) {
+          P[j] = ((i64)k * f.gc[i][j] + r % (k + 1)) << sh;
+          r /= (k + 1);
+        }
+        if (P[0] < x0 || P[0] >= x1) continue;
+        keys.push_back(morton(d, P));
+      }
+    }
+    radix_sort_keys(keys, cbits * d);
+    for (size_t q = 0; q < keys.size(); ++q)
+      if (q == 0 || keys[q] != keys[q - 1]) ++total;
+  }
+  return total;
+}
+
+}  // namespace gmg

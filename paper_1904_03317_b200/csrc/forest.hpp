@@ -44,6 +44,7 @@ Forest forest_from_refined(int dim, const std::vector<Vec3>& trees, std::vector<
 i64 close_balance(int dim, const Forest& dom, std::vector<FlatSet>& R,
                   std::vector<std::pair<int, u64>>& work);
 Forest forest_generate(const gmg_recipe& r);
+i64 count_leaf_nodes(const Forest& f, int k);
 Forest forest_sequence(int dim, gmg_sequence kind, int L);
 Forest forest_create(int dim, int n_trees, const int32_t* tree_xyz, i64 n_leaves,
                      const int32_t* leaf_tree, const int8_t* leaf_level, const uint64_t* leaf_morton,
