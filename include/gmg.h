@@ -284,6 +284,10 @@ typedef struct {
    * other rank needs); 0 on levels without the family-tensor kernel and for
    * GMG_HOST_ONLY hierarchies */
   int64_t level_r1[GMG_MAX_LEVELS];
+  /* grandfamily patches of this rank run by the 9^3-patch kernel (complete
+   * grandfamilies with one coefficient, 3D Q2 tensor levels; 0 elsewhere and with
+   * GMG_GFAM=0) */
+  int64_t level_gf[GMG_MAX_LEVELS];
 } gmg_info;
 gmg_status gmg_hierarchy_info(const gmg_hierarchy *h, gmg_info *out);
 /* Leaf vectors of this rank: n_owned free leaf DoFs, the global

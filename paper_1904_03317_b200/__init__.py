@@ -99,7 +99,7 @@ class Info(C.Structure):
                 ("level_families", C.c_int64 * MAX_LEVELS), ("level_S", C.c_int64 * MAX_LEVELS),
                 ("level_E", C.c_int64 * MAX_LEVELS), ("level_B", C.c_int64 * MAX_LEVELS),
                 ("level_leaf_cells", C.c_int64 * MAX_LEVELS), ("mg_vector_len", C.c_int64),
-                ("level_r1", C.c_int64 * MAX_LEVELS)]
+                ("level_r1", C.c_int64 * MAX_LEVELS), ("level_gf", C.c_int64 * MAX_LEVELS)]
 
 
 class KernelStat(C.Structure):
@@ -385,7 +385,7 @@ class Hierarchy:
         nl = i.n_levels
         out = {f: getattr(i, f) for f, _ in Info._fields_ if not f.startswith("level_")}
         for f in ("level_dofs", "level_cells", "level_families", "level_S", "level_E", "level_B",
-                  "level_leaf_cells", "level_r1"):
+                  "level_leaf_cells", "level_r1", "level_gf"):
             out[f] = list(getattr(i, f)[:nl])
         return out
 

@@ -296,6 +296,7 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
       o->level_B[l] = t.nB;
       o->level_leaf_cells[l] = (gmg::i64)t.leaf_cells.size();
       o->level_r1[l] = h->dev ? gmg::device_level_r1(h->dev, l) : 0;
+      o->level_gf[l] = h->dev ? gmg::device_level_gf(h->dev, l) : 0;
       // this rank's level vector (owned + ghosts), padded like the device segments (kernels.cuh VEC_PAD)
       mg += (h->local.lv[l].n_local() + 511) / 512 * 512;
     }

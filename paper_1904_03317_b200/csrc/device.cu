@@ -39,6 +39,10 @@ struct DevLevel {
   int* fam_dofs = nullptr;          // SoA [(2k+1)^d][n_fam], only for the cell-form family apply (fam_apply)
   int* xfer = nullptr;              // AoS [n_fam][(2k+1)^d + (k+1)^d] fine patch | parent DoFs
   i64 n_r1 = 0;                     // device order (plan.hpp): rows [0, n_r1) finished by the fused apply
+  i64 n_gf = 0, n_single = 0;       // grandfamily patches / families left to the family kernel
+  int* gx = nullptr;                // [n_gf][GF_ROW] grandfamily tables (plan.hpp)
+  int* singles = nullptr;           // families not in a grandfamily
+  double* gcoef = nullptr;          // coefficient per grandfamily (config 4)
   bool fuse_pro = false;            // prolongation fused into the first post-smoothing step on EVERY rank
   int* perm = nullptr;              // rank-local level index -> device index (API boundary)
   int* leaf_cells = nullptr;
@@ -267,6 +271,39 @@ static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t v
   return 2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam;
 }
 
+// The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
+// plus the remaining families (fam_tensor_apply over the singles list), or all
+// families.  Epilogue mode TM, fused Chebyshev arguments as fam_tensor_apply.
+template <int K, typename T, int TM>
+static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1,
+                          double c2, const T* xc, cudaStream_t s) {
+  const int np = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), nn = (K + 1) * (K + 1) * (K + 1);
+  if (v.n_gf > 0) {
+    static const bool attr = [] {
+      CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)dev::gf_smem_bytes<K, T>()));
+      return true;
+    }();
+    (void)attr;
+    const int grid = (int)((v.n_gf + dev::GF_SLOTS - 1) / dev::GF_SLOTS);
+    dev::gfam_tensor_apply<K, T, TM><<<grid, dev::GF_THREADS, dev::gf_smem_bytes<K, T>(), s>>>(
+        (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc);
+    d->launches++;
+  }
+  const i64 nf = v.n_gf > 0 ? v.n_single : v.n_fam;
+  if (nf > 0) {
+    if constexpr (K == 2)
+      dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
+          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
+          v.n_gf > 0 ? 0 : tensor_wave<K, T, TM>(d), v.n_gf > 0 ? v.singles : nullptr);
+    else
+      dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
+          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc, 0,
+          v.n_gf > 0 ? v.singles : nullptr);
+    d->launches++;
+  }
+}
+
 template <typename T>
 static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* x, T* y, cudaStream_t s) {
   if (n == 0) return;
@@ -294,12 +331,10 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* 
                                                                                v.fcoef, v.scale, x, y);
     } else {
       if (d->k == 2)
-        dev::fam_tensor_apply<2, T><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y, 0, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0,
-            nullptr, tensor_wave<2, T, dev::TA_APPLY>(d));
+        launch_tensor<2, T, dev::TA_APPLY>(d, v, x, y, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, s);
       else
-        dev::fam_tensor_apply<1, T><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-            (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, y);
+        launch_tensor<1, T, dev::TA_APPLY>(d, v, x, y, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+      d->launches--;     // counted per kernel in launch_tensor
     }
   } else if (full) {                              // per-cell coefficients inside a family (config 4, level 2)
     DISPATCH_DK(d->dim, d->k, {
@@ -403,13 +438,9 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
                    : TM == dev::TA_CHEB_01 ? GMG_K_CHEB_01 : GMG_K_CHEB_00;
     Prof pr(d, s, kind, l, fb + idx, fb + idx_layout);
     if (d->k == 2)
-      dev::fam_tensor_apply<2, T, TM><<<tensor_grid<2>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc,
-          tensor_wave<2, T, TM>(d));
+      launch_tensor<2, T, TM>(d, v, x, t, g, dv, x, c1, c2, xc, s);
     else
-      dev::fam_tensor_apply<1, T, TM><<<tensor_grid<1>(v.n_fam), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale, x, t, v.n_r1, g, MG<T>::Dinv(v), dv, x, c1, c2, xc);
-    d->launches++;
+      launch_tensor<1, T, TM>(d, v, x, t, g, dv, x, c1, c2, xc, s);
     pr.end();
     export_add(d, l, t, s);
     const i64 n = v.n_pad - v.n_r1;
@@ -730,7 +761,11 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
                                i64 n0_global) {
   auto* d = new DeviceHierarchy();
   try {
-    const DevicePlan plan = plan_device_order(Tp);   // device order of the level vectors (rewrites Tp)
+    const bool gfam = [] {
+      const char* e = std::getenv("GMG_GFAM");
+      return !(e && e[0] == '0');
+    }();
+    const DevicePlan plan = plan_device_order(Tp, gfam);   // device order of the level vectors (rewrites Tp)
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
@@ -793,6 +828,13 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       v.leaf_cells = d->upload(t.leaf_cells);
       v.n_r1 = plan.n_r1[l];
       v.perm = d->upload(plan.perm[l]);
+      v.n_gf = plan.n_gf[l];
+      if (v.n_gf > 0) {
+        v.gx = d->upload(plan.gx[l]);
+        v.n_single = (i64)plan.singles[l].size();
+        v.singles = d->upload(plan.singles[l]);
+        if (!plan.gcoef[l].empty()) v.gcoef = d->upload(plan.gcoef[l]);
+      }
       if (!t.cell_coef.empty()) v.coef = d->upload(t.cell_coef);
       if (!t.fam_coef.empty()) v.fcoef = d->upload(t.fam_coef);
       if (!t.cell_elem.empty()) v.elem = d->upload(t.cell_elem);
@@ -969,6 +1011,10 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
 }
 
 long long device_mg_len(const DeviceHierarchy* d) { return d ? (long long)d->N : 0; }
+
+long long device_level_gf(const DeviceHierarchy* d, int level) {
+  return d && level >= 0 && level < (int)d->lv.size() ? (long long)d->lv[level].n_gf : 0;
+}
 
 long long device_level_r1(const DeviceHierarchy* d, int level) {
   return d && level >= 0 && level < (int)d->lv.size() ? (long long)d->lv[level].n_r1 : 0;

@@ -34,6 +34,7 @@ long long device_launches(const DeviceHierarchy* d);
 long long device_mg_len(const DeviceHierarchy* d);
 int device_profile_vcycle(DeviceHierarchy* d, const double* b, double* x, int n_rep, gmg_kernel_stat* out,
                           int max_out, void* stream);
+long long device_level_gf(const DeviceHierarchy* d, int level);
 long long device_level_r1(const DeviceHierarchy* d, int level);
 void device_launch_profile(const DeviceHierarchy* d, long long* per_vcycle, long long* per_leaf_apply);
 

@@ -129,6 +129,9 @@ struct LocalLevel {
   std::vector<i32> fam_dofs;               // [n_fam][(2k+1)^d] local, transfer-owner encoding
   std::vector<i32> xfer;                   // [n_fam][(2k+1)^d + (k+1)^d] fine | parent (level l-1 local)
   std::vector<i32> leaf_cells, edge_fams;
+  // complete grandfamilies (3D): local family index of the first of 8 consecutive
+  // local families whose parents are the 8 children of one level-(l-2) cell
+  std::vector<i32> gf_first;
   std::vector<uint8_t> cls, lam;           // per local DoF (ghosts: lam = 0)
   std::vector<double> eig_v;               // eigen start vector on owned S DoFs
   i64 nS_global = 0;

@@ -361,7 +361,8 @@ __global__ void __launch_bounds__(32 * TG_WARPS)
 fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0) {
+                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
+                 const int* __restrict__ flist = nullptr) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
@@ -371,9 +372,11 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
   __shared__ T s0[NS], s1[NS];
   __shared__ T cb[PRO ? FPB : 1][(K + 1) * (K + 1) * (K + 1) + 1];   // PRO: the parents' values
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
-  const long f = (long)blockIdx.x * FPB + slot;
-  const bool act = slot < FPB && f < nfam;
-  if (pf > 0) {   // the patch rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
+  const long fi = (long)blockIdx.x * FPB + slot;
+  const bool act = slot < FPB && fi < nfam;
+  // flist: the families not covered by grandfamily patches (gfam_tensor_apply)
+  const long f = flist ? (act ? (long)__ldg(flist + fi) : 0) : fi;
+  if (pf > 0 && !flist) {   // the patch rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
     const long fb = ((long)blockIdx.x + pf) * FPB;
     const long bytes = (long)FPB * row * 4, off = (long)threadIdx.x * 128;
     if (fb < nfam && off < bytes && fb * row * 4 + off < (long)nfam * row * 4)
@@ -581,6 +584,284 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       } else {
         if (PRO && ((own >> z) & 1)) dv[i] = inc[z];  // P x_{l-1} of a streamed row (cheb_range<PRO>)
         if (i < n_r1 || (inner && z > 0 && z < 2 * K)) y[i] = v;   // only this family touches the node
+        else atomicAdd(y + i, v);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- grandfamily patches
+// gfam_tensor_apply: the level operator on the (4k+1)^3 patch of a complete
+// grandfamily -- the 64 level-l cells below one level-(l-2) cell G all of whose 8
+// children are refined -- as ONE Kronecker sum with the 1-D matrices assembled
+// over four cells (Kt4, Mt4).  Against eight separate family patches this
+// gathers 729 instead of 1000 values (Q2), reads 729 instead of 1000 index
+// entries, transposes 27 % fewer values through shared memory, and its 7^3
+// patch-interior nodes (343 of the 512 rows the 64 cells own) are complete rows:
+// stored / finished by the fused Chebyshev epilogue instead of reduced at L2 and
+// streamed.  Thick refined regions (config 5's shell, config 4's corner) consist
+// mostly of complete grandfamilies; thin ones (config 3's finest level) have none
+// and keep the family kernel.  Epilogue modes as fam_tensor_apply (TA_*).
+// Table gxfer [n_gf][GF_ROW]: 729 fine patch entries (x fastest; v >= 0: this
+// grandfamily holds the node's transfer-owner family, v <= -2: DoF -2-v owned by
+// another family, -1: Dirichlet), then the 125 level-(l-1) DoFs of G's family
+// patch (the 8 parents' nodes; used by TA_CHEB_P01).
+template <int K>
+__host__ __device__ __forceinline__ constexpr double Kt4(int i, int j) {
+  double s = 0.0;
+  for (int e = 0; e < 4; ++e) {
+    const int li = i - e * K, lj = j - e * K;
+    if (li >= 0 && li <= K && lj >= 0 && lj <= K) s += Q<K>::Km(li, lj);
+  }
+  return s;
+}
+template <int K>
+__host__ __device__ __forceinline__ constexpr double Mt4(int i, int j) {
+  double s = 0.0;
+  for (int e = 0; e < 4; ++e) {
+    const int li = i - e * K, lj = j - e * K;
+    if (li >= 0 && li <= K && lj >= 0 && lj <= K) s += Q<K>::Mm(li, lj);
+  }
+  return s;
+}
+
+constexpr int GF_SLOTS = 3;           // grandfamilies per block: 3 x 81 = 243 of 256 lanes busy
+constexpr int GF_THREADS = 256;
+#ifndef GF_MIN_BLOCKS_DEFAULT
+#define GF_MIN_BLOCKS_DEFAULT 3
+#endif
+constexpr int GF_MIN_BLOCKS = GF_MIN_BLOCKS_DEFAULT;   // register cap 65536 / (256 x 3) = 85
+template <int K> struct GfShape {
+  static constexpr int N1 = 4 * K + 1, NL = N1 * N1, NP = N1 * N1 * N1;
+  static constexpr int NCP = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);   // G's family patch one level up
+  static constexpr int ROW = NP + NCP;
+};
+// Transposition layouts (index = cx x + cy y + cz z, per slot).  fp64 shared
+// memory serves a half-warp per pass over 16 bank pairs, so an access whose 16
+// lanes hit 16 distinct addresses mod 16 takes the minimum of one wavefront per
+// half-warp.  Lanes number a line as L = a + 9 b (a, b its two coordinates); the
+// strides (1, 9) and (9, 1) (mod 16) are both injective on 16 consecutive L, so
+// for Q2 (9^3 patch):
+//   A  z-pass store (px, py), y-pass load (px, pz):  ax = 1, ay = 9,  az = 89
+//   B  y-pass store (px, pz), x-pass load (py, pz):  bx = 9, by = 89, bz = 1
+//   N  x-pass store (py, pz), scatter load (px, py):  nx = 1, ny = 9,  nz = 81
+// every pass is conflict-free (up to the half-warps straddling two slots; the
+// slot stride is 1 mod 16).  N reuses the first buffer.  Other K: natural order.
+template <int K> struct GfLayout {
+  static constexpr int N1 = 4 * K + 1;
+  static constexpr bool Q2 = N1 == 9;
+  static constexpr int ax = 1, ay = Q2 ? 9 : N1, az = Q2 ? 89 : N1 * N1;
+  static constexpr int bx = Q2 ? 9 : 1, by = Q2 ? 89 : N1, bz = Q2 ? 1 : N1 * N1;
+  static constexpr int nx = 1, ny = N1, nz = N1 * N1;
+  static constexpr int SA = ax * (N1 - 1) + ay * (N1 - 1) + az * (N1 - 1) + 1;
+  static constexpr int SB = bx * (N1 - 1) + by * (N1 - 1) + bz * (N1 - 1) + 1;
+  static constexpr int SN = N1 * N1 * N1;
+  static constexpr int SS = SA > SB ? (SA > SN ? SA : SN) : (SB > SN ? SB : SN);
+  static constexpr int SLOT = SS + ((17 - SS % 16) % 16);   // = 1 mod 16
+};
+template <int K, typename T>
+constexpr size_t gf_smem_bytes() {
+  return sizeof(T) * 2 * GF_SLOTS * GfLayout<K>::SLOT + (size_t)sizeof(T) * GF_SLOTS * (GfShape<K>::NCP + 1);
+}
+
+template <int K, typename T, int TM = TA_APPLY>
+__global__ void __launch_bounds__(GF_THREADS, GF_MIN_BLOCKS)
+gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict__ gcoef, double scale_,
+                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
+                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
+                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr) {
+  constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
+  constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
+  constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
+  using S = GfShape<K>;
+  using LY = GfLayout<K>;
+  constexpr int N1 = S::N1, NL = S::NL, ROW = S::ROW, NP = S::NP;
+  extern __shared__ __align__(16) unsigned char gf_smem[];
+  T* s0 = reinterpret_cast<T*>(gf_smem);
+  T* s1 = s0 + GF_SLOTS * LY::SLOT;
+  T* cbase = s1 + GF_SLOTS * LY::SLOT;             // PRO: G's coarse patch per slot
+  const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;
+  const long q0 = (long)blockIdx.x * GF_SLOTS + slot;
+  const bool act = slot < GF_SLOTS && q0 < ngf;
+  const int* rp = gx + (act ? q0 : 0) * (long)ROW;
+  T* const a0 = s0 + (act ? slot : 0) * LY::SLOT;
+  T* const a1 = s1 + (act ? slot : 0) * LY::SLOT;
+  T* const cb = cbase + (act ? slot : 0) * (S::NCP + 1);
+  const T scale = (T)(act && gcoef ? scale_ * __ldg(gcoef + q0) : scale_);
+  const int px = lane % N1, py = lane / N1;
+  int gi[N1];
+  T u[N1], ukeep[N1];
+  T inc[PRO ? N1 : 1];
+  int own = 0;
+  if (act) {              // z lines: lane = (px, py)
+#pragma unroll
+    for (int z = 0; z < N1; ++z) {
+      const int e = __ldg(rp + z * NL + lane);
+      gi[z] = decode_dof(e);
+      if (PRO && e >= 0) own |= 1 << z;
+    }
+#pragma unroll
+    for (int z = 0; z < N1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+  }
+  if constexpr (PRO) {
+    // x + P x_{l-1}: every fine node from one parent containing it, in
+    // warp_prolongate's order (x, y, z passes, fma chains over ascending coarse
+    // index); nodes on a face between two parents get the same bits from either
+    // (the 1-D weight across the face is an exact pick of the shared coarse node)
+    constexpr int N = K + 1, NC1 = 2 * K + 1;
+    if (act)
+      for (int c = lane; c < S::NCP; c += NL) {
+        const int ci = __ldg(rp + NP + c);
+        cb[c] = ci >= 0 ? __ldg(xc + ci) : T(0);
+      }
+    __syncthreads();
+    if (act) {
+      const int cx = px <= 2 * K ? 0 : 1, cy = py <= 2 * K ? 0 : 1;   // a containing parent in x, y
+      const int lx = px - 2 * K * cx, ly = py - 2 * K * cy;
+      T wx[N], wy[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        wx[a] = wy[a] = T(0);
+#pragma unroll
+        for (int p = 0; p < NC1; ++p) {
+          if (lx == p) wx[a] = (T)Q<K>::P(p, a);
+          if (ly == p) wy[a] = (T)Q<K>::P(p, a);
+        }
+      }
+      T w[2][N];
+#pragma unroll
+      for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          w[cz][c] = T(0);
+#pragma unroll
+          for (int b = 0; b < N; ++b) {
+            T sx = T(0);
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+              sx = fma(wx[a], cb[(K * cx + a) + NC1 * (K * cy + b) + NC1 * NC1 * (K * cz + c)], sx);
+            w[cz][c] = fma(wy[b], sx, w[cz][c]);
+          }
+        }
+#pragma unroll
+      for (int z = 0; z < N1; ++z) {
+        const int cz = z <= 2 * K ? 0 : 1, lz = z - 2 * K * cz;
+        T sz = T(0);
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          if (Q<K>::P(lz, c) != 0.0) sz = fma((T)Q<K>::P(lz, c), w[cz][c], sz);
+        inc[z] = sz;
+      }
+    }
+  }
+  if (act) {
+    if constexpr (PRO) {
+#pragma unroll
+      for (int z = 0; z < N1; ++z)
+        if (gi[z] >= 0) u[z] = u[z] + inc[z];
+    }
+#pragma unroll
+    for (int z = 0; z < N1; ++z) ukeep[z] = u[z];
+#pragma unroll
+    for (int z = 0; z < N1; ++z) {
+      T t1 = 0, t2 = 0;
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        if (Mt4<K>(z, q) != 0.0) t1 = fma((T)Mt4<K>(z, q), u[q], t1);
+        if (Kt4<K>(z, q) != 0.0) t2 = fma((T)Kt4<K>(z, q), u[q], t2);
+      }
+      const int ia = LY::ax * px + LY::ay * py + LY::az * z;
+      a0[ia] = t1;
+      a1[ia] = t2;
+    }
+  }
+  __syncthreads();
+  T t1[N1], t2[N1];
+  const int pz = lane / N1;     // y lines: lane = (px, pz)
+  if (act) {
+    const int ba = LY::ax * px + LY::az * pz;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) {
+      t1[q] = a0[ba + LY::ay * q];
+      t2[q] = a1[ba + LY::ay * q];
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int bb_ = LY::bx * px + LY::bz * pz;
+#pragma unroll
+    for (int yy = 0; yy < N1; ++yy) {
+      T a = 0, bb = 0;
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        if (Mt4<K>(yy, q) != 0.0) {
+          a = fma((T)Mt4<K>(yy, q), t1[q], a);
+          bb = fma((T)Mt4<K>(yy, q), t2[q], bb);
+        }
+        if (Kt4<K>(yy, q) != 0.0) bb = fma((T)Kt4<K>(yy, q), t1[q], bb);
+      }
+      a0[bb_ + LY::by * yy] = a;
+      a1[bb_ + LY::by * yy] = bb;
+    }
+  }
+  __syncthreads();
+  T out[N1];
+  if (act) {              // x lines: lane = (py, pz)
+    const int qy = lane % N1, qz = lane / N1;
+    const int bx = LY::by * qy + LY::bz * qz;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) {
+      t1[q] = a0[bx + LY::bx * q];
+      t2[q] = a1[bx + LY::bx * q];
+    }
+#pragma unroll
+    for (int xx = 0; xx < N1; ++xx) {
+      T o = 0;
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        if (Kt4<K>(xx, q) != 0.0) o = fma((T)Kt4<K>(xx, q), t1[q], o);
+        if (Mt4<K>(xx, q) != 0.0) o = fma((T)Mt4<K>(xx, q), t2[q], o);
+      }
+      out[xx] = scale * o;
+    }
+  }
+  __syncthreads();        // every lane has read layout B
+  if (act) {              // x-line results -> layout N (first buffer, reused), read back along z lines
+    const int qy = lane % N1, qz = lane / N1;
+    const int bn = LY::ny * qy + LY::nz * qz;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) a0[bn + LY::nx * q] = out[q];
+  }
+  T pg[N1], pd[N1], pv[N1];
+  if (TM != TA_APPLY && act) {
+#pragma unroll
+    for (int z = 0; z < N1; ++z) {
+      const int i = gi[z];
+      pg[z] = pd[z] = pv[z] = T(0);
+      if (i >= 0 && i < n_r1) {
+        pg[z] = __ldg(g + i);
+        pd[z] = __ldg(Dinv + i);
+        if (RDV && !DVX) pv[z] = dv[i];
+      }
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const bool inner = px > 0 && px < 4 * K && py > 0 && py < 4 * K;
+    const int bn = LY::nx * px + LY::ny * py;
+#pragma unroll
+    for (int z = 0; z < N1; ++z) {
+      const int i = gi[z];
+      if (i < 0) continue;
+      const T v = a0[bn + LY::nz * z];
+      if (TM != TA_APPLY && i < n_r1) {
+        T dd = (T)c2_ * pd[z] * (pg[z] - v);
+        if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
+        if (WDV) dv[i] = dd;
+        xw[i] = ukeep[z] + dd;
+      } else {
+        if (PRO && ((own >> z) & 1)) dv[i] = inc[z];
+        if (i < n_r1 || (inner && z > 0 && z < 4 * K)) y[i] = v;   // only this patch touches the node
         else atomicAdd(y + i, v);
       }
     }

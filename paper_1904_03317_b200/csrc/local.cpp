@@ -120,6 +120,23 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     v.n_cells = (i64)cellg[l].size();
     v.cell_global = cellg[l];
     v.n_fam = (i64)famg[l].size();
+    if (d == 3 && l >= 2) {
+      // complete grandfamilies: 8 consecutive local families (SFC order) whose
+      // parents are children 0..7 of one level-(l-2) cell
+      const auto& pk = p.levels[l - 1].key;
+      const i64 nf = v.n_fam;
+      for (i64 lf = 0; lf + 7 < nf;) {
+        const u64 k0 = pk[t.fam_parent[famg[l][lf]]];
+        bool ok = (k0 & 7) == 0;
+        for (int j = 1; ok && j < 8; ++j) ok = pk[t.fam_parent[famg[l][lf + j]]] == (k0 | (u64)j);
+        if (ok) {
+          v.gf_first.push_back((i32)lf);
+          lf += 8;
+        } else {
+          ++lf;
+        }
+      }
+    }
   }
   auto local_of = [&](int l, i64 g) -> i32 {
     if (g < 0) return -1;

@@ -10,7 +10,16 @@ static inline i32 remap_enc(i32 v, const std::vector<i32>& p) {
   return -1;
 }
 
-DevicePlan plan_device_order(LocalTopo& T) {
+// Node of grandfamily position (X, Y, Z) (0 .. 4k each) in family-patch terms:
+// the family j = cx + 2 cy + 4 cz of the grandfamily and its patch position a.
+static inline void gf_pos(int k, int X, int Y, int Z, int& j, int& a) {
+  const int NP1 = 2 * k + 1;
+  const int cx = X > 2 * k ? 1 : 0, cy = Y > 2 * k ? 1 : 0, cz = Z > 2 * k ? 1 : 0;
+  j = cx + 2 * cy + 4 * cz;
+  a = (X - 2 * k * cx) + NP1 * (Y - 2 * k * cy) + NP1 * NP1 * (Z - 2 * k * cz);
+}
+
+DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
   const int d = T.dim, k = T.k, L = T.L;
   const int NP1 = 2 * k + 1;
   int nn = 1, np = 1;
@@ -18,6 +27,7 @@ DevicePlan plan_device_order(LocalTopo& T) {
     nn *= k + 1;
     np *= NP1;
   }
+  const int G1 = 4 * k + 1, GNP = G1 * G1 * G1;
   // interior patch positions, z-major (ascending patch index)
   std::vector<int> inner;
   for (int a = 0; a < np; ++a) {
@@ -29,6 +39,13 @@ DevicePlan plan_device_order(LocalTopo& T) {
   DevicePlan P;
   P.perm.resize(L + 1);
   P.n_r1.assign(L + 1, 0);
+  P.n_gf.assign(L + 1, 0);
+  P.gx.resize(L + 1);
+  P.singles.resize(L + 1);
+  P.gcoef.resize(L + 1);
+  // per level: grandfamilies in use (first local family of each) and a family ->
+  // grandfamily map (-1: single)
+  std::vector<std::vector<i32>> gfs(L + 1), fam_gf(L + 1);
   // ---------------- 1. device order of every level (from the original tables)
   for (int l = 0; l <= L; ++l) {
     const LocalLevel& v = T.lv[l];
@@ -43,28 +60,51 @@ DevicePlan plan_device_order(LocalTopo& T) {
     if (tensor) {
       std::vector<char> remote(no, 0);
       for (i32 s : v.send_idx) remote[s] = 1;
-      // number of local family patches touching each local DoF
-      std::vector<uint8_t> touch(n, 0);
-      for (i64 f = 0; f < v.n_fam; ++f)
-        for (int a = 0; a < np; ++a) {
-          const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
-          if (g >= 0 && touch[g] < 255) ++touch[g];
+      // grandfamily patches in use: Q2, one coefficient for all 8 families
+      std::vector<i32>& fg = fam_gf[l];
+      fg.assign(v.n_fam, -1);
+      if (grandfamilies && k == 2)
+        for (i32 f0 : v.gf_first) {
+          bool ok = true;
+          if (!v.fam_coef.empty())
+            for (int j = 1; j < 8; ++j) ok &= v.fam_coef[f0 + j] == v.fam_coef[f0];
+          if (!ok) continue;
+          for (int j = 0; j < 8; ++j) fg[f0 + j] = (i32)gfs[l].size();
+          gfs[l].push_back(f0);
         }
-      for (i64 f = 0; f < v.n_fam; ++f) {
+      // executed patches in SFC order (a grandfamily at its first family), each
+      // visiting its nodes in patch order, once per distinct node
+      auto for_patches = [&](auto&& fn) {
+        for (i64 f = 0; f < v.n_fam; ++f) {
+          if (fg[f] < 0) {
+            for (int a = 0; a < np; ++a) fn(dec(v.fam_dofs[(size_t)f * np + a]));
+          } else if (gfs[l][fg[f]] == f) {
+            for (int Z = 0; Z < G1; ++Z)
+              for (int Y = 0; Y < G1; ++Y)
+                for (int X = 0; X < G1; ++X) {
+                  int j, a;
+                  gf_pos(k, X, Y, Z, j, a);
+                  fn(dec(v.fam_dofs[(size_t)(f + j) * np + a]));
+                }
+          }
+        }
+      };
+      // number of executed patches touching each local DoF
+      std::vector<uint8_t> touch(n, 0);
+      for_patches([&](i64 g) {
+        if (g >= 0 && touch[g] < 255) ++touch[g];
+      });
+      for (i64 f = 0; f < v.n_fam; ++f)
         for (int a : inner)
           GMG_REQUIRE(dec(v.fam_dofs[(size_t)f * np + a]) >= 0, GMG_E_STATE, "interior patch node without a DoF");
-        for (int a = 0; a < np; ++a) {
-          const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
-          if (g >= 0 && g < no && touch[g] == 1 && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
-        }
-      }
+      for_patches([&](i64 g) {
+        if (g >= 0 && g < no && touch[g] == 1 && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
+      });
       P.n_r1[l] = pos;
-      // the rest in the order the family patches first reach them (patch order)
-      for (i64 f = 0; f < v.n_fam; ++f)
-        for (int a = 0; a < np; ++a) {
-          const i64 g = dec(v.fam_dofs[(size_t)f * np + a]);
-          if (g >= 0 && g < no && perm[g] < 0) perm[g] = (i32)pos++;
-        }
+      // the rest in the order the executed patches first reach them (patch order)
+      for_patches([&](i64 g) {
+        if (g >= 0 && g < no && perm[g] < 0) perm[g] = (i32)pos++;
+      });
     }
     for (i64 i = 0; i < no; ++i)
       if (perm[i] < 0) perm[i] = (i32)pos++;
@@ -104,6 +144,51 @@ DevicePlan plan_device_order(LocalTopo& T) {
   }
   for (size_t g = 0; g < T.leaf_local.size(); ++g)
     T.leaf_local[g] = P.perm[T.leaf_level[g]][T.leaf_local[g]];
+  // ---------------- 3. grandfamily tables (device order) and the single families
+  const int NCP = NP1 * NP1 * NP1, GROW = GNP + NCP;
+  for (int l = 0; l <= L; ++l) {
+    const LocalLevel& v = T.lv[l];
+    if (gfs[l].empty()) continue;
+    const std::vector<i32>& fg = fam_gf[l];
+    P.n_gf[l] = (i64)gfs[l].size();
+    std::vector<i32>& gx = P.gx[l];
+    gx.assign((size_t)P.n_gf[l] * GROW, -1);
+    for (size_t q = 0; q < gfs[l].size(); ++q) {
+      const i64 f0 = gfs[l][q];
+      i32* row = gx.data() + q * GROW;
+      for (int Z = 0; Z < G1; ++Z)
+        for (int Y = 0; Y < G1; ++Y)
+          for (int X = 0; X < G1; ++X) {
+            int j, a;
+            gf_pos(k, X, Y, Z, j, a);
+            const i64 g = dec(v.fam_dofs[(size_t)(f0 + j) * np + a]);
+            // transfer owner inside the grandfamily: some family containing the node
+            // holds it with a non-negative entry
+            bool own = false;
+            for (int cz = 0; cz < 2; ++cz)
+              for (int cy = 0; cy < 2; ++cy)
+                for (int cx = 0; cx < 2; ++cx) {
+                  const int lx = X - 2 * k * cx, ly = Y - 2 * k * cy, lz = Z - 2 * k * cz;
+                  if (lx < 0 || lx > 2 * k || ly < 0 || ly > 2 * k || lz < 0 || lz > 2 * k) continue;
+                  const i32 e = v.fam_dofs[(size_t)(f0 + cx + 2 * cy + 4 * cz) * np + lx + NP1 * ly + NP1 * NP1 * lz];
+                  if (e >= 0) own = true;
+                }
+            row[X + G1 * Y + G1 * G1 * Z] = g < 0 ? -1 : (own ? (i32)g : (i32)(-2 - g));
+          }
+      // G's family patch one level up: the 8 parents' (k+1)^3 nodes
+      for (int c = 0; c < NP1; ++c)
+        for (int b = 0; b < NP1; ++b)
+          for (int a = 0; a < NP1; ++a) {
+            const int cx = a > k ? 1 : 0, cy = b > k ? 1 : 0, cz = c > k ? 1 : 0;
+            const int la = a - k * cx, lb = b - k * cy, lc = c - k * cz;
+            const i32* xr = v.xfer.data() + (size_t)(f0 + cx + 2 * cy + 4 * cz) * (np + nn);
+            row[GNP + a + NP1 * b + NP1 * NP1 * c] = xr[np + la + (k + 1) * lb + (k + 1) * (k + 1) * lc];
+          }
+      if (!v.fam_coef.empty()) P.gcoef[l].push_back(v.fam_coef[f0]);
+    }
+    for (i64 f = 0; f < v.n_fam; ++f)
+      if (fg[f] < 0) P.singles[l].push_back((i32)f);
+  }
   return P;
 }
 
