@@ -56,6 +56,13 @@ def uniform_pm1(n: int, stream: int = STREAM_RHS, seed: int = SEED, offset: int 
     return 2.0 * uniform01(seed, stream, np.arange(offset, offset + n, dtype=np.uint64)) - 1.0
 
 
+def uniform_pm1_keys(keys, stream: int = STREAM_RHS, seed: int = SEED) -> np.ndarray:
+    """v = 2u - 1 drawn by node key instead of canonical index (rank-local
+    hierarchies: a rank knows the keys of its DoFs, not their canonical ranks);
+    independent of the number of ranks."""
+    return 2.0 * uniform01(seed, stream, np.asarray(keys, dtype=np.uint64)) - 1.0
+
+
 def log_uniform_coef(n: int, stream: int = STREAM_COEF, seed: int = SEED) -> np.ndarray:
     """a = 10^(4u - 2), log-uniform in [1e-2, 1e2) (config 4)."""
     u = uniform01(seed, stream, np.arange(n, dtype=np.uint64))

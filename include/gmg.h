@@ -189,6 +189,12 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
                                  fp64 interface (conversion at copy_to/from_mg) */
 #define GMG_LOCAL_RANKS 4u    /* all n_ranks ranks live in this process (one host thread and
                                  stream each, same GPU); params.nccl_comm is a gmg_local_world */
+#define GMG_RANK_LOCAL 32u    /* build only this rank's part of the level topology:
+                                 no global level numbering (global exports -> GMG_E_STATE), global
+                                 sizes summed over the communicator; implies GMG_EIG_KEY */
+#define GMG_EIG_KEY 64u       /* eigen start vector -5.5 + (level-lattice Morton key mod 12) on the
+                                 S DoFs (reading R10b, rank-local) instead of the canonical-rank
+                                 pattern of R10 */
 #define GMG_HOST_RANKS 16u    /* ranks are processes joined by a gmg_host_world, passed as params.nccl_comm */
 
 /* ------------------------------------------------------------------ communicators
@@ -309,6 +315,31 @@ gmg_status gmg_export_leaf_dofs(const gmg_hierarchy *h, int64_t *n, uint64_t *ke
  * parents of its next-finer families touch.  ghosts may be NULL. */
 gmg_status gmg_export_rank_level(const gmg_hierarchy *h, int level, int64_t *first_owned, int64_t *n_owned,
                                  int64_t *n_ghost, int64_t *ghosts);
+/* Rank-local layout of `level` in keys (works for GMG_RANK_LOCAL and global
+ * builds alike): owned DoFs (local order = Morton key order), ghosts (sorted by
+ * (owner, key)) with their owners, and the exchange plan -- peers, per-peer
+ * offsets [n_peers + 1] into send_idx (local indices of owned DoFs sent to the
+ * peer) and recv_idx (local indices n_owned + i of the ghosts received).  Sizes:
+ * query n_owned, n_ghost, n_peers with NULL arrays first; send/recv lengths are
+ * send_off[n_peers] / recv_off[n_peers].  Keys are Morton keys of
+ * finest-lattice node coordinates. */
+gmg_status gmg_export_local_level(const gmg_hierarchy *h, int level, int64_t *n_owned, int64_t *n_ghost,
+                                  uint64_t *owned_key, uint64_t *ghost_key, int32_t *ghost_owner,
+                                  int32_t *n_peers, int32_t *peers, int64_t *send_off, int64_t *recv_off,
+                                  int32_t *send_idx, int32_t *recv_idx);
+/* The rank's local tables of `level` before the device reordering (GMG_HOST_ONLY
+ * hierarchies only, else GMG_E_STATE): cell -> local DoF [n_cells][(k+1)^d] (-1
+ * Dirichlet), transfer rows [n_fam][(2k+1)^d + (k+1)^d] (fine patch in transfer-
+ * owner encoding v >= 0 / -2-v / -1, then the parent's level-(l-1) local DoFs),
+ * class (0 S, 1 E) and lambda flag per local DoF, eigen start vector, global
+ * C_l index of every local cell.  Query n_cells, n_fam with NULL arrays. */
+gmg_status gmg_export_local_tables(const gmg_hierarchy *h, int level, int64_t *n_cells, int64_t *n_fam,
+                                   int32_t *cell_dofs, int32_t *xfer, uint8_t *cls, uint8_t *lam,
+                                   double *eig_v, int64_t *cell_global);
+/* This rank's free leaf DoFs in leaf order: finest-lattice Morton key and level
+ * lambda (size query with NULL arrays).  Random inputs drawn by key do not depend
+ * on the rank count (gmg_inputs.uniform_pm1_keys). */
+gmg_status gmg_export_owned_leaf_keys(const gmg_hierarchy *h, int64_t *n, uint64_t *key, int8_t *lambda);
 /* Cell -> level-DoF table of `level` (global index, -1 for Dirichlet nodes):
  * host [n_cells * (k+1)^d], cells in SFC order, local nodes x fastest. */
 gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_cells,

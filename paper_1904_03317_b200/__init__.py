@@ -47,6 +47,8 @@ GMG_NO_GRAPH = 2
 GMG_MIXED_PRECISION = 8
 GMG_LOCAL_RANKS = 4
 GMG_HOST_RANKS = 16
+GMG_RANK_LOCAL = 32
+GMG_EIG_KEY = 64
 MAX_LEVELS = 64
 
 
@@ -161,6 +163,10 @@ _SIGS = {
     "gmg_host_world_destroy": ([_vp], C.c_int),
     "gmg_leaf_layout": ([_vp, _i64p, _i64p, _i64p], C.c_int),
     "gmg_forest_count_nodes": ([_vp, C.c_int, _i64p], C.c_int),
+    "gmg_export_local_level": ([_vp, C.c_int, _i64p, _i64p, _vp, _vp, _vp, C.POINTER(C.c_int32), _vp, _vp, _vp,
+                                _vp, _vp], C.c_int),
+    "gmg_export_local_tables": ([_vp, C.c_int, _i64p, _i64p, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "gmg_export_owned_leaf_keys": ([_vp, _i64p, _vp, _vp], C.c_int),
     "gmg_profile_vcycle": ([_vp, _vp, _vp, C.c_int, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int), _vp],
                            C.c_int),
 }
@@ -418,6 +424,56 @@ class Hierarchy:
         _check(_lib.gmg_export_rank_level(self.h, level, C.byref(fo), C.byref(no), C.byref(ng), _ptr(gh)))
         return fo.value, no.value, gh
 
+    def local_level(self, level):
+        """Rank-local layout in keys (gmg_export_local_level): dict of numpy arrays."""
+        no, ng, npr = C.c_int64(), C.c_int64(), C.c_int32()
+        _check(_lib.gmg_export_local_level(self.h, level, C.byref(no), C.byref(ng), None, None, None, C.byref(npr),
+                                           None, None, None, None, None))
+        ok = np.empty(no.value, np.uint64)
+        gk = np.empty(ng.value, np.uint64)
+        go = np.empty(ng.value, np.int32)
+        peers = np.empty(npr.value, np.int32)
+        so = np.empty(npr.value + 1, np.int64)
+        ro = np.empty(npr.value + 1, np.int64)
+        _check(_lib.gmg_export_local_level(self.h, level, C.byref(no), C.byref(ng), _ptr(ok), _ptr(gk), _ptr(go),
+                                           C.byref(npr), _ptr(peers), _ptr(so), _ptr(ro), None, None))
+        si = np.empty(int(so[-1]), np.int32)
+        ri = np.empty(int(ro[-1]), np.int32)
+        _check(_lib.gmg_export_local_level(self.h, level, C.byref(no), C.byref(ng), None, None, None, C.byref(npr),
+                                           None, None, None, _ptr(si), _ptr(ri)))
+        return dict(owned_key=ok, ghost_key=gk, ghost_owner=go, peers=peers, send_off=so, recv_off=ro,
+                    send_idx=si, recv_idx=ri)
+
+    def local_tables(self, level):
+        """Local tables before device reordering (GMG_HOST_ONLY hierarchies)."""
+        nc, nf = C.c_int64(), C.c_int64()
+        _check(_lib.gmg_export_local_tables(self.h, level, C.byref(nc), C.byref(nf), None, None, None, None, None,
+                                            None))
+        lv = self.local_level(level)
+        nloc = lv["owned_key"].size + lv["ghost_key"].size
+        i = self.info()
+        nn = (i["k"] + 1) ** i["dim"]
+        row = (2 * i["k"] + 1) ** i["dim"] + nn
+        cd = np.empty(nc.value * nn, np.int32)
+        xf = np.empty(nf.value * row, np.int32)
+        cls = np.empty(nloc, np.uint8)
+        lam = np.empty(nloc, np.uint8)
+        ev = np.empty(nloc, np.float64)
+        cg = np.empty(nc.value, np.int64)
+        _check(_lib.gmg_export_local_tables(self.h, level, C.byref(nc), C.byref(nf), _ptr(cd), _ptr(xf), _ptr(cls),
+                                            _ptr(lam), _ptr(ev), _ptr(cg)))
+        return dict(cell_dofs=cd.reshape(-1, nn), xfer=xf.reshape(-1, row) if nf.value else xf, cls=cls, lam=lam,
+                    eig_v=ev, cell_global=cg)
+
+    def owned_leaf_keys(self):
+        """(keys, lambda) of this rank's free leaf DoFs in leaf order."""
+        n = C.c_int64()
+        _check(_lib.gmg_export_owned_leaf_keys(self.h, C.byref(n), None, None))
+        k = np.empty(n.value, np.uint64)
+        lam = np.empty(n.value, np.int8)
+        _check(_lib.gmg_export_owned_leaf_keys(self.h, C.byref(n), _ptr(k), _ptr(lam)))
+        return k, lam
+
     def cell_dofs(self, level):
         n = C.c_int64()
         _check(_lib.gmg_export_cell_dofs(self.h, level, C.byref(n), None))
@@ -588,7 +644,7 @@ class NcclComm:
 
 def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_degree=4, rank=0,
               coef_level2=None, graph=True, device=-1, comm=None, mixed=False,
-              coarse="cholesky", allocator=None) -> Hierarchy:
+              coarse="cholesky", allocator=None, rank_local=False, eig_key=False) -> Hierarchy:
     """comm: None (one rank), a LocalWorld (ranks as threads), a HostWorld (ranks
     as processes, host-staged) or an NcclComm.  allocator: None (cudaMalloc) or
     "torch" (the torch caching allocator through gmg_params.dev_alloc/dev_free)."""
@@ -599,7 +655,8 @@ def gmg_setup(forest: Forest, part: Partitioning, k=2, host_only=False, cheb_deg
     p.n_ranks = part.n_ranks
     p.device = device
     p.flags = (GMG_HOST_ONLY if host_only else 0) | (0 if graph else GMG_NO_GRAPH) | \
-        (GMG_MIXED_PRECISION if mixed else 0)
+        (GMG_MIXED_PRECISION if mixed else 0) | (GMG_RANK_LOCAL if rank_local else 0) | \
+        (GMG_EIG_KEY if eig_key else 0)
     p.coarse_solver = {"cholesky": 0, "chebyshev": 1}[coarse]
     if isinstance(comm, LocalWorld):
         p.flags |= GMG_LOCAL_RANKS

@@ -15,9 +15,18 @@ struct gmg_partitioning {
   const gmg_forest* forest;
   gmg::Partition p;
 };
+// Global sizes reported by gmg_hierarchy_info: from the global Topology, or, for
+// rank-local builds (GMG_RANK_LOCAL), the per-rank counts summed over the ranks.
+struct GlobalSizes {
+  int dim = 2, k = 2, L = 0, n_ranks = 1;
+  gmg::i64 n_leaf_nodes = -1, n_leaf_free = -1, hanging = -1, dirichlet = -1, n0 = 0;
+  std::vector<gmg::i64> dofs, cells, fams, S, E, B, leaf_cells;
+};
+
 struct gmg_hierarchy {
-  gmg::Topology topo;
+  gmg::Topology topo;          // global level numbering (empty for GMG_RANK_LOCAL builds)
   gmg::LocalTopo local;
+  GlobalSizes sz;
   gmg_params prm{};
   gmg::DeviceHierarchy* dev = nullptr;
   ~gmg_hierarchy() { gmg::device_destroy(dev); }
@@ -57,7 +66,11 @@ gmg::DeviceHierarchy* need_dev(gmg_hierarchy* h) {
   return h->dev;
 }
 void need_level(const gmg_hierarchy* h, int level) {
-  GMG_REQUIRE(level >= 0 && level <= h->topo.L, GMG_E_INVALID_ARG, "level out of range");
+  GMG_REQUIRE(level >= 0 && level <= h->sz.L, GMG_E_INVALID_ARG, "level out of range");
+}
+void need_global(const gmg_hierarchy* h) {
+  GMG_REQUIRE(!h->local.rank_local, GMG_E_STATE,
+              "global level numbering not available for a GMG_RANK_LOCAL hierarchy (use gmg_export_local_level)");
 }
 }  // namespace
 
@@ -226,30 +239,103 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
                 GMG_E_INVALID_ARG, "coarse_solver");
     auto h = std::make_unique<gmg_hierarchy>();
     h->prm = *prm;
-    h->topo = gmg::make_topology(f->f, p->p, prm->k);
-    h->local = gmg::make_local(f->f, p->p, h->topo, prm->rank);
-    if (!(prm->flags & GMG_HOST_ONLY)) {
-      if (prm->coef_level2) gmg::attach_coefficients(h->local, f->f, p->p, prm->coef_level2);
-      std::unique_ptr<gmg::Comm> comm;
-      if (prm->n_ranks > 1) {
-        GMG_REQUIRE(prm->nccl_comm != nullptr, GMG_E_INVALID_ARG, "n_ranks > 1 needs a communicator");
-        if (prm->flags & GMG_HOST_RANKS) {
-          auto* w = static_cast<gmg::HostWorld*>(prm->nccl_comm);
-          GMG_REQUIRE(w->n == prm->n_ranks && w->rank == prm->rank, GMG_E_INVALID_ARG,
-                      "host world rank/size != params");
-          comm = std::make_unique<gmg::HostComm>(w);
-        } else if (prm->flags & GMG_LOCAL_RANKS) {
-          auto* w = static_cast<gmg::LocalWorld*>(prm->nccl_comm);
-          GMG_REQUIRE(w->n == prm->n_ranks, GMG_E_INVALID_ARG, "local world size != n_ranks");
-          comm = std::make_unique<gmg::ThreadComm>(w, prm->rank);
-        } else {
-          auto c = std::make_unique<gmg::NcclComm>(prm->nccl_comm);
-          GMG_REQUIRE(c->size() == prm->n_ranks && c->rank() == prm->rank, GMG_E_INVALID_ARG,
-                      "NCCL communicator rank/size != params");
-          comm = std::move(c);
-        }
+    const bool rank_local = (prm->flags & GMG_RANK_LOCAL) != 0;
+    const bool eig_key = rank_local || (prm->flags & GMG_EIG_KEY) != 0;
+    const bool host_only = (prm->flags & GMG_HOST_ONLY) != 0;
+    std::unique_ptr<gmg::Comm> comm;
+    if (!host_only && prm->n_ranks > 1) {
+      GMG_REQUIRE(prm->nccl_comm != nullptr, GMG_E_INVALID_ARG, "n_ranks > 1 needs a communicator");
+      if (prm->device >= 0) {
+        cudaError_t e = cudaSetDevice(prm->device);
+        GMG_REQUIRE(e == cudaSuccess, GMG_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
       }
-      h->dev = gmg::device_create(h->local, *prm, std::move(comm), h->topo.lv[0].n_dofs);
+      if (prm->flags & GMG_HOST_RANKS) {
+        auto* w = static_cast<gmg::HostWorld*>(prm->nccl_comm);
+        GMG_REQUIRE(w->n == prm->n_ranks && w->rank == prm->rank, GMG_E_INVALID_ARG,
+                    "host world rank/size != params");
+        comm = std::make_unique<gmg::HostComm>(w);
+      } else if (prm->flags & GMG_LOCAL_RANKS) {
+        auto* w = static_cast<gmg::LocalWorld*>(prm->nccl_comm);
+        GMG_REQUIRE(w->n == prm->n_ranks, GMG_E_INVALID_ARG, "local world size != n_ranks");
+        comm = std::make_unique<gmg::ThreadComm>(w, prm->rank);
+      } else {
+        auto c = std::make_unique<gmg::NcclComm>(prm->nccl_comm);
+        GMG_REQUIRE(c->size() == prm->n_ranks && c->rank() == prm->rank, GMG_E_INVALID_ARG,
+                    "NCCL communicator rank/size != params");
+        comm = std::move(c);
+      }
+    }
+    GlobalSizes& z = h->sz;
+    const gmg::Partition& P = p->p;
+    z.dim = f->f.dim;
+    z.k = prm->k;
+    z.L = f->f.L;
+    z.n_ranks = prm->n_ranks;
+    const int nch = 1 << z.dim;
+    for (int l = 0; l <= z.L; ++l) {
+      const auto& c = P.levels[l];
+      z.cells.push_back((gmg::i64)c.key.size());
+      z.fams.push_back(l == 0 ? 0 : (gmg::i64)c.key.size() / nch);
+      gmg::i64 nl = 0;
+      for (auto x : c.leaf) nl += x ? 1 : 0;
+      z.leaf_cells.push_back(nl);
+    }
+    if (!rank_local) {
+      h->topo = gmg::make_topology(f->f, P, prm->k);
+      h->local = gmg::make_local(f->f, P, h->topo, prm->rank, eig_key);
+      const auto& T = h->topo;
+      z.n_leaf_nodes = T.n_leaf_nodes;
+      z.n_leaf_free = T.n_leaf;
+      z.hanging = T.n_hanging;
+      z.dirichlet = T.n_dirichlet;
+      z.n0 = T.lv[0].n_dofs;
+      for (int l = 0; l <= z.L; ++l) {
+        z.dofs.push_back(T.lv[l].n_dofs);
+        z.S.push_back(T.lv[l].nS);
+        z.E.push_back(T.lv[l].nE);
+        z.B.push_back(T.lv[l].nB);
+      }
+    } else {
+      gmg::LocalCounts lc;
+      h->local = gmg::make_local_direct(f->f, P, prm->k, prm->rank, true, &lc);
+      // one sum over the ranks: [S | E | B | own_S | own_dofs] per level, 4 scalars,
+      // and the owned leaf DoFs of every rank (slot r) for the leaf offsets
+      const int nl = z.L + 1, R = prm->n_ranks;
+      std::vector<double> v;
+      for (auto* a : {&lc.S, &lc.E, &lc.B, &lc.own_S, &lc.own_dofs}) v.insert(v.end(), a->begin(), a->end());
+      v.push_back(lc.leaf_nodes);
+      v.push_back(lc.hanging);
+      v.push_back(lc.dirichlet);
+      v.push_back(lc.leaf_free);
+      std::vector<double> leafc(R, 0.0);
+      leafc[prm->rank] = (double)h->local.n_leaf_owned;
+      v.insert(v.end(), leafc.begin(), leafc.end());
+      const bool summed = comm != nullptr || R == 1;
+      gmg::comm_allreduce_host(comm.get(), v);
+      auto at = [&](int blk, int l) { return (gmg::i64)v[(size_t)blk * nl + l]; };
+      for (int l = 0; l < nl; ++l) {
+        z.S.push_back(summed ? at(0, l) : -1);
+        z.E.push_back(summed ? at(1, l) : -1);
+        z.B.push_back(summed ? at(2, l) : -1);
+        z.dofs.push_back(summed ? at(4, l) : -1);
+        h->local.lv[l].nS_global = summed ? at(3, l) : -1;
+      }
+      const size_t o = (size_t)5 * nl;
+      if (summed) {
+        z.n_leaf_nodes = (gmg::i64)v[o];
+        z.hanging = (gmg::i64)v[o + 1];
+        z.dirichlet = (gmg::i64)v[o + 2];
+        z.n_leaf_free = (gmg::i64)v[o + 3];
+        gmg::i64 first = 0;
+        for (int q = 0; q < prm->rank; ++q) first += (gmg::i64)v[o + 4 + q];
+        h->local.leaf_first = first;
+        h->local.n_leaf_global = z.n_leaf_free;
+      }
+      z.n0 = summed ? at(4, 0) : h->local.lv[0].n_owned;
+    }
+    if (!host_only) {
+      if (prm->coef_level2) gmg::attach_coefficients(h->local, f->f, P, prm->coef_level2);
+      h->dev = gmg::device_create(h->local, *prm, std::move(comm), z.n0);
     }
     *out = h.release();
   });
@@ -273,28 +359,27 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
     NEED(h);
     NEED(o);
     std::memset(o, 0, sizeof *o);
-    const auto& T = h->topo;
-    o->dim = T.dim;
-    o->k = T.k;
-    o->n_levels = T.L + 1;
-    o->n_ranks = T.n_ranks;
+    const GlobalSizes& z = h->sz;
+    o->dim = z.dim;
+    o->k = z.k;
+    o->n_levels = z.L + 1;
+    o->n_ranks = z.n_ranks;
     o->rank = h->prm.rank;
-    o->n_leaf_nodes = T.n_leaf_nodes;
-    o->n_leaf_free = T.n_leaf;
-    o->n_leaf_hanging = T.n_hanging;
-    o->n_leaf_dirichlet = T.n_dirichlet;
+    o->n_leaf_nodes = z.n_leaf_nodes;
+    o->n_leaf_free = z.n_leaf_free;
+    o->n_leaf_hanging = z.hanging;
+    o->n_leaf_dirichlet = z.dirichlet;
     o->n_owned = h->local.n_leaf_owned;
     o->first_owned = h->local.leaf_first;
     gmg::i64 mg = 0;
-    for (int l = 0; l <= T.L && l < GMG_MAX_LEVELS; ++l) {
-      const auto& t = T.lv[l];
-      o->level_dofs[l] = t.n_dofs;
-      o->level_cells[l] = t.n_cells;
-      o->level_families[l] = t.n_fam;
-      o->level_S[l] = t.nS;
-      o->level_E[l] = t.nE;
-      o->level_B[l] = t.nB;
-      o->level_leaf_cells[l] = (gmg::i64)t.leaf_cells.size();
+    for (int l = 0; l <= z.L && l < GMG_MAX_LEVELS; ++l) {
+      o->level_dofs[l] = z.dofs[l];
+      o->level_cells[l] = z.cells[l];
+      o->level_families[l] = z.fams[l];
+      o->level_S[l] = z.S[l];
+      o->level_E[l] = z.E[l];
+      o->level_B[l] = z.B[l];
+      o->level_leaf_cells[l] = z.leaf_cells[l];
       o->level_r1[l] = h->dev ? gmg::device_level_r1(h->dev, l) : 0;
       o->level_gf[l] = h->dev ? gmg::device_level_gf(h->dev, l) : 0;
       // this rank's level vector (owned + ghosts), padded like the device segments (kernels.cuh VEC_PAD)
@@ -307,6 +392,8 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
 gmg_status gmg_export_level_dofs(const gmg_hierarchy* h, int level, int64_t* n, uint64_t* key, uint8_t* cls,
                                  int32_t* owner, int64_t* canonical) {
   return guard([&] {
+    NEED(h);
+    need_global(h);
     NEED(h);
     NEED(n);
     need_level(h, level);
@@ -325,6 +412,8 @@ gmg_status gmg_export_leaf_dofs(const gmg_hierarchy* h, int64_t* n, uint64_t* ke
                                 int64_t* canonical) {
   return guard([&] {
     NEED(h);
+    need_global(h);
+    NEED(h);
     NEED(n);
     const auto& T = h->topo;
     *n = T.n_leaf;
@@ -342,6 +431,7 @@ gmg_status gmg_export_rank_level(const gmg_hierarchy* h, int level, int64_t* fir
   return guard([&] {
     NEED(h);
     need_level(h, level);
+    need_global(h);
     const auto& v = h->local.lv[level];
     if (first_owned) *first_owned = v.first_owned;
     if (n_owned) *n_owned = v.n_owned;
@@ -383,6 +473,58 @@ gmg_status gmg_local_world_destroy(void* world) {
   return guard([&] { delete static_cast<gmg::LocalWorld*>(world); });
 }
 
+gmg_status gmg_export_local_level(const gmg_hierarchy* h, int level, int64_t* n_owned, int64_t* n_ghost,
+                                  uint64_t* owned_key, uint64_t* ghost_key, int32_t* ghost_owner, int32_t* n_peers,
+                                  int32_t* peers, int64_t* send_off, int64_t* recv_off, int32_t* send_idx,
+                                  int32_t* recv_idx) {
+  return guard([&] {
+    NEED(h);
+    need_level(h, level);
+    const auto& v = h->local.lv[level];
+    if (n_owned) *n_owned = v.n_owned;
+    if (n_ghost) *n_ghost = v.n_ghost;
+    if (n_peers) *n_peers = (int32_t)v.peers.size();
+    if (owned_key) std::copy(v.owned_key.begin(), v.owned_key.end(), owned_key);
+    if (ghost_key) std::copy(v.ghost_key.begin(), v.ghost_key.end(), ghost_key);
+    if (ghost_owner) std::copy(v.ghost_owner.begin(), v.ghost_owner.end(), ghost_owner);
+    if (peers) std::copy(v.peers.begin(), v.peers.end(), peers);
+    if (send_off) std::copy(v.send_off.begin(), v.send_off.end(), send_off);
+    if (recv_off) std::copy(v.recv_off.begin(), v.recv_off.end(), recv_off);
+    if (send_idx) std::copy(v.send_idx.begin(), v.send_idx.end(), send_idx);
+    if (recv_idx) std::copy(v.recv_idx.begin(), v.recv_idx.end(), recv_idx);
+  });
+}
+
+gmg_status gmg_export_local_tables(const gmg_hierarchy* h, int level, int64_t* n_cells, int64_t* n_fam,
+                                   int32_t* cell_dofs, int32_t* xfer, uint8_t* cls, uint8_t* lam, double* eig_v,
+                                   int64_t* cell_global) {
+  return guard([&] {
+    NEED(h);
+    need_level(h, level);
+    GMG_REQUIRE(h->dev == nullptr, GMG_E_STATE, "local tables are exported from GMG_HOST_ONLY hierarchies "
+                                                "(device setup reorders them)");
+    const auto& v = h->local.lv[level];
+    if (n_cells) *n_cells = v.n_cells;
+    if (n_fam) *n_fam = v.n_fam;
+    if (cell_dofs) std::copy(v.cell_dofs.begin(), v.cell_dofs.end(), cell_dofs);
+    if (xfer) std::copy(v.xfer.begin(), v.xfer.end(), xfer);
+    if (cls) std::copy(v.cls.begin(), v.cls.end(), cls);
+    if (lam) std::copy(v.lam.begin(), v.lam.end(), lam);
+    if (eig_v) std::copy(v.eig_v.begin(), v.eig_v.end(), eig_v);
+    if (cell_global) std::copy(v.cell_global.begin(), v.cell_global.end(), cell_global);
+  });
+}
+
+gmg_status gmg_export_owned_leaf_keys(const gmg_hierarchy* h, int64_t* n, uint64_t* key, int8_t* lambda) {
+  return guard([&] {
+    NEED(h);
+    NEED(n);
+    *n = h->local.n_leaf_owned;
+    if (key) std::copy(h->local.leaf_key.begin(), h->local.leaf_key.end(), key);
+    if (lambda) std::copy(h->local.leaf_level.begin(), h->local.leaf_level.end(), lambda);
+  });
+}
+
 gmg_status gmg_forest_count_nodes(const gmg_forest* f, int k, int64_t* n_nodes) {
   return guard([&] {
     NEED(f);
@@ -418,6 +560,8 @@ gmg_status gmg_host_world_destroy(void* world) {
 
 gmg_status gmg_export_cell_dofs(const gmg_hierarchy* h, int level, int64_t* n_cells, int64_t* dofs) {
   return guard([&] {
+    NEED(h);
+    need_global(h);
     NEED(h);
     NEED(n_cells);
     need_level(h, level);

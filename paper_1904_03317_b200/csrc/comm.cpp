@@ -28,7 +28,7 @@ LocalWorld::LocalWorld(int n_) : n(n_), slot(n_) {
   for (auto& s : slot) {
     CKC(cudaEventCreateWithFlags(&s.packed, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
-    CKC(cudaMallocHost(&s.red, 64 * sizeof(double)));
+    CKC(cudaMallocHost(&s.red, 4096 * sizeof(double)));
   }
 }
 LocalWorld::~LocalWorld() {
@@ -79,7 +79,7 @@ void ThreadComm::exchange(const std::vector<int>& peers, const double* sendbuf, 
 }
 
 void ThreadComm::allreduce(double* buf, int n, cudaStream_t s) {
-  GMG_REQUIRE(n <= 64, GMG_E_INVALID_ARG, "allreduce size");
+  GMG_REQUIRE(n <= 4096, GMG_E_INVALID_ARG, "allreduce size");
   auto& me = w->slot[r];
   CKC(cudaMemcpyAsync(me.red, buf, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));

@@ -87,6 +87,7 @@ struct DeviceHierarchy {
   int* coarse_idx = nullptr;
   bool use_graph = true;
   bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
+  int gf_slots = 1;             // grandfamilies per block of gfam_tensor_apply (GMG_GF_SLOTS = 1, 2, 3)
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
@@ -271,6 +272,20 @@ static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t v
   return 2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam;
 }
 
+template <int K, typename T, int TM, int SL>
+static void launch_gf(DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1, double c2, const T* xc,
+                      cudaStream_t s) {
+  static const bool attr = [] {
+    CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)dev::gf_smem_bytes<K, T, SL>()));
+    return true;
+  }();
+  (void)attr;
+  const int grid = (int)((v.n_gf + SL - 1) / SL);
+  dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
+      (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc);
+}
+
 // The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
 // plus the remaining families (fam_tensor_apply over the singles list), or all
 // families.  Epilogue mode TM, fused Chebyshev arguments as fam_tensor_apply.
@@ -279,15 +294,9 @@ static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, con
                           double c2, const T* xc, cudaStream_t s) {
   const int np = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), nn = (K + 1) * (K + 1) * (K + 1);
   if (v.n_gf > 0) {
-    static const bool attr = [] {
-      CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)dev::gf_smem_bytes<K, T>()));
-      return true;
-    }();
-    (void)attr;
-    const int grid = (int)((v.n_gf + dev::GF_SLOTS - 1) / dev::GF_SLOTS);
-    dev::gfam_tensor_apply<K, T, TM><<<grid, dev::GF_THREADS, dev::gf_smem_bytes<K, T>(), s>>>(
-        (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc);
+    if (d->gf_slots == 1) launch_gf<K, T, TM, 1>(v, x, y, g, dv, xw, c1, c2, xc, s);
+    else if (d->gf_slots == 2) launch_gf<K, T, TM, 2>(v, x, y, g, dv, xw, c1, c2, xc, s);
+    else launch_gf<K, T, TM, 3>(v, x, y, g, dv, xw, c1, c2, xc, s);
     d->launches++;
   }
   const i64 nf = v.n_gf > 0 ? v.n_single : v.n_fam;
@@ -788,6 +797,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     d->mixed = (prm.flags & GMG_MIXED_PRECISION) != 0;
     d->coarse_cheb = prm.coarse_solver == GMG_COARSE_CHEBYSHEV;
     if (const char* e = std::getenv("GMG_APPLY")) d->tensor_apply = std::string(e) != "cell";
+    if (const char* e = std::getenv("GMG_GF_SLOTS")) d->gf_slots = std::max(1, std::min(3, std::atoi(e)));
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
     const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
@@ -1011,6 +1021,26 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
 }
 
 long long device_mg_len(const DeviceHierarchy* d) { return d ? (long long)d->N : 0; }
+
+void comm_allreduce_host(Comm* comm, std::vector<double>& v) {
+  if (!comm || v.empty()) return;
+  double* buf = nullptr;
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    CK(cudaMalloc(&buf, v.size() * sizeof(double)));
+    CK(cudaMemcpyAsync(buf, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    comm->allreduce(buf, (int)v.size(), s);
+    CK(cudaMemcpyAsync(v.data(), buf, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    if (buf) cudaFree(buf);
+    cudaStreamDestroy(s);
+    throw;
+  }
+  cudaFree(buf);
+  cudaStreamDestroy(s);
+}
 
 long long device_level_gf(const DeviceHierarchy* d, int level) {
   return d && level >= 0 && level < (int)d->lv.size() ? (long long)d->lv[level].n_gf : 0;

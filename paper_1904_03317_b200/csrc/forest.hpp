@@ -133,6 +133,10 @@ struct LocalLevel {
   // local families whose parents are the 8 children of one level-(l-2) cell
   std::vector<i32> gf_first;
   std::vector<uint8_t> cls, lam;           // per local DoF (ghosts: lam = 0)
+  // rank-local builds (make_local_direct): finest-lattice Morton keys of the owned
+  // DoFs and of the ghosts, and the ghosts' owners (ghost_global stays empty)
+  std::vector<u64> owned_key, ghost_key;
+  std::vector<i32> ghost_owner;
   std::vector<double> eig_v;               // eigen start vector on owned S DoFs
   i64 nS_global = 0;
   std::vector<i64> cell_global;            // global index (in C_l) of each local cell
@@ -145,13 +149,35 @@ struct LocalLevel {
 
 struct LocalTopo {
   int rank = 0, n_ranks = 1, dim = 2, k = 2, L = 0;
+  bool rank_local = false;                 // built by make_local_direct (no global numbering)
   std::vector<LocalLevel> lv;
   i64 n_leaf_owned = 0, leaf_first = 0, n_leaf_global = 0;
   std::vector<int8_t> leaf_level;          // per owned leaf DoF
   std::vector<i64> leaf_local;             // local index at its level
+  std::vector<u64> leaf_key;               // rank-local builds: finest-lattice key per owned leaf DoF
+  struct LeafRec {
+    u64 key;
+    int8_t level;
+    i64 local;
+  };
+  std::vector<LeafRec> leaf_tmp;
 };
 
-LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank);
+// eig_key: eigen start vector -5.5 + (level-lattice Morton key mod 12) on the
+// owned S DoFs (reading R10b) instead of the canonical-rank pattern (R10)
+LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank, bool eig_key = false);
+
+// Per-rank contributions to the global sizes of a rank-local build, summed over
+// ranks by the caller (every node counted by exactly one rank).
+struct LocalCounts {
+  std::vector<double> S, E, B, own_S, own_dofs;   // per level
+  double leaf_nodes = 0, hanging = 0, dirichlet = 0, leaf_free = 0;
+  void resize(int L) {
+    for (auto* v : {&S, &E, &B, &own_S, &own_dofs}) v->assign(L + 1, 0.0);
+  }
+};
+LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank, bool eig_key,
+                            LocalCounts* counts);
 
 // Piecewise-constant coefficient per level-2 cell (config 4): coef2[i] belongs to
 // the i-th cell of C_2 in SFC order.  Fills the coefficient fields of every level.

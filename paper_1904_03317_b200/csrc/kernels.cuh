@@ -625,12 +625,12 @@ __host__ __device__ __forceinline__ constexpr double Mt4(int i, int j) {
   return s;
 }
 
-constexpr int GF_SLOTS = 3;           // grandfamilies per block: 3 x 81 = 243 of 256 lanes busy
-constexpr int GF_THREADS = 256;
-#ifndef GF_MIN_BLOCKS_DEFAULT
-#define GF_MIN_BLOCKS_DEFAULT 3
-#endif
-constexpr int GF_MIN_BLOCKS = GF_MIN_BLOCKS_DEFAULT;   // register cap 65536 / (256 x 3) = 85
+// Grandfamilies per block (SLOTS) and threads: 1 -> 96 (81 lanes busy), 2 -> 192,
+// 3 -> 256 (243 busy); the minimum-blocks bound caps registers at ~80.
+template <int SLOTS> struct GfBlock {
+  static constexpr int THREADS = SLOTS == 1 ? 96 : (SLOTS == 2 ? 192 : 256);
+  static constexpr int MIN_BLOCKS = 65536 / (THREADS * 80);
+};
 template <int K> struct GfShape {
   static constexpr int N1 = 4 * K + 1, NL = N1 * N1, NP = N1 * N1 * N1;
   static constexpr int NCP = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);   // G's family patch one level up
@@ -659,13 +659,13 @@ template <int K> struct GfLayout {
   static constexpr int SS = SA > SB ? (SA > SN ? SA : SN) : (SB > SN ? SB : SN);
   static constexpr int SLOT = SS + ((17 - SS % 16) % 16);   // = 1 mod 16
 };
-template <int K, typename T>
+template <int K, typename T, int SLOTS>
 constexpr size_t gf_smem_bytes() {
-  return sizeof(T) * 2 * GF_SLOTS * GfLayout<K>::SLOT + (size_t)sizeof(T) * GF_SLOTS * (GfShape<K>::NCP + 1);
+  return sizeof(T) * 2 * SLOTS * GfLayout<K>::SLOT + (size_t)sizeof(T) * SLOTS * (GfShape<K>::NCP + 1);
 }
 
-template <int K, typename T, int TM = TA_APPLY>
-__global__ void __launch_bounds__(GF_THREADS, GF_MIN_BLOCKS)
+template <int K, typename T, int TM, int GF_SLOTS>
+__global__ void __launch_bounds__(GfBlock<GF_SLOTS>::THREADS, GfBlock<GF_SLOTS>::MIN_BLOCKS)
 gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict__ gcoef, double scale_,
                   const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                   const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,

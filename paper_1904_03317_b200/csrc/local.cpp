@@ -11,7 +11,7 @@ namespace gmg {
 
 static inline i64 decode_enc(i32 v) { return v >= 0 ? (i64)v : (v <= -2 ? -2 - (i64)v : -1); }
 
-LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank) {
+LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int rank, bool eig_key) {
   const int d = T.dim, k = T.k, L = T.L, P = p.n_ranks;
   GMG_REQUIRE(rank >= 0 && rank < P, GMG_E_INVALID_ARG, "rank out of range");
   int nn = 1, np = 1;
@@ -158,19 +158,40 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     const i64 nloc = v.n_local();
     v.cls.resize(nloc);
     v.lam.assign(nloc, 0);
+    v.owned_key.resize(v.n_owned);
+    v.ghost_key.resize(v.n_ghost);
+    v.ghost_owner.resize(v.n_ghost);
     for (i64 i = 0; i < nloc; ++i) {
       const i64 g = i < v.n_owned ? v.first_owned + i : v.ghost_global[i - v.n_owned];
       v.cls[i] = t.dof_cls[g];
-      if (i < v.n_owned) v.lam[i] = t.dof_lam[g];
+      if (i < v.n_owned) {
+        v.lam[i] = t.dof_lam[g];
+        v.owned_key[i] = t.dof_key[g];
+      } else {
+        v.ghost_key[i - v.n_owned] = t.dof_key[g];
+        v.ghost_owner[i - v.n_owned] = t.dof_owner[g];
+      }
     }
-    // eigen start vector: -5.5 + (canonical S rank mod 12) on owned S DoFs (R10)
+    // eigen start vector on owned S DoFs: -5.5 + (canonical S rank mod 12) (R10) or,
+    // eig_key, -5.5 + (level-lattice Morton key mod 12) (R10b, the rank-local form)
     v.eig_v.assign(nloc, 0.0);
-    i64 cs = 0;
-    for (i64 c = 0; c < t.n_dofs; ++c) {
-      const i64 g = t.canon_to_global[c];
-      if (t.dof_cls[g] != CLS_S) continue;
-      if (g >= v.first_owned && g < v.first_owned + v.n_owned) v.eig_v[g - v.first_owned] = -5.5 + (double)(cs % 12);
-      ++cs;
+    if (eig_key) {
+      for (i64 i = 0; i < v.n_owned; ++i) {
+        const i64 g = v.first_owned + i;
+        if (t.dof_cls[g] != CLS_S) continue;
+        const Vec3 X = unmorton(d, t.dof_key[g]);
+        Vec3 Y{0, 0, 0};
+        for (int j = 0; j < d; ++j) Y[j] = X[j] >> (L - l);
+        v.eig_v[i] = -5.5 + (double)(morton(d, Y) % 12);
+      }
+    } else {
+      i64 cs = 0;
+      for (i64 c = 0; c < t.n_dofs; ++c) {
+        const i64 g = t.canon_to_global[c];
+        if (t.dof_cls[g] != CLS_S) continue;
+        if (g >= v.first_owned && g < v.first_owned + v.n_owned) v.eig_v[g - v.first_owned] = -5.5 + (double)(cs % 12);
+        ++cs;
+      }
     }
     if (l > 0) {
       const int row = np + nn;
@@ -209,6 +230,7 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     if (first < 0) first = g;
     const int l = T.leaf_lambda[g];
     Lt.leaf_level.push_back((int8_t)l);
+    Lt.leaf_key.push_back(T.leaf_key[g]);
     Lt.leaf_local.push_back(T.leaf_level_index[g] - Lt.lv[l].first_owned);
     GMG_REQUIRE(Lt.leaf_local.back() >= 0 && Lt.leaf_local.back() < Lt.lv[l].n_owned, GMG_E_STATE,
                 "leaf DoF not owned at its lambda level");

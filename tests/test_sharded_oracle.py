@@ -249,3 +249,71 @@ def test_host_world_rejects_bad_arguments():
         G.HostWorld("no_slash", 2, 0)
     with pytest.raises(G.GmgError):
         G.HostWorld("/gmg_x", 2, 5)
+
+
+# ------------------------------------------------------------------ rank-local builds vs the oracle
+RL_CASES = [("c1", None, 3, "first_child"), ("c3p2", None, 4, "first_child"), ("c3p2", None, 8, "first_child"),
+            ("c4s", None, 3, "per_level"), ("brick8", 1, 5, "first_child")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,k,p,mode", RL_CASES)
+def test_rank_local_threads_vs_oracle(name, k, p, mode):
+    """GMG_RANK_LOCAL hierarchies (no global numbering; inputs and outputs
+    matched by node key) against the oracle: V-cycle 1e-10, CG +-1 / 1e-8."""
+    import torch
+    from gmg_inputs import uniform_pm1_keys
+    cfg = _cfg(name, k)
+    oh, _, _, it_ref, lams = _oracle(cfg)
+    from oracle import mg
+    okeys = oh.leaf.key[oh.leaf.free_index >= 0].astype(np.uint64)        # canonical (Morton) order
+    b_ref = uniform_pm1_keys(okeys)
+    x_ref = mg.vcycle(oh, b_ref)
+    world = G.LocalWorld(p)
+    lf = G.gmg_forest_generate(G.recipe_from_config(cfg))
+    part = G.gmg_partition(lf, p, mode=mode)
+    hs = [None] * p
+    streams = [torch.cuda.Stream() for _ in range(p)]
+
+    def setup(r):
+        def fn():
+            torch.cuda.set_device(0)
+            hs[r] = G.gmg_setup(lf, part, k=cfg["k"], rank=r, comm=world, coef_level2=_coef(cfg), rank_local=True)
+            for l, lam in enumerate(lams, start=1):
+                hs[r].set_eigen(l, lam)
+        return fn
+
+    _run_threads([setup(r) for r in range(p)])
+    assert hs[0].info()["n_leaf_free"] == oh.leaf.n_free
+    res = [None] * p
+
+    def work(r):
+        def fn():
+            torch.cuda.set_device(0)
+            keys, _ = hs[r].owned_leaf_keys()
+            s = streams[r]
+            with torch.cuda.stream(s):
+                b = torch.tensor(uniform_pm1_keys(keys), device="cuda", dtype=torch.float64)
+                x = torch.zeros_like(b)
+                hs[r].vcycle(b, x, stream=s.cuda_stream)
+                rhs = torch.zeros_like(b)
+                hs[r].rhs_constant(1.0, rhs, stream=s.cuda_stream)
+                xs = torch.zeros_like(b)
+                it, _, _ = hs[r].solve_cg(rhs, xs, rtol=1e-8, stream=s.cuda_stream)
+                s.synchronize()
+            res[r] = (keys, x.cpu().numpy(), xs.cpu().numpy(), it)
+        return fn
+
+    _run_threads([work(r) for r in range(p)])
+    keys = np.concatenate([q[0] for q in res])
+    order = np.argsort(keys)
+    assert np.array_equal(keys[order], okeys)
+    xv = np.concatenate([q[1] for q in res])[order]
+    xsv = np.concatenate([q[2] for q in res])[order]
+    assert len({q[3] for q in res}) == 1
+    assert _rel(xv, x_ref) <= VC_TOL, _rel(xv, x_ref)
+    assert abs(res[0][3] - it_ref) <= 1
+    tr = np.linalg.norm(oh.b_leaf - oh.A_leaf @ xsv) / np.linalg.norm(oh.b_leaf)
+    assert tr <= 1.01e-8, tr
+    for h in hs:
+        h.close()
