@@ -327,16 +327,24 @@ def measure(ctx, args, name, main=True):
     coef = None
     if cfg.get("coef") == "level2_log_uniform":        # config 4: a per level-2 cell (SFC order)
         coef = log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+    # N > 1: rank-local setup (only this rank's part of the level topology,
+    # P:529-539); inputs drawn by node key (independent of N)
+    rank_local = ctx.world > 1
     h = G.gmg_setup(f, part, k=cfg["k"], rank=ctx.rank, comm=ctx.comm, mixed=mixed, coef_level2=coef,
-                    cheb_degree=args.cheb_degree, device=ctx.gpu)
+                    cheb_degree=args.cheb_degree, device=ctx.gpu, rank_local=rank_local)
     setup_s = time.time() - t0
     info = h.info()
     n_dofs = info["n_leaf_nodes"]
-    fo, n_own = info["first_owned"], info["n_owned"]
-    canon = h.leaf_dofs()[3]
-    b_can = uniform_pm1(info["n_leaf_free"])
-    b_host = np.ascontiguousarray(b_can[canon[fo:fo + n_own]])
-    del canon, b_can
+    n_own = info["n_owned"]
+    if rank_local:
+        from gmg_inputs import uniform_pm1_keys
+        b_host = np.ascontiguousarray(uniform_pm1_keys(h.owned_leaf_keys()[0]))
+    else:
+        fo = info["first_owned"]
+        canon = h.leaf_dofs()[3]
+        b_can = uniform_pm1(info["n_leaf_free"])
+        b_host = np.ascontiguousarray(b_can[canon[fo:fo + n_own]])
+        del canon, b_can
     b = torch.tensor(b_host, device=ctx.dev, dtype=torch.float64)
     x = torch.zeros_like(b)
     stream = torch.cuda.current_stream()
@@ -458,6 +466,7 @@ def measure(ctx, args, name, main=True):
     res["cg"] = {"iters": its, "rel_res": relres, "seconds": t_cg, "rtol": 1e-8, "dofs_per_s": n_dofs / t_cg}
     model = part.model()
     res["partition_eta"] = model["eta"]
+    res["setup"] = "rank-local (GMG_RANK_LOCAL)" if rank_local else "global numbering"
     res["ghost_children_ratio"] = sum(model["ghost_children"]) / max(sum(model["children"]), 1)
     res["mg_vector_mb"] = info["mg_vector_len"] * (4 if mixed else 8) / 1e6
     h.close()
@@ -500,7 +509,8 @@ def run_ours(args):
                           "parallelism": "single GPU" if ctx.world == 1 else
                           f"{ctx.world} ranks, SFC partition ({args.partition}), {args.transport} ghost exchange",
                           "partition": args.partition, "partition_eta": main["partition_eta"],
-                          "ghost_children_ratio": main["ghost_children_ratio"], "setup_s": main["setup_s"]},
+                          "ghost_children_ratio": main["ghost_children_ratio"], "setup_s": main["setup_s"],
+                          "setup": main["setup"]},
                "roofline": main["roofline"], "apply_plain": main["apply_plain"], "kernels": main["kernels"],
                "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
                "launches_per_vcycle": main["launches_per_vcycle"], "clocks": main["clocks"], "cg": main["cg"]}
@@ -514,6 +524,46 @@ def run_ours(args):
                 "setup_s": sec["setup_s"]}}
         print(json.dumps(out), flush=True)
     ctx.close()
+
+
+def dry_run(args):
+    """--dry-run: every rank builds its part of the hierarchy on the host only
+    (rank-local topology, no GPU) and reports setup time and peak host RSS; rank 0
+    prints one JSON line (not a bench line).  Shows that the N-rank setup of a
+    config fits the host: `python bench.py --gpus 8 --config c5 --dry-run`."""
+    import resource
+    import torch.distributed as dist
+    import paper_1904_03317_b200 as G
+    from gmg_inputs import config, config_c5
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = config_c5(world) if args.config == "c5" else config(args.config)
+    t0 = time.time()
+    f = G.gmg_forest_generate(G.recipe_from_config(cfg))
+    t_forest = time.time() - t0
+    part = G.gmg_partition(f, world, mode=args.partition)
+    t_part = time.time() - t0 - t_forest
+    h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, host_only=True, rank_local=True)
+    t_setup = time.time() - t0
+    info = h.info()
+    mine = {"rank": rank, "setup_s": round(t_setup, 1), "forest_s": round(t_forest, 1), "partition_s": round(t_part, 1),
+            "max_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 2),
+            "owned_leaf_dofs": info["n_owned"],
+            "owned_level_dofs": [int(h.local_level(l)["owned_key"].size) for l in range(info["n_levels"])],
+            "ghost_level_dofs": [int(h.local_level(l)["ghost_key"].size) for l in range(info["n_levels"])]}
+    allv = [mine]
+    if world > 1:
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+    if rank == 0:
+        m = part.model()
+        print(json.dumps({"dry_run": True, "config": args.config, "n_ranks": world,
+                          "n_leaves": f.info()["n_leaves"], "levels": info["n_levels"],
+                          "partition_eta": m["eta"], "ranks": allv}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def relaunch(args):
@@ -544,6 +594,8 @@ def main():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
                     help="fp64 V-cycle (default, BASELINE) or fp32 V-cycle inside the fp64 CG (P:897)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host-only rank-local setup of every rank, reports time and host RSS (no GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -552,6 +604,9 @@ def main():
         return 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args)
+    if args.dry_run:
+        dry_run(args)
+        return 0
     run_ours(args)
     return 0
 

@@ -118,9 +118,10 @@ CONFIGS = {
                shell=(4, 1024), passes=7),
 }
 
-# config 5 for n GPUs: w_n / 2^-10.  n = 1 is measured; n > 1 are estimates from
-# the measured growth (~19M nodes per 2^-10 of half-width) pending a count on a
-# host large enough to build the 0.25-1B node forests.
+# config 5 for n GPUs: w_n / 2^-10, the smallest multiple giving >= 125M n leaf
+# nodes, counted exactly (tools/count_c5.py -> profiles/c5_shell_counts.json):
+# n = 1: 125,785,013 (m = 3: 106,745,081); n = 2: 258,586,909 (m = 10: 239,752,501);
+# n = 4: 506,559,201 (m = 23: 487,502,405); n = 8: 1,008,420,977 (m = 49: 988,810,125).
 C5_SHELL = {1: 4, 2: 11, 4: 24, 8: 50}
 
 

@@ -8,20 +8,22 @@
 // Produces the same LocalTopo as make_local (local.cpp) from the global
 // Topology -- same owned/ghost sets and local order, exchange plans, cell /
 // family / transfer tables, classes, lambda slots, leaf DoFs -- but touches only
-// the families of this rank, the families whose parents contain the parents of
-// this rank's next-finer families, and their vertex neighbours (the "halo").
-// What needs other ranks' DoF counts (global leaf offset, global level sizes) is
-// summed by the caller's allreduce afterwards (LocalCounts); the global DoF
-// indices themselves are never formed (ghost_global stays empty; keys are kept).
+// the families of this rank, the families whose cells are parents of this
+// rank's next-finer families, and their vertex neighbours (the "halo").  What
+// needs other ranks' DoF counts (global leaf offset, global level sizes) is
+// summed by the caller afterwards (LocalCounts); global DoF indices are never
+// formed (ghost_global stays empty; keys are kept).
 //
 // Why the halo suffices.  A node of a family F (level l) lies in the closure of
 // F's parent P; every other family containing it has a parent touching P, i.e.
 // one of P's 3^d - 1 vertex neighbours.  So owner (min computing rank of the
 // families containing the node, R25), transfer owner (first such family of the
-// owner, R26), class (B: some neighbour of P outside the domain shares it; E: a
-// neighbour that is a leaf shares it) and the ranks that need the node (those
-// computing a containing family; those computing the next-finer family of a
-// containing refined cell) are all decided inside the halo.
+// owner, R26), class (B: a neighbour of P outside the domain shares it; E: a
+// neighbour that is a leaf shares it), lambda (a containing level-l cell is a
+// leaf) and the ranks that need the node (those computing a containing family;
+// those computing the next-finer family of a containing refined cell) are all
+// decided inside the halo.  Construction as topology.cpp: occurrences (key,
+// halo family, patch position) radix-sorted by key, one pass over equal keys.
 #include <numeric>
 
 #include "patch.hpp"
@@ -30,10 +32,42 @@ namespace gmg {
 
 namespace {
 
-struct Occ {
-  u64 key;
-  i64 fam;      // family index in C_l / nch (level >= 1) or cell index (level 0)
-  int a;        // patch position (level >= 1) or local node (level 0)
+// LSD radix sort of (64-bit key, 32-bit value) pairs by key; stable.
+void radix_sort_pairs32(std::vector<u64>& key, std::vector<u32>& val, int key_bits) {
+  const size_t n = key.size();
+  std::vector<u64> k2(n);
+  std::vector<u32> v2(n);
+  const int RB = 11, R = 1 << RB;
+  std::vector<size_t> cnt(R);
+  for (int shift = 0; shift < key_bits; shift += RB) {
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (size_t i = 0; i < n; ++i) cnt[(key[i] >> shift) & (R - 1)]++;
+    size_t s = 0;
+    for (int b = 0; b < R; ++b) {
+      size_t c = cnt[b];
+      cnt[b] = s;
+      s += c;
+    }
+    for (size_t i = 0; i < n; ++i) {
+      const size_t d = cnt[(key[i] >> shift) & (R - 1)]++;
+      k2[d] = key[i];
+      v2[d] = val[i];
+    }
+    key.swap(k2);
+    val.swap(v2);
+  }
+}
+
+// per level: what the next level needs from this one
+struct LevelKeep {
+  std::vector<i64> halo;          // halo families (level >= 1) or level-0 cells, sorted
+  std::vector<i32> node_of_occ;   // occurrence (halo position * np + a, or cell * nn + b) -> node
+  std::vector<i32> local;         // node -> local index (-1: not local or Dirichlet)
+  i64 pos_of(i64 fam) const {
+    auto it = std::lower_bound(halo.begin(), halo.end(), fam);
+    GMG_REQUIRE(it != halo.end() && *it == fam, GMG_E_STATE, "family outside the halo");
+    return (i64)(it - halo.begin());
+  }
 };
 
 }  // namespace
@@ -47,6 +81,7 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
   const i64 emax = std::max({f.ext[0], f.ext[1], f.ext[2]});
   const int cbits = bits_for((u64)(k * emax) << L);
   GMG_REQUIRE(cbits * d <= 64 && (d == 2 || cbits <= 21), GMG_E_DEPTH, "lattice keys exceed 64 bits");
+  const int kbits = cbits * d;
   PatchTables pt(d, k);
   const int nn = pt.nn, np = pt.np, nch = pt.nch;
   LocalTopo Lt;
@@ -60,7 +95,8 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
   LocalCounts cnt;
   cnt.resize(L);
 
-  // ---------------- helpers over the global partition (cells of every level, SFC order)
+  // ---------------- helpers over the global partition (cells of every level, SFC order;
+  // the cells of level l >= 1 are families of nch consecutive children)
   auto nfam_of = [&](int l) -> i64 { return l == 0 ? 0 : (i64)p.levels[l].key.size() / nch; };
   auto comp = [&](int l, i64 fi) -> int { return p.levels[l].owner[(size_t)fi * nch]; };   // computing rank
   auto cell_index = [&](int l, u64 key) -> i64 {
@@ -68,180 +104,207 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     auto it = std::lower_bound(ks.begin(), ks.end(), key);
     return (it != ks.end() && *it == key) ? (i64)(it - ks.begin()) : -1;
   };
-  // family (level l >= 1) of the children of level-(l-1) cell `pkey` (-1: not refined)
-  auto fam_of_parent = [&](int l, u64 pkey) -> i64 {
-    if (l > L) return -1;
-    const i64 c = cell_index(l, pkey << d);
-    return c < 0 ? -1 : c / nch;
-  };
   auto parent_key = [&](int l, i64 fi) -> u64 { return p.levels[l].key[(size_t)fi * nch] >> d; };
-  auto node_X = [&](int l, u64 pkey, int a) {   // finest-lattice coordinates of patch node a
-    const Vec3 G = unmorton(d, pkey);
+  auto X_of = [&](const Vec3& G, int l, const std::array<int, 3>& off, int mult) {
     Vec3 X{0, 0, 0};
-    for (int j = 0; j < d; ++j) X[j] = ((i64)2 * k * G[j] + pt.pa[a][j]) << (L - l);
+    for (int j = 0; j < d; ++j) X[j] = ((i64)mult * k * G[j] + off[j]) << (L - l);
     return X;
   };
+  // level-0 local node b of a cell: offsets on the level-0 node lattice
+  std::vector<std::array<int, 3>> off0(nn);
+  for (int b = 0; b < nn; ++b) {
+    int r = b;
+    for (int j = 0; j < 3; ++j) {
+      off0[b][j] = j < d ? r % (k + 1) : 0;
+      if (j < d) r /= (k + 1);
+    }
+  }
 
-  // ---------------- families computed here, per level
+  // ---------------- families computed here, per level (level 0: cells)
   std::vector<std::vector<i64>> mine(L + 1);
+  for (i64 c = 0; c < (i64)p.levels[0].key.size(); ++c)
+    if (p.levels[0].owner[c] == rank) mine[0].push_back(c);
   for (int l = 1; l <= L; ++l)
     for (i64 fi = 0; fi < nfam_of(l); ++fi)
       if (comp(l, fi) == rank) mine[l].push_back(fi);
-  std::vector<i64> mine0;
-  for (i64 c = 0; c < (i64)p.levels[0].key.size(); ++c)
-    if (p.levels[0].owner[c] == rank) mine0.push_back(c);
 
-  // per level: local index of every node this rank needs (by key), for the xfer
-  // rows of the next level
-  std::vector<std::vector<u64>> owned_keys(L + 1), ghost_keys(L + 1);
-  std::vector<std::vector<std::pair<u64, i32>>> keymap(L + 1);   // key -> local index
-
+  LevelKeep prev;   // level l-1
   for (int l = 0; l <= L; ++l) {
     LocalLevel& v = Lt.lv[l];
     v.level = l;
     v.first_owned = -1;
-    // ---------------- occurrences of the halo
-    std::vector<Occ> occ;
-    // needed: (key) of the nodes this rank needs
-    std::vector<u64> need;
+    LevelKeep cur;
+    const int stride = l == 0 ? nn : np;       // occurrences per halo entry
+    // ---------------- halo and what this rank needs of it
+    // needmask[h]: children of halo family h whose nodes this rank needs (parents of
+    // its level-(l+1) families); ismine[h]: h computed here (its whole patch needed)
+    std::vector<i64>& H = cur.halo;
     if (l == 0) {
-      const auto& c0 = p.levels[0];
-      for (i64 c = 0; c < (i64)c0.key.size(); ++c) {
-        const Vec3 G = unmorton(d, c0.key[c]);
-        for (int b = 0; b < nn; ++b) {
-          Vec3 X{0, 0, 0};
-          int r = b;
-          for (int j = 0; j < d; ++j) {
-            X[j] = ((i64)k * G[j] + r % (k + 1)) << L;
-            r /= (k + 1);
-          }
-          occ.push_back({morton(d, X), c, b});
-        }
-      }
-      std::vector<char> needc(c0.key.size(), 0);
-      for (i64 c : mine0) needc[c] = 1;
-      if (L >= 1)
-        for (i64 fi : mine[1]) needc[cell_index(0, parent_key(1, fi))] = 1;
-      for (const Occ& o : occ)
-        if (needc[o.fam]) need.push_back(o.key);
+      H.resize(p.levels[0].key.size());
+      std::iota(H.begin(), H.end(), 0);
     } else {
-      // families whose parents' nodes or patches this rank needs
       std::vector<i64> needfam = mine[l];
-      std::vector<std::pair<i64, int>> needcell;   // (family, child) parents of next-level families
       if (l < L)
-        for (i64 fi1 : mine[l + 1]) {
-          const u64 pk = parent_key(l + 1, fi1);                 // a level-l cell
-          const i64 c = cell_index(l, pk);
-          needfam.push_back(c / nch);
-          needcell.push_back({c / nch, (int)(c % nch)});
-        }
+        for (i64 f1 : mine[l + 1]) needfam.push_back(cell_index(l, parent_key(l + 1, f1)) / nch);
       std::sort(needfam.begin(), needfam.end());
       needfam.erase(std::unique(needfam.begin(), needfam.end()), needfam.end());
-      // halo: families whose parent is a vertex neighbour of a needed family's parent
-      std::vector<i64> halo;
       for (i64 fi : needfam) {
         const Vec3 G = unmorton(d, parent_key(l, fi));
         for (int o = 0; o < pt.ndir; ++o) {
           const Vec3 Q{G[0] + o % 3 - 1, G[1] + (o / 3) % 3 - 1, d == 3 ? G[2] + o / 9 - 1 : 0};
           if (!f.in_domain(l - 1, Q)) continue;
-          const i64 g = fam_of_parent(l, morton(d, Q));
-          if (g >= 0) halo.push_back(g);
+          const i64 c = cell_index(l, morton(d, Q) << d);
+          if (c >= 0) H.push_back(c / nch);
         }
       }
-      std::sort(halo.begin(), halo.end());
-      halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
-      occ.reserve(halo.size() * np);
-      for (i64 fi : halo) {
-        const u64 pk = parent_key(l, fi);
-        for (int a = 0; a < np; ++a) occ.push_back({morton(d, node_X(l, pk, a)), fi, a});
+      std::sort(H.begin(), H.end());
+      H.erase(std::unique(H.begin(), H.end()), H.end());
+    }
+    const i64 nh = (i64)H.size();
+    std::vector<uint8_t> ismine(nh, 0);
+    std::vector<u32> needmask(nh, 0);
+    if (l == 0) {
+      for (i64 c : mine[0]) ismine[c] = 1;
+      if (L >= 1)
+        for (i64 f1 : mine[1]) ismine[cell_index(0, parent_key(1, f1))] = 1;   // a level-0 cell: all its nodes
+    } else {
+      for (i64 fi : mine[l]) ismine[cur.pos_of(fi)] = 1;
+      if (l < L)
+        for (i64 f1 : mine[l + 1]) {
+          const i64 c = cell_index(l, parent_key(l + 1, f1));
+          needmask[cur.pos_of(c / nch)] |= 1u << (c % nch);
+        }
+    }
+    // per halo entry: computing rank, class masks, next-level computing rank per child
+    std::vector<i32> hcomp(nh);
+    std::vector<u32> hout(nh, 0), hleafn(nh, 0);
+    std::vector<std::array<i32, 8>> hnext(nh);
+    for (i64 h = 0; h < nh; ++h) {
+      const i64 fi = H[h];
+      hnext[h].fill(-1);
+      if (l == 0) {
+        hcomp[h] = 0;   // coarse handoff: level-0 DoFs owned by rank 0 (R25)
+        continue;
       }
-      for (i64 fi : mine[l]) {
-        const u64 pk = parent_key(l, fi);
-        for (int a = 0; a < np; ++a) need.push_back(morton(d, node_X(l, pk, a)));
+      hcomp[h] = comp(l, fi);
+      const Vec3 G = unmorton(d, parent_key(l, fi));
+      for (int o = 0; o < pt.ndir; ++o) {
+        const Vec3 Q{G[0] + o % 3 - 1, G[1] + (o / 3) % 3 - 1, d == 3 ? G[2] + o / 9 - 1 : 0};
+        if (Q == G) continue;
+        if (!f.in_domain(l - 1, Q)) hout[h] |= 1u << o;
+        else if (!f.is_refined(l - 1, morton(d, Q))) hleafn[h] |= 1u << o;
       }
-      for (auto& fc : needcell) {
-        const u64 pk = parent_key(l, fc.first);
-        for (int b = 0; b < nn; ++b) need.push_back(morton(d, node_X(l, pk, pt.cell_to_patch[fc.second][b])));
+      if (l < L)
+        for (int c = 0; c < nch; ++c) {
+          const size_t ci = (size_t)fi * nch + c;
+          if (p.levels[l].leaf[ci]) continue;
+          const i64 c1 = cell_index(l + 1, p.levels[l].key[ci] << d);
+          if (c1 >= 0) hnext[h][c] = comp(l + 1, c1 / nch);
+        }
+    }
+    // ---------------- occurrences, sorted by key
+    const i64 n_occ = nh * stride;
+    GMG_REQUIRE(n_occ < ((i64)1 << 32), GMG_E_OOM, "halo too large for 32-bit occurrence ids");
+    std::vector<u64> okey(n_occ);
+    std::vector<u32> oid(n_occ);
+    for (i64 h = 0; h < nh; ++h) {
+      const Vec3 G = unmorton(d, l == 0 ? p.levels[0].key[H[h]] : parent_key(l, H[h]));
+      for (int a = 0; a < stride; ++a) {
+        const Vec3 X = l == 0 ? X_of(G, 0, off0[a], 1) : X_of(G, l, pt.pa[a], 2);
+        okey[h * stride + a] = morton(d, X);
+        oid[h * stride + a] = (u32)(h * stride + a);
       }
     }
-    std::sort(occ.begin(), occ.end(), [](const Occ& a, const Occ& b) {
-      return a.key != b.key ? a.key < b.key : (a.fam != b.fam ? a.fam < b.fam : a.a < b.a);
-    });
-    std::sort(need.begin(), need.end());
-    need.erase(std::unique(need.begin(), need.end()), need.end());
-    // ---------------- unique halo nodes: flags, owner, transfer owner
-    struct Node {
-      u64 key;
-      uint8_t fl;
-      int owner;
-      i64 tfam;     // transfer-owner family (level >= 1)
-      i64 o0, o1;   // occurrence range
-    };
-    std::vector<Node> nodes;
-    for (size_t s = 0; s < occ.size();) {
-      size_t e = s;
-      Node nd{occ[s].key, 0, INT32_MAX, INT64_MAX, (i64)s, 0};
-      while (e < occ.size() && occ[e].key == occ[s].key) ++e;
-      nd.o1 = (i64)e;
-      for (size_t q = s; q < e; ++q) {
-        const Occ& o = occ[q];
+    radix_sort_pairs32(okey, oid, kbits);
+    // ---------------- unique nodes: flags, owner, transfer owner, need, ranks that need it
+    cur.node_of_occ.assign(n_occ, -1);
+    std::vector<u64> nkey;
+    std::vector<uint8_t> nfl, nneed, nmine;
+    std::vector<i32> nown, ntpos;      // owner; transfer-owner family as halo position
+    std::vector<std::vector<i32>> sidx(P);   // filled after local numbering: (node, peer)
+    std::vector<std::pair<i32, i32>> sends;   // (peer, node) for owned nodes
+    for (i64 s = 0; s < n_occ;) {
+      i64 e = s;
+      while (e < n_occ && okey[e] == okey[s]) ++e;
+      uint8_t fl = 0, need = 0, inmine = 0;
+      i32 own = INT32_MAX;
+      const i32 node = (i32)nkey.size();
+      for (i64 q = s; q < e; ++q) {
+        const i64 h = oid[q] / stride;
+        const int a = (int)(oid[q] % stride);
+        cur.node_of_occ[oid[q]] = node;
+        own = std::min(own, hcomp[h]);
         if (l == 0) {
-          nd.owner = 0;                                          // coarse handoff (R25)
-          if (p.levels[0].leaf[o.fam]) nd.fl |= F_LEAF;
-          continue;
+          if (p.levels[0].leaf[H[h]]) fl |= F_LEAF;
+        } else {
+          if (pt.dirmask[a] & hout[h]) fl |= F_B;
+          if (pt.dirmask[a] & hleafn[h]) fl |= F_EREG;
+          for (int c = 0; c < nch; ++c)
+            if ((pt.childmask[a] & (1u << c)) && p.levels[l].leaf[(size_t)H[h] * nch + c]) fl |= F_LEAF;
         }
-        const int cr = comp(l, o.fam);
-        nd.owner = std::min(nd.owner, cr);
-        for (int c = 0; c < nch; ++c)
-          if ((pt.childmask[o.a] & (1u << c)) && p.levels[l].leaf[(size_t)o.fam * nch + c]) nd.fl |= F_LEAF;
+        const bool m = ismine[h] != 0;
+        const bool nc = l > 0 && (pt.childmask[a] & needmask[h]) != 0;
+        if (m || nc) need = 1;
+        if (m && hcomp[h] == rank) inmine = 1;
       }
       if (l == 0) {
-        if (on_boundary(f, k, unmorton(d, nd.key))) nd.fl |= F_B;
-      } else {
-        for (size_t q = s; q < e; ++q) {
-          const Occ& o = occ[q];
-          if (comp(l, o.fam) == nd.owner) nd.tfam = std::min(nd.tfam, o.fam);
+        fl |= on_boundary(f, k, unmorton(d, okey[s])) ? F_B : 0;
+        own = 0;
+        inmine = rank == 0;
+      }
+      i32 tpos = INT32_MAX;
+      if (l > 0)
+        for (i64 q = s; q < e; ++q) {
+          const i32 h = (i32)(oid[q] / stride);
+          if (hcomp[h] == own) tpos = std::min(tpos, h);
         }
-        // class from the parent's neighbours (as topology.cpp), any occurrence decides
-        const Occ& o = occ[s];
-        const Vec3 G = unmorton(d, parent_key(l, o.fam));
-        for (int dd = 0; dd < pt.ndir; ++dd) {
-          if (!(pt.dirmask[o.a] & (1u << dd))) continue;
-          const Vec3 Q{G[0] + dd % 3 - 1, G[1] + (dd / 3) % 3 - 1, d == 3 ? G[2] + dd / 9 - 1 : 0};
-          if (!f.in_domain(l - 1, Q)) nd.fl |= F_B;
-          else if (!f.is_refined(l - 1, morton(d, Q))) nd.fl |= F_EREG;
+      // ranks needing an owned node: computing ranks of the containing families and
+      // of the next-finer families of containing refined cells
+      if (l > 0 && own == rank && inmine && !(fl & F_B)) {
+        i32 qs[64];
+        int nq = 0;
+        for (i64 q = s; q < e; ++q) {
+          const i64 h = oid[q] / stride;
+          const int a = (int)(oid[q] % stride);
+          if (hcomp[h] != rank && nq < 64) qs[nq++] = hcomp[h];
+          for (int c = 0; c < nch; ++c)
+            if ((pt.childmask[a] & (1u << c)) && hnext[h][c] >= 0 && hnext[h][c] != rank && nq < 64)
+              qs[nq++] = hnext[h][c];
+        }
+        GMG_REQUIRE(nq < 64, GMG_E_STATE, "too many ranks share one node");
+        if (nq) {
+          std::sort(qs, qs + nq);
+          nq = (int)(std::unique(qs, qs + nq) - qs);
+          for (int t = 0; t < nq; ++t) sends.push_back({qs[t], node});
         }
       }
-      nodes.push_back(nd);
+      nkey.push_back(okey[s]);
+      nfl.push_back(fl);
+      nown.push_back(own);
+      ntpos.push_back(tpos);
+      nneed.push_back(need);
+      nmine.push_back(inmine);
       s = e;
     }
-    auto node_of = [&](u64 key) -> i64 {
-      auto it = std::lower_bound(nodes.begin(), nodes.end(), key, [](const Node& a, u64 kk) { return a.key < kk; });
-      GMG_REQUIRE(it != nodes.end() && it->key == key, GMG_E_STATE, "node outside the halo");
-      return (i64)(it - nodes.begin());
-    };
-    // ---------------- counts (each node counted by its owner; B nodes by the min computing rank)
+    okey.clear();
+    okey.shrink_to_fit();
+    oid.clear();
+    oid.shrink_to_fit();
+    const i64 nnodes = (i64)nkey.size();
+    // ---------------- counts: each node by its owner (B nodes by the min computing rank)
     {
       const i64 cstep = (i64)1 << (L - l + 1);
-      for (const Node& nd : nodes) {
-        // only nodes whose containing families are complete in the halo: the owner's
-        // own nodes (owner == rank => the node is in one of this rank's families)
-        if (nd.owner != rank) continue;
-        if (l > 0) {
-          bool in_mine = false;
-          for (i64 q = nd.o0; q < nd.o1 && !in_mine; ++q) in_mine = comp(l, occ[q].fam) == rank;
-          if (!in_mine) continue;
-        } else if (rank != 0) {
-          continue;
-        }
-        const bool B = nd.fl & F_B, E = nd.fl & F_EREG, inleaf = nd.fl & F_LEAF;
+      for (i64 i = 0; i < nnodes; ++i) {
+        if (nown[i] != rank || !nmine[i]) continue;
+        const uint8_t fl = nfl[i];
+        const bool B = fl & F_B, E = fl & F_EREG, inleaf = fl & F_LEAF;
         if (B) cnt.B[l]++;
         else if (E) cnt.E[l]++;
         else cnt.S[l]++;
         if (!inleaf) continue;
         bool coarse = false;
         if (l > 0 && E) {
-          const Vec3 X = unmorton(d, nd.key);
+          const Vec3 X = unmorton(d, nkey[i]);
           coarse = true;
           for (int j = 0; j < d; ++j)
             if (X[j] % cstep) coarse = false;
@@ -253,84 +316,50 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
       }
     }
     // ---------------- owned and ghost DoFs (local order = global order restricted)
-    std::vector<i64> owned, ghosts;       // node indices
-    if (l == 0 && rank == 0) {
-      for (i64 i = 0; i < (i64)nodes.size(); ++i)
-        if (!(nodes[i].fl & F_B)) owned.push_back(i);
+    std::vector<i64> owned, ghosts;
+    for (i64 i = 0; i < nnodes; ++i) {
+      if (nfl[i] & F_B) continue;
+      if (nown[i] == rank && (l > 0 ? (nneed[i] && nmine[i]) : rank == 0)) owned.push_back(i);
+      else if (nneed[i] && nown[i] != rank) ghosts.push_back(i);
     }
-    for (u64 kk : need) {
-      const i64 i = node_of(kk);
-      if (nodes[i].fl & F_B) continue;
-      if (nodes[i].owner == rank) {
-        if (l > 0) owned.push_back(i);
-      } else {
-        ghosts.push_back(i);
-      }
-    }
-    std::sort(owned.begin(), owned.end());
-    owned.erase(std::unique(owned.begin(), owned.end()), owned.end());
-    std::sort(ghosts.begin(), ghosts.end(), [&](i64 a, i64 b) {
-      return nodes[a].owner != nodes[b].owner ? nodes[a].owner < nodes[b].owner : nodes[a].key < nodes[b].key;
-    });
-    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    std::stable_sort(ghosts.begin(), ghosts.end(), [&](i64 a, i64 b) { return nown[a] < nown[b]; });
     v.n_owned = (i64)owned.size();
     v.n_ghost = (i64)ghosts.size();
     const i64 nloc = v.n_local();
-    std::vector<i32> local(nodes.size(), -1);
-    for (i64 i = 0; i < v.n_owned; ++i) local[owned[i]] = (i32)i;
-    for (i64 i = 0; i < v.n_ghost; ++i) local[ghosts[i]] = (i32)(v.n_owned + i);
-    owned_keys[l].resize(v.n_owned);
-    ghost_keys[l].resize(v.n_ghost);
+    cur.local.assign(nnodes, -1);
+    for (i64 i = 0; i < v.n_owned; ++i) cur.local[owned[i]] = (i32)i;
+    for (i64 i = 0; i < v.n_ghost; ++i) cur.local[ghosts[i]] = (i32)(v.n_owned + i);
+    v.owned_key.resize(v.n_owned);
+    v.ghost_key.resize(v.n_ghost);
     v.ghost_owner.resize(v.n_ghost);
-    for (i64 i = 0; i < v.n_owned; ++i) owned_keys[l][i] = nodes[owned[i]].key;
+    for (i64 i = 0; i < v.n_owned; ++i) v.owned_key[i] = nkey[owned[i]];
     for (i64 i = 0; i < v.n_ghost; ++i) {
-      ghost_keys[l][i] = nodes[ghosts[i]].key;
-      v.ghost_owner[i] = nodes[ghosts[i]].owner;
+      v.ghost_key[i] = nkey[ghosts[i]];
+      v.ghost_owner[i] = nown[ghosts[i]];
     }
-    v.owned_key = owned_keys[l];
-    v.ghost_key = ghost_keys[l];
-    keymap[l].reserve(nloc);
-    for (i64 i = 0; i < v.n_owned; ++i) keymap[l].push_back({owned_keys[l][i], (i32)i});
-    for (i64 i = 0; i < v.n_ghost; ++i) keymap[l].push_back({ghost_keys[l][i], (i32)(v.n_owned + i)});
-    std::sort(keymap[l].begin(), keymap[l].end());
-    // ---------------- exchange plan: who needs each owned DoF
-    std::vector<std::vector<i32>> sidx(P);
+    // ---------------- exchange plan
     if (l == 0) {
-      if (rank == 0) {
-        // rank q needs the nodes of its level-0 cells and of the parents of its level-1 families
-        std::vector<std::vector<char>> needq(P, std::vector<char>(p.levels[0].key.size(), 0));
-        for (i64 c = 0; c < (i64)p.levels[0].key.size(); ++c) needq[p.levels[0].owner[c]][c] = 1;
-        if (L >= 1)
-          for (i64 fi = 0; fi < nfam_of(1); ++fi) needq[comp(1, fi)][cell_index(0, parent_key(1, fi))] = 1;
+      if (rank == 0)
         for (int q = 1; q < P; ++q) {
-          std::vector<i64> ns;
-          for (const Occ& o : occ)
-            if (needq[q][o.fam]) ns.push_back(node_of(o.key));
+          // rank q needs the nodes of its level-0 cells and of the parents of its level-1 families
+          std::vector<char> needc(nh, 0);
+          for (i64 c = 0; c < nh; ++c)
+            if (p.levels[0].owner[c] == q) needc[c] = 1;
+          if (L >= 1)
+            for (i64 fi = 0; fi < nfam_of(1); ++fi)
+              if (comp(1, fi) == q) needc[cell_index(0, parent_key(1, fi))] = 1;
+          std::vector<i32> ns;
+          for (i64 c = 0; c < nh; ++c)
+            if (needc[c])
+              for (int b = 0; b < nn; ++b) ns.push_back(cur.node_of_occ[c * nn + b]);
           std::sort(ns.begin(), ns.end());
           ns.erase(std::unique(ns.begin(), ns.end()), ns.end());
-          for (i64 i : ns)
-            if (!(nodes[i].fl & F_B)) sidx[q].push_back(local[i]);
+          for (i32 i : ns)
+            if (!(nfl[i] & F_B)) sidx[q].push_back(cur.local[i]);
         }
-      }
     } else {
-      for (i64 oi = 0; oi < v.n_owned; ++oi) {
-        const Node& nd = nodes[owned[oi]];
-        std::vector<int> qs;
-        for (i64 q = nd.o0; q < nd.o1; ++q) {
-          const Occ& o = occ[q];
-          qs.push_back(comp(l, o.fam));                        // operator: a containing family
-          for (int c = 0; c < nch; ++c) {                        // transfer: next-finer family of a refined cell
-            if (!(pt.childmask[o.a] & (1u << c))) continue;
-            if (p.levels[l].leaf[(size_t)o.fam * nch + c]) continue;
-            const i64 f1 = fam_of_parent(l + 1, p.levels[l].key[(size_t)o.fam * nch + c]);
-            if (f1 >= 0) qs.push_back(comp(l + 1, f1));
-          }
-        }
-        std::sort(qs.begin(), qs.end());
-        qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
-        for (int q : qs)
-          if (q != rank) sidx[q].push_back((i32)oi);
-      }
+      std::sort(sends.begin(), sends.end());   // by peer, then node (= key order)
+      for (auto& pr : sends) sidx[pr.first].push_back(cur.local[pr.second]);
     }
     std::vector<i64> rcount(P, 0);
     for (i64 i = 0; i < v.n_ghost; ++i) rcount[v.ghost_owner[i]]++;
@@ -340,15 +369,32 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     for (int q = 0; q < P; ++q) {
       if (rcount[q] == 0 && sidx[q].empty()) continue;
       v.peers.push_back(q);
-      for (i32 s : sidx[q]) v.send_idx.push_back(s);
+      for (i32 s2 : sidx[q]) v.send_idx.push_back(s2);
       for (i64 c = 0; c < rcount[q]; ++c) v.recv_idx.push_back((i32)(v.n_owned + gpos + c));
       gpos += rcount[q];
       v.send_off.push_back((i64)v.send_idx.size());
       v.recv_off.push_back((i64)v.recv_idx.size());
     }
-    // ---------------- local cells / families and their tables
+    // ---------------- local cells, classes, lambda, eigen start vector
+    v.cls.resize(nloc);
+    v.lam.assign(nloc, 0);
+    v.eig_v.assign(nloc, 0.0);
+    auto fill_node = [&](i64 li, i64 i) {
+      const uint8_t fl = nfl[i];
+      v.cls[li] = (fl & F_EREG) ? CLS_E : CLS_S;
+      if (li >= v.n_owned || v.cls[li] != CLS_S) return;
+      v.lam[li] = (fl & F_LEAF) ? 1 : 0;   // S here, in a level-l leaf: not S on level l+1
+      const Vec3 X = unmorton(d, nkey[i]);
+      Vec3 Y{0, 0, 0};
+      for (int j = 0; j < d; ++j) Y[j] = X[j] >> (L - l);
+      v.eig_v[li] = -5.5 + (double)(morton(d, Y) % 12);   // R10b
+    };
+    for (i64 i = 0; i < v.n_owned; ++i) fill_node(i, owned[i]);
+    for (i64 i = 0; i < v.n_ghost; ++i) fill_node(v.n_owned + i, ghosts[i]);
+    for (i64 i = 0; i < v.n_owned; ++i)
+      if (v.cls[i] == CLS_S) cnt.own_S[l]++;
     if (l == 0) {
-      for (i64 c : mine0) v.cell_global.push_back(c);
+      for (i64 c : mine[0]) v.cell_global.push_back(c);
     } else {
       for (i64 fi : mine[l])
         for (int c = 0; c < nch; ++c) v.cell_global.push_back(fi * nch + c);
@@ -359,109 +405,49 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     for (i64 c = 0; c < v.n_cells; ++c) {
       const i64 gc = v.cell_global[c];
       for (int b = 0; b < nn; ++b) {
-        u64 key;
-        if (l == 0) {
-          const Vec3 G = unmorton(d, p.levels[0].key[gc]);
-          Vec3 X{0, 0, 0};
-          int r = b;
-          for (int j = 0; j < d; ++j) {
-            X[j] = ((i64)k * G[j] + r % (k + 1)) << L;
-            r /= (k + 1);
-          }
-          key = morton(d, X);
-        } else {
-          key = morton(d, node_X(l, parent_key(l, gc / nch), pt.cell_to_patch[gc % nch][b]));
-        }
-        const i64 i = node_of(key);
-        v.cell_dofs[(size_t)c * nn + b] = (nodes[i].fl & F_B) ? -1 : local[i];
+        const i64 occ = l == 0 ? gc * nn + b : cur.pos_of(gc / nch) * np + pt.cell_to_patch[gc % nch][b];
+        const i32 i = cur.node_of_occ[occ];
+        v.cell_dofs[(size_t)c * nn + b] = (nfl[i] & F_B) ? -1 : cur.local[i];
       }
       if (p.levels[l].leaf[gc]) v.leaf_cells.push_back((i32)c);
     }
-    v.cls.resize(nloc);
-    v.lam.assign(nloc, 0);
-    v.eig_v.assign(nloc, 0.0);
-    auto fill_node = [&](i64 li, i64 i) {
-      const Node& nd = nodes[i];
-      v.cls[li] = (nd.fl & F_EREG) ? CLS_E : CLS_S;
-      if (li >= v.n_owned || v.cls[li] != CLS_S) return;
-      // lambda slot: S here and some in-domain level-l cell containing the node is a leaf
-      const Vec3 X = unmorton(d, nd.key);
-      const i64 s = (i64)k << (L - l);
-      bool up = true;
-      for (int c = 0; c < (1 << d) && up; ++c) {
-        Vec3 Q{0, 0, 0};
-        for (int j = 0; j < d; ++j) Q[j] = ((c >> j) & 1) ? X[j] / s : (X[j] - 1) / s - ((X[j] - 1) < 0 ? 1 : 0);
-        bool neg = false;
-        for (int j = 0; j < d; ++j) neg |= Q[j] < 0;
-        if (neg || !f.in_domain(l, Q)) continue;
-        if (!f.is_refined(l, morton(d, Q))) up = false;
-      }
-      v.lam[li] = up ? 0 : 1;
-      // eigen start vector, key-based (R10b): -5.5 + (level-lattice Morton key mod 12)
-      Vec3 Y{0, 0, 0};
-      for (int j = 0; j < d; ++j) Y[j] = X[j] >> (L - l);
-      v.eig_v[li] = -5.5 + (double)(morton(d, Y) % 12);
-    };
-    for (i64 i = 0; i < v.n_owned; ++i) fill_node(i, owned[i]);
-    for (i64 i = 0; i < v.n_ghost; ++i) fill_node(v.n_owned + i, ghosts[i]);
-    for (i64 i = 0; i < v.n_owned; ++i)
-      if (v.cls[i] == CLS_S) cnt.own_S[l]++;
     if (l > 0) {
       const int row = np + nn;
       v.fam_dofs.resize((size_t)v.n_fam * np);
       v.xfer.resize((size_t)v.n_fam * row);
-      const auto& km = keymap[l - 1];
-      auto local_coarse = [&](u64 key) -> i32 {   // level-(l-1) local index of a node (-1: Dirichlet / absent)
-        auto it = std::lower_bound(km.begin(), km.end(), std::make_pair(key, (i32)INT32_MIN));
-        return (it != km.end() && it->first == key) ? it->second : -1;
-      };
       for (i64 lf = 0; lf < v.n_fam; ++lf) {
         const i64 fi = mine[l][lf];
-        const u64 pk = parent_key(l, fi);
+        const i64 hp = cur.pos_of(fi);
         bool edge = false;
         for (int a = 0; a < np; ++a) {
-          const i64 i = node_of(morton(d, node_X(l, pk, a)));
+          const i32 i = cur.node_of_occ[hp * np + a];
           i32 enc = -1;
-          if (!(nodes[i].fl & F_B)) {
-            const i32 lg = local[i];
+          if (!(nfl[i] & F_B)) {
+            const i32 lg = cur.local[i];
             GMG_REQUIRE(lg >= 0, GMG_E_STATE, "patch node without a local index");
-            const bool towner = nodes[i].tfam == fi;
+            const bool towner = ntpos[i] == (i32)hp;
             enc = towner ? lg : -2 - lg;
             if (towner) {
               GMG_REQUIRE(lg < v.n_owned, GMG_E_STATE, "transfer owner is not the DoF owner");
-              if (nodes[i].fl & F_EREG) edge = true;
+              if (nfl[i] & F_EREG) edge = true;
             }
           }
           v.fam_dofs[(size_t)lf * np + a] = enc;
           v.xfer[(size_t)lf * row + a] = enc;
         }
         // the parent's (k+1)^d nodes on level l-1
-        const i64 pc = cell_index(l - 1, pk);
+        const i64 pc = cell_index(l - 1, parent_key(l, fi));
         for (int b = 0; b < nn; ++b) {
-          u64 key;
-          if (l - 1 == 0) {
-            const Vec3 G = unmorton(d, pk);
-            Vec3 X{0, 0, 0};
-            int r = b;
-            for (int j = 0; j < d; ++j) {
-              X[j] = ((i64)k * G[j] + r % (k + 1)) << L;
-              r /= (k + 1);
-            }
-            key = morton(d, X);
-          } else {
-            const int child = (int)(pc % nch);
-            key = morton(d, node_X(l - 1, parent_key(l - 1, pc / nch), pt.cell_to_patch[child][b]));
-          }
-          const i32 lc = local_coarse(key);
-          v.xfer[(size_t)lf * row + np + b] = lc;
+          const i64 occ = l - 1 == 0 ? pc * nn + b : prev.pos_of(pc / nch) * np + pt.cell_to_patch[pc % nch][b];
+          const i32 i = prev.node_of_occ[occ];
+          v.xfer[(size_t)lf * row + np + b] = prev.local[i];
         }
         if (edge) v.edge_fams.push_back((i32)lf);
       }
       // complete grandfamilies (as make_local)
-      if (d == 3 && l >= 2) {
-        const auto& pkk = p.levels[l - 1].key;
+      if (d == 3 && l >= 2)
         for (i64 lf = 0; lf + 7 < v.n_fam;) {
-          const u64 k0 = pkk[cell_index(l - 1, parent_key(l, mine[l][lf]))];
+          const u64 k0 = parent_key(l, mine[l][lf]);
           bool ok = (k0 & 7) == 0;
           for (int j = 1; ok && j < 8; ++j) ok = parent_key(l, mine[l][lf + j]) == (k0 | (u64)j);
           if (ok) {
@@ -471,12 +457,15 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
             ++lf;
           }
         }
-      }
     }
     // ---------------- owned free leaf DoFs of this level
     for (i64 i = 0; i < v.n_owned; ++i)
-      if (v.lam[i]) Lt.leaf_tmp.push_back({owned_keys[l][i], (int8_t)l, i});
-    cnt.own_dofs[l] = v.n_owned;
+      if (v.lam[i]) Lt.leaf_tmp.push_back({v.owned_key[i], (int8_t)l, i});
+    cnt.own_dofs[l] = (double)v.n_owned;
+    // the Dirichlet nodes have local -1: prev.local gives -1 for them (xfer parent part)
+    for (i64 i = 0; i < nnodes; ++i)
+      if (nfl[i] & F_B) cur.local[i] = -1;
+    prev = std::move(cur);
   }
   // leaf order (owner, key): this rank's leaf DoFs by key
   std::sort(Lt.leaf_tmp.begin(), Lt.leaf_tmp.end(),
@@ -487,10 +476,11 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     Lt.leaf_key.push_back(r.key);
   }
   Lt.leaf_tmp.clear();
+  Lt.leaf_tmp.shrink_to_fit();
   Lt.n_leaf_owned = (i64)Lt.leaf_level.size();
   Lt.leaf_first = -1;          // set from the other ranks' counts (LocalCounts)
   Lt.n_leaf_global = -1;
-  cnt.leaf_free = Lt.n_leaf_owned;
+  cnt.leaf_free = (double)Lt.n_leaf_owned;
   if (counts) *counts = cnt;
   return Lt;
 }
