@@ -17,7 +17,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmg.so")
+# GMG_LIB_PATH: an alternative build of the same library (A/B experiments with
+# compile-time kernel variants); default the in-tree build
+LIB_PATH = os.environ.get("GMG_LIB_PATH") or os.path.join(_HERE, "libgmg.so")
 
 if "GMG_NCCL_LIB" not in os.environ:
     # use the libnccl that torch loads (pip nvidia-nccl), not the system copy

@@ -273,17 +273,24 @@ static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t v
 }
 
 template <int K, typename T, int TM, int SL>
-static void launch_gf(DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1, double c2, const T* xc,
-                      cudaStream_t s) {
-  static const bool attr = [] {
+static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1,
+                      double c2, const T* xc, cudaStream_t s) {
+  static const int per_sm = [] {
     CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)dev::gf_smem_bytes<K, T, SL>()));
-    return true;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gfam_tensor_apply<K, T, TM, SL>,
+                                                     dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>()));
+    return std::max(nb, 1);
   }();
-  (void)attr;
+  static const bool prefetch = [] {
+    const char* e = std::getenv("GMG_GF_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
   const int grid = (int)((v.n_gf + SL - 1) / SL);
   dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
-      (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc);
+      (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
+      prefetch ? per_sm * d->sms : 0);
 }
 
 // The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
@@ -294,9 +301,9 @@ static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, con
                           double c2, const T* xc, cudaStream_t s) {
   const int np = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), nn = (K + 1) * (K + 1) * (K + 1);
   if (v.n_gf > 0) {
-    if (d->gf_slots == 1) launch_gf<K, T, TM, 1>(v, x, y, g, dv, xw, c1, c2, xc, s);
-    else if (d->gf_slots == 2) launch_gf<K, T, TM, 2>(v, x, y, g, dv, xw, c1, c2, xc, s);
-    else launch_gf<K, T, TM, 3>(v, x, y, g, dv, xw, c1, c2, xc, s);
+    if (d->gf_slots == 1) launch_gf<K, T, TM, 1>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
+    else if (d->gf_slots == 2) launch_gf<K, T, TM, 2>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
+    else launch_gf<K, T, TM, 3>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
     d->launches++;
   }
   const i64 nf = v.n_gf > 0 ? v.n_single : v.n_fam;

@@ -627,6 +627,10 @@ __host__ __device__ __forceinline__ constexpr double Mt4(int i, int j) {
 
 // Grandfamilies per block (SLOTS) and threads: 1 -> 96 (81 lanes busy), 2 -> 192,
 // 3 -> 256 (243 busy); the minimum-blocks bound caps registers at ~80.
+#ifndef GF_LOAD_AT_DEFAULT
+#define GF_LOAD_AT_DEFAULT 2
+#endif
+constexpr int GF_LOAD_AT = GF_LOAD_AT_DEFAULT;   // fused epilogue loads: 1 after the z pass, 2 after the x pass
 template <int SLOTS> struct GfBlock {
   static constexpr int THREADS = SLOTS == 1 ? 96 : (SLOTS == 2 ? 192 : 256);
   static constexpr int MIN_BLOCKS = 65536 / (THREADS * 80);
@@ -669,11 +673,17 @@ __global__ void __launch_bounds__(GfBlock<GF_SLOTS>::THREADS, GfBlock<GF_SLOTS>:
 gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict__ gcoef, double scale_,
                   const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                   const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr) {
+                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   using S = GfShape<K>;
+  if (pf > 0) {   // the table rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
+    const long fb = ((long)blockIdx.x + pf) * GF_SLOTS;
+    const long bytes = (long)GF_SLOTS * GfShape<K>::ROW * 4, off = (long)threadIdx.x * 128;
+    if (fb < ngf && off < bytes && fb * GfShape<K>::ROW * 4 + off < (long)ngf * GfShape<K>::ROW * 4)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(gx + fb * (long)GfShape<K>::ROW) + off));
+  }
   using LY = GfLayout<K>;
   constexpr int N1 = S::N1, NL = S::NL, ROW = S::ROW, NP = S::NP;
   extern __shared__ __align__(16) unsigned char gf_smem[];
@@ -692,6 +702,7 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
   int gi[N1];
   T u[N1], ukeep[N1];
   T inc[PRO ? N1 : 1];
+  T pg[N1], pd[N1], pv[N1];   // fused modes: g, D^-1, dv of the R1 rows
   int own = 0;
   if (act) {              // z lines: lane = (px, py)
 #pragma unroll
@@ -774,6 +785,18 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
       a0[ia] = t1;
       a1[ia] = t2;
     }
+    if (TM != TA_APPLY && GF_LOAD_AT == 1) {   // in flight across the y and x passes
+#pragma unroll
+      for (int z = 0; z < N1; ++z) {
+        const int i = gi[z];
+        pg[z] = pd[z] = pv[z] = T(0);
+        if (i >= 0 && i < n_r1) {
+          pg[z] = __ldg(g + i);
+          pd[z] = __ldg(Dinv + i);
+          if (RDV && !DVX) pv[z] = dv[i];
+        }
+      }
+    }
   }
   __syncthreads();
   T t1[N1], t2[N1];
@@ -832,8 +855,7 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
 #pragma unroll
     for (int q = 0; q < N1; ++q) a0[bn + LY::nx * q] = out[q];
   }
-  T pg[N1], pd[N1], pv[N1];
-  if (TM != TA_APPLY && act) {
+  if (TM != TA_APPLY && GF_LOAD_AT == 2 && act) {
 #pragma unroll
     for (int z = 0; z < N1; ++z) {
       const int i = gi[z];

@@ -17,7 +17,7 @@ SWEEP = {
     2: {"uniform": range(8, 13), "circle": range(10, 17), "quadrant": range(8, 14), "annulus": range(8, 14)},
     3: {"uniform": range(4, 8), "circle": range(6, 11), "quadrant": range(5, 9), "annulus": range(5, 9)},
 }
-PS = {2: (4, 16, 64, 256, 1024, 4096), 3: (8, 64, 512, 4096)}
+PS = {2: (4, 16, 64, 256, 1024, 2048, 4096, 8192, 16384), 3: (8, 64, 512, 4096)}
 
 
 def main(out):
@@ -46,4 +46,4 @@ def main(out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "profiles/r01_fig4_fig5_sweeps.csv")
+    main(sys.argv[1] if len(sys.argv) > 1 else "profiles/r02_fig4_fig5_sweeps.csv")
