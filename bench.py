@@ -322,7 +322,8 @@ def measure(ctx, args, name, main=True):
     cfg = config_c5(ctx.world) if name == "c5" else config(name)
     t0 = time.time()
     f = G.gmg_forest_generate(G.recipe_from_config(cfg))
-    part = G.gmg_partition(f, ctx.world, mode=args.partition)
+    # N > 1: the smallest levels are gathered on rank 0
+    part = G.gmg_partition(f, ctx.world, mode=args.partition, coarse_cells=args.coarse_cells if ctx.world > 1 else 0)
     mixed = args.precision == "mixed"
     coef = None
     if cfg.get("coef") == "level2_log_uniform":        # config 4: a per level-2 cell (SFC order)
@@ -352,6 +353,11 @@ def measure(ctx, args, name, main=True):
     for _ in range(max(args.warmup, 1)):
         h.vcycle(b, x)
     ctx.barrier()
+    if args.profile and main:      # one V-cycle inside cudaProfilerStart/Stop (ncu --profile-from-start off)
+        torch.cuda.profiler.start()
+        h.vcycle(b, x)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     launches0 = h.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(ctx.gpu) as clk:
@@ -507,7 +513,8 @@ def run_ours(args):
                           "l2": "inputs larger than L2 (MG-layout vectors %.0f MB each > 126 MB)"
                                 % main["mg_vector_mb"],
                           "parallelism": "single GPU" if ctx.world == 1 else
-                          f"{ctx.world} ranks, SFC partition ({args.partition}), {args.transport} ghost exchange",
+                          f"{ctx.world} ranks, SFC partition ({args.partition}), levels <= {args.coarse_cells} cells "
+                          f"on rank 0, {args.transport} ghost exchange",
                           "partition": args.partition, "partition_eta": main["partition_eta"],
                           "ghost_children_ratio": main["ghost_children_ratio"], "setup_s": main["setup_s"],
                           "setup": main["setup"]},
@@ -593,7 +600,11 @@ def main():
                     help="level ownership: first-child rule (P:604, default) or per-level SFC balance (P:597)")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
                     help="fp64 V-cycle (default, BASELINE) or fp32 V-cycle inside the fp64 CG (P:897)")
+    ap.add_argument("--coarse-cells", type=int, default=4096,
+                    help="N > 1: levels with at most this many cells are gathered on rank 0 (0 = off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="cudaProfilerStart/Stop around one V-cycle of the headline config (ncu launch lists)")
     ap.add_argument("--dry-run", action="store_true",
                     help="host-only rank-local setup of every rank, reports time and host RSS (no GPU)")
     args = ap.parse_args()

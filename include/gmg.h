@@ -140,6 +140,15 @@ gmg_status gmg_partition(const gmg_forest *f, int n_ranks, gmg_partitioning **ou
 #define GMG_PARTITION_FIRST_CHILD 0
 #define GMG_PARTITION_PER_LEVEL 1
 gmg_status gmg_partition_mode(const gmg_forest *f, int n_ranks, int mode, gmg_partitioning **out);
+/* As gmg_partition_mode, and the coarse levels gathered on rank 0: every level
+ * from 0 up to the last one with at most coarse_cells cells (strictly on that
+ * level) is owned entirely by rank 0 ("processors drop out automatically on
+ * coarser levels"); the small levels then run without exchanges and
+ * the handoff is the ghost exchange of the first finer level.  0 = off
+ * (gmg_partition_mode).  The model of gmg_partition_model counts the owners as
+ * assigned.  Errors: INVALID_ARG. */
+gmg_status gmg_partition_ex(const gmg_forest *f, int n_ranks, int mode, int64_t coarse_cells,
+                            gmg_partitioning **out);
 gmg_status gmg_partition_destroy(gmg_partitioning *p);
 
 #define GMG_MAX_LEVELS 64

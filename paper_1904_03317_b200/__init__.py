@@ -128,6 +128,7 @@ _SIGS = {
     "gmg_partition": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
     "gmg_partition_mode": ([_vp, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "gmg_partition_destroy": ([_vp], C.c_int),
+    "gmg_partition_ex": ([_vp, C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)], C.c_int),
     "gmg_partition_model": ([_vp, C.c_int64, C.POINTER(Model)], C.c_int),
     "gmg_export_tallies": ([_vp, _vp], C.c_int),
     "gmg_export_level_cells": ([_vp, C.c_int, _i64p, _vp, _vp, _vp], C.c_int),
@@ -343,11 +344,13 @@ class Partitioning:
 PARTITION_MODES = {"first_child": 0, "per_level": 1}
 
 
-def gmg_partition(forest: Forest, n_ranks: int, mode: str = "first_child") -> Partitioning:
+def gmg_partition(forest: Forest, n_ranks: int, mode: str = "first_child", coarse_cells: int = 0) -> Partitioning:
     """SFC partition with the first-child rule or, mode="per_level",
-    every level balanced on its own (P:597 alternative, reading R29)."""
+    every level balanced on its own (P:597 alternative, reading R29);
+    coarse_cells > 0 gathers the levels with at most that many cells on rank 0
+    (gmg_partition_ex, P:616-617)."""
     h = _vp()
-    _check(_lib.gmg_partition_mode(forest.h, n_ranks, PARTITION_MODES[mode], C.byref(h)))
+    _check(_lib.gmg_partition_ex(forest.h, n_ranks, PARTITION_MODES[mode], int(coarse_cells), C.byref(h)))
     return Partitioning(h, forest, n_ranks)
 
 

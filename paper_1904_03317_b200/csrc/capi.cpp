@@ -162,6 +162,18 @@ gmg_status gmg_partition_mode(const gmg_forest* f, int n_ranks, int mode, gmg_pa
   });
 }
 
+gmg_status gmg_partition_ex(const gmg_forest* f, int n_ranks, int mode, int64_t coarse_cells, gmg_partitioning** out) {
+  return guard([&] {
+    NEED(f);
+    NEED(out);
+    GMG_REQUIRE(coarse_cells >= 0, GMG_E_INVALID_ARG, "coarse_cells must be >= 0");
+    auto p = std::make_unique<gmg_partitioning>();
+    p->forest = f;
+    p->p = gmg::make_partition(f->f, n_ranks, mode, coarse_cells);
+    *out = p.release();
+  });
+}
+
 gmg_status gmg_partition_destroy(gmg_partitioning* p) {
   delete p;
   return GMG_OK;

@@ -61,11 +61,12 @@ struct Partition {
   const Forest* f = nullptr;
   int n_ranks = 1;
   int mode = GMG_PARTITION_FIRST_CHILD;
+  i64 coarse_cells = 0;        // levels 0.. with <= coarse_cells cells gathered on rank 0
   std::vector<i32> leaf_owner;
   std::vector<LevelCells> levels;
 };
 
-Partition make_partition(const Forest& f, int n_ranks, int mode = GMG_PARTITION_FIRST_CHILD);
+Partition make_partition(const Forest& f, int n_ranks, int mode = GMG_PARTITION_FIRST_CHILD, i64 coarse_cells = 0);
 gmg_model partition_model(const Partition& p, i64 W0_override);
 
 // ------------------------------------------------------------------ topology

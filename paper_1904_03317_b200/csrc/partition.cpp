@@ -11,7 +11,7 @@
 
 namespace gmg {
 
-Partition make_partition(const Forest& f, int n_ranks, int mode) {
+Partition make_partition(const Forest& f, int n_ranks, int mode, i64 coarse_cells) {
   GMG_REQUIRE(n_ranks >= 1, GMG_E_INVALID_ARG, "n_ranks must be >= 1");
   GMG_REQUIRE(mode == GMG_PARTITION_FIRST_CHILD || mode == GMG_PARTITION_PER_LEVEL, GMG_E_INVALID_ARG,
               "partition mode");
@@ -79,6 +79,15 @@ Partition make_partition(const Forest& f, int n_ranks, int mode) {
       }
     }
   }
+  // coarse-level gather ("processors drop out automatically on coarser levels",
+  // P:616-617, taken to its end): the levels from 0 up to the last one with at most
+  // coarse_cells cells live entirely on rank 0, so the small levels of the V-cycle
+  // run without exchanges; the handoff to the finer levels is the ordinary
+  // restriction / prolongation ghost exchange of the first finer level
+  if (coarse_cells > 0)
+    for (int l = 0; l <= L && (i64)p.levels[l].key.size() <= coarse_cells; ++l)
+      std::fill(p.levels[l].owner.begin(), p.levels[l].owner.end(), 0);
+  p.coarse_cells = coarse_cells;
   return p;
 }
 

@@ -33,12 +33,13 @@ def _cfg(name):
     return config(name), -1
 
 
-@pytest.mark.parametrize("name,k,mode,ps", CASES)
-def test_rank_local_equals_global_layout(name, k, mode, ps):
+@pytest.mark.parametrize("name,k,mode,ps,coarse", [c + (0,) for c in CASES] +
+                         [("c3p2", 2, "first_child", (3, 8), 600), ("c4s", 2, "per_level", (4,), 100)])
+def test_rank_local_equals_global_layout(name, k, mode, ps, coarse):
     cfg, passes = _cfg(name)
     f = G.gmg_forest_generate(G.recipe_from_config(cfg, passes))
     for p in ps:
-        part = G.gmg_partition(f, p, mode=mode)
+        part = G.gmg_partition(f, p, mode=mode, coarse_cells=coarse)
         for r in range(p):
             hg = G.gmg_setup(f, part, k=k, rank=r, host_only=True, eig_key=True)
             hl = G.gmg_setup(f, part, k=k, rank=r, host_only=True, rank_local=True)

@@ -114,15 +114,23 @@ THREAD_CASES = [("c1", None, 2, "first_child"), ("c1", None, 3, "first_child"), 
                 ("brick8", 1, 5, "first_child"), ("c3p2", 1, 32, "first_child")]
 
 
+# coarse-level gather (gmg_partition_ex): levels with <= coarse cells on rank 0
+COARSE_CASES = [("c3p2", None, 4, "first_child", 64), ("c3p2", None, 8, "first_child", 600),
+                ("c4s", None, 3, "first_child", 100), ("c1", None, 5, "per_level", 20)]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,k,p,mode", THREAD_CASES)
-def test_thread_ranks_vs_oracle(name, k, p, mode):
+@pytest.mark.parametrize("name,k,p,mode,coarse", [c + (0,) for c in THREAD_CASES] + COARSE_CASES)
+def test_thread_ranks_vs_oracle(name, k, p, mode, coarse):
     import torch
     cfg = _cfg(name, k)
     oh, b_can, x_ref, it_ref, lams = _oracle(cfg)
     world = G.LocalWorld(p)
     lf = G.gmg_forest_generate(G.recipe_from_config(cfg))
-    part = G.gmg_partition(lf, p, mode=mode)
+    part = G.gmg_partition(lf, p, mode=mode, coarse_cells=coarse)
+    if coarse:
+        t = part.tallies()
+        assert (t[0, 1:] == 0).all() and (t[1, 1:] == 0).all()   # gathered levels on rank 0
     hs = [None] * p
     streams = [torch.cuda.Stream() for _ in range(p)]
 
@@ -252,13 +260,14 @@ def test_host_world_rejects_bad_arguments():
 
 
 # ------------------------------------------------------------------ rank-local builds vs the oracle
-RL_CASES = [("c1", None, 3, "first_child"), ("c3p2", None, 4, "first_child"), ("c3p2", None, 8, "first_child"),
-            ("c4s", None, 3, "per_level"), ("brick8", 1, 5, "first_child")]
+RL_CASES = [("c1", None, 3, "first_child", 0), ("c3p2", None, 4, "first_child", 0),
+            ("c3p2", None, 8, "first_child", 0), ("c4s", None, 3, "per_level", 0), ("brick8", 1, 5, "first_child", 0),
+            ("c3p2", None, 8, "first_child", 600)]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,k,p,mode", RL_CASES)
-def test_rank_local_threads_vs_oracle(name, k, p, mode):
+@pytest.mark.parametrize("name,k,p,mode,coarse", RL_CASES)
+def test_rank_local_threads_vs_oracle(name, k, p, mode, coarse):
     """GMG_RANK_LOCAL hierarchies (no global numbering; inputs and outputs
     matched by node key) against the oracle: V-cycle 1e-10, CG +-1 / 1e-8."""
     import torch
@@ -271,7 +280,7 @@ def test_rank_local_threads_vs_oracle(name, k, p, mode):
     x_ref = mg.vcycle(oh, b_ref)
     world = G.LocalWorld(p)
     lf = G.gmg_forest_generate(G.recipe_from_config(cfg))
-    part = G.gmg_partition(lf, p, mode=mode)
+    part = G.gmg_partition(lf, p, mode=mode, coarse_cells=coarse)
     hs = [None] * p
     streams = [torch.cuda.Stream() for _ in range(p)]
 

@@ -39,5 +39,13 @@ recs = [r for r in recs if r["launches"]]
 recs.sort(key=lambda r: -r["seconds"])
 top = [(r["kind"], r["level"], round(1e6 * r["seconds"] / r["launches"], 1), round(r["seconds"] / 2 / ms * 1e3, 3))
        for r in recs[:10]]
+per_level = {}
+for r in recs:
+    per_level[r["level"]] = per_level.get(r["level"], 0.0) + r["seconds"] / 2
+launches = {}
+for r in recs:
+    launches[r["level"]] = launches.get(r["level"], 0) + r["launches"] // 2
 print(json.dumps({"tag": args.tag, "config": args.config, "ms": ms, "dofs_per_s": info["n_leaf_nodes"] / ms * 1e3,
-                  "gf": sum(info["level_gf"]), "top": top}))
+                  "gf": sum(info["level_gf"]), "top": top,
+                  "per_level_us": {l: round(1e6 * v, 1) for l, v in sorted(per_level.items())},
+                  "per_level_launch_records": launches}))
