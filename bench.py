@@ -533,44 +533,63 @@ def run_ours(args):
     ctx.close()
 
 
-def dry_run(args):
-    """--dry-run: every rank builds its part of the hierarchy on the host only
-    (rank-local topology, no GPU) and reports setup time and peak host RSS; rank 0
-    prints one JSON line (not a bench line).  Shows that the N-rank setup of a
-    config fits the host: `python bench.py --gpus 8 --config c5 --dry-run`."""
+def dry_run_rank(args, rank, world):
+    """One rank's host-only rank-local setup (no GPU, no communication): time and
+    peak host RSS, as a dict."""
     import resource
-    import torch.distributed as dist
     import paper_1904_03317_b200 as G
     from gmg_inputs import config, config_c5
-    rank, world, _ = env_rank()
-    if world > 1:
-        dist.init_process_group("gloo")
     cfg = config_c5(world) if args.config == "c5" else config(args.config)
     t0 = time.time()
     f = G.gmg_forest_generate(G.recipe_from_config(cfg))
     t_forest = time.time() - t0
-    part = G.gmg_partition(f, world, mode=args.partition)
+    part = G.gmg_partition(f, world, mode=args.partition, coarse_cells=args.coarse_cells if world > 1 else 0)
     t_part = time.time() - t0 - t_forest
     h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, host_only=True, rank_local=True)
     t_setup = time.time() - t0
     info = h.info()
-    mine = {"rank": rank, "setup_s": round(t_setup, 1), "forest_s": round(t_forest, 1), "partition_s": round(t_part, 1),
-            "max_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 2),
-            "owned_leaf_dofs": info["n_owned"],
-            "owned_level_dofs": [int(h.local_level(l)["owned_key"].size) for l in range(info["n_levels"])],
-            "ghost_level_dofs": [int(h.local_level(l)["ghost_key"].size) for l in range(info["n_levels"])]}
-    allv = [mine]
-    if world > 1:
-        allv = [None] * world
-        dist.all_gather_object(allv, mine)
+    out = {"rank": rank, "setup_s": round(t_setup, 1), "forest_s": round(t_forest, 1),
+           "partition_s": round(t_part, 1), "topology_s": round(t_setup - t_forest - t_part, 1),
+           "max_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 2),
+           "owned_leaf_dofs": info["n_owned"],
+           "owned_level_dofs": [int(h.local_level(l)["owned_key"].size) for l in range(info["n_levels"])],
+           "ghost_level_dofs": [int(h.local_level(l)["ghost_key"].size) for l in range(info["n_levels"])]}
     if rank == 0:
         m = part.model()
-        print(json.dumps({"dry_run": True, "config": args.config, "n_ranks": world,
-                          "n_leaves": f.info()["n_leaves"], "levels": info["n_levels"],
-                          "partition_eta": m["eta"], "ranks": allv}), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        out.update(n_leaves=f.info()["n_leaves"], levels=info["n_levels"], partition_eta=m["eta"])
+    return out
+
+
+def dry_run(args):
+    """--dry-run: the N-rank setup of a config on the host only.  Every rank's
+    rank-local setup (the part of the hierarchy it would hold) is built in its own
+    process -- at most --dry-run-parallel at a time, since ranks need no
+    communication for it -- and reports setup time and peak host RSS; one JSON
+    line (not a bench line).  E.g. `python bench.py --gpus 8 --config c5 --dry-run`
+    shows that config 5 at 8 x 125M DoFs sets up within the host's RAM."""
+    world = args.gpus
+    if os.environ.get("GMG_DRY_RANK") is not None:
+        print(json.dumps(dry_run_rank(args, int(os.environ["GMG_DRY_RANK"]), world)), flush=True)
+        return
+    procs, results = [], []
+    pending = list(range(world))
+    while pending or procs:
+        while pending and len(procs) < max(1, args.dry_run_parallel):
+            r = pending.pop(0)
+            env = dict(os.environ, GMG_DRY_RANK=str(r))
+            env.pop("WORLD_SIZE", None)
+            procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                          stdout=subprocess.PIPE, text=True))
+        p0 = procs.pop(0)
+        out, _ = p0.communicate()
+        if p0.returncode != 0:
+            raise SystemExit(f"dry-run rank failed: rc {p0.returncode}")
+        results.append(json.loads(out.strip().splitlines()[-1]))
+    results.sort(key=lambda d: d["rank"])
+    head = {k: results[0].pop(k) for k in ("n_leaves", "levels", "partition_eta")}
+    print(json.dumps({"dry_run": True, "config": args.config, "n_ranks": world, **head,
+                      "max_rss_gb_per_rank": max(r["max_rss_gb"] for r in results),
+                      "max_setup_s": max(r["setup_s"] for r in results), "ranks": results}), flush=True)
 
 
 def relaunch(args):
@@ -607,17 +626,18 @@ def main():
                     help="cudaProfilerStart/Stop around one V-cycle of the headline config (ncu launch lists)")
     ap.add_argument("--dry-run", action="store_true",
                     help="host-only rank-local setup of every rank, reports time and host RSS (no GPU)")
+    ap.add_argument("--dry-run-parallel", type=int, default=2, help="--dry-run: ranks set up concurrently")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
         return 0
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return relaunch(args)
     if args.dry_run:
         dry_run(args)
         return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     run_ours(args)
     return 0
 

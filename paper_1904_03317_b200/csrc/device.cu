@@ -41,6 +41,7 @@ struct DevLevel {
   i64 n_r1 = 0;                     // device order (plan.hpp): rows [0, n_r1) finished by the fused apply
   i64 n_gf = 0, n_single = 0;       // grandfamily patches / families left to the family kernel
   int* gx = nullptr;                // [n_gf][GF_ROW] grandfamily tables (plan.hpp)
+  int* gr1 = nullptr;               // [n_gf][2] the grandfamily's R1-row run (start, count)
   int* singles = nullptr;           // families not in a grandfamily
   double* gcoef = nullptr;          // coefficient per grandfamily (config 4)
   bool fuse_pro = false;            // prolongation fused into the first post-smoothing step on EVERY rank
@@ -287,10 +288,17 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
     const char* e = std::getenv("GMG_GF_PREFETCH");
     return !(e && e[0] == '0');
   }();
+  // GMG_GF_XPF: 0 off, 1 also prefetch x of the blocks half a wave ahead, 2 and the
+  // epilogue's R1-row runs
+  static const int xmode = [] {
+    const char* e = std::getenv("GMG_GF_XPF");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int wave = per_sm * d->sms;
   const int grid = (int)((v.n_gf + SL - 1) / SL);
   dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
       (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
-      prefetch ? per_sm * d->sms : 0);
+      prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr);
 }
 
 // The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
@@ -848,6 +856,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       v.n_gf = plan.n_gf[l];
       if (v.n_gf > 0) {
         v.gx = d->upload(plan.gx[l]);
+        v.gr1 = d->upload(plan.gr1[l]);
         v.n_single = (i64)plan.singles[l].size();
         v.singles = d->upload(plan.singles[l]);
         if (!plan.gcoef[l].empty()) v.gcoef = d->upload(plan.gcoef[l]);

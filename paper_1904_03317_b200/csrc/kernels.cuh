@@ -673,7 +673,8 @@ __global__ void __launch_bounds__(GfBlock<GF_SLOTS>::THREADS, GfBlock<GF_SLOTS>:
 gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict__ gcoef, double scale_,
                   const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                   const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0) {
+                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
+                  int xpf = 0, const int2* __restrict__ r1run = nullptr) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
@@ -686,6 +687,30 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
   }
   using LY = GfLayout<K>;
   constexpr int N1 = S::N1, NL = S::NL, ROW = S::ROW, NP = S::NP;
+  if (xpf > 0) {
+    // the x values (and, r1run, the epilogue's g, D^-1, dv runs) of the block xpf
+    // blocks ahead -> L2: its table row is already in L2 (prefetched pf > xpf ahead),
+    // so these requests turn its DRAM-latency gathers into L2 hits
+    const long qb = ((long)blockIdx.x + xpf) * GF_SLOTS + threadIdx.x / NL;
+    if (threadIdx.x / NL < GF_SLOTS && qb < ngf) {
+      const int* rq = gx + qb * (long)ROW;
+      const int ln = threadIdx.x % NL;
+#pragma unroll
+      for (int z = 0; z < N1; ++z) {
+        const int i = decode_dof(__ldg(rq + z * NL + ln));
+        if (i >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(x + i));
+      }
+      if (TM != TA_APPLY && r1run) {
+        const int2 run = __ldg(r1run + qb);
+        const int per_line = 128 / (int)sizeof(T);
+        for (int c = ln * per_line; c < run.y; c += NL * per_line) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(g + run.x + c));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(Dinv + run.x + c));
+          if (RDV && !DVX) asm volatile("prefetch.global.L2 [%0];" ::"l"(dv + run.x + c));
+        }
+      }
+    }
+  }
   extern __shared__ __align__(16) unsigned char gf_smem[];
   T* s0 = reinterpret_cast<T*>(gf_smem);
   T* s1 = s0 + GF_SLOTS * LY::SLOT;

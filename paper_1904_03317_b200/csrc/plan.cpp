@@ -42,6 +42,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
   P.n_gf.assign(L + 1, 0);
   P.gx.resize(L + 1);
   P.singles.resize(L + 1);
+  P.gr1.resize(L + 1);
   P.gcoef.resize(L + 1);
   // per level: grandfamilies in use (first local family of each) and a family ->
   // grandfamily map (-1: single)
@@ -185,6 +186,17 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
             row[GNP + a + NP1 * b + NP1 * NP1 * c] = xr[np + la + (k + 1) * lb + (k + 1) * (k + 1) * lc];
           }
       if (!v.fam_coef.empty()) P.gcoef[l].push_back(v.fam_coef[f0]);
+      // R1 rows of this grandfamily: a contiguous run (R1 is ordered by executed patch)
+      i32 lo = INT32_MAX, cntr = 0;
+      for (int a = 0; a < GNP; ++a) {
+        const i64 g = dec(row[a]);
+        if (g >= 0 && g < P.n_r1[l]) {
+          lo = std::min(lo, (i32)g);
+          ++cntr;
+        }
+      }
+      P.gr1[l].push_back(cntr ? lo : 0);
+      P.gr1[l].push_back(cntr);
     }
     for (i64 f = 0; f < v.n_fam; ++f)
       if (fg[f] < 0) P.singles[l].push_back((i32)f);

@@ -37,6 +37,7 @@ struct DevicePlan {
   // kernel through a list); singles is empty and n_gf = 0 where grandfamilies are off
   std::vector<i64> n_gf;
   std::vector<std::vector<i32>> gx, singles;
+  std::vector<std::vector<i32>> gr1;     // per grandfamily: (first R1 row, R1 rows) -- contiguous by construction
   std::vector<std::vector<double>> gcoef;
 };
 
