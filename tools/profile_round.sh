@@ -16,11 +16,14 @@ ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control no
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_c3.csv python bench.py --profile --config c3 --secondary none --no-cpu-baseline --steps 2 --warmup 3 \
     > $OUT/ncu_launch_c3.log 2>&1
-# tensor launches of a V-cycle start at level 10: X1 (gfam, fam), 11 (gfam, fam), 11, 10, apply
+# tensor launches of a V-cycle start on the finest level: pre-smoothing X1, 11, 10, then the
+# residual's plain apply (c5: each a grandfamily + a family kernel; c3's finest level: family only)
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply \
     --launch-skip 2 --launch-count 2 -o $OUT/ncu_c5_cheb11 -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply \
-    --launch-skip 4 --launch-count 1 -o $OUT/ncu_c3_apply -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3.log 2>&1
+    --launch-skip 3 --launch-count 1 -o $OUT/ncu_c3_apply -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3.log 2>&1
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply \
+    --launch-skip 6 --launch-count 2 -o $OUT/ncu_c5_apply -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full_c5a.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply \
     --launch-skip 1 --launch-count 1 -o $OUT/ncu_c3_cheb11 -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3b.log 2>&1
 echo done
