@@ -348,6 +348,26 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
     if (!host_only) {
       if (prm->coef_level2) gmg::attach_coefficients(h->local, f->f, P, prm->coef_level2);
       h->dev = gmg::device_create(h->local, *prm, std::move(comm), z.n0);
+      // the device holds its own copies: drop the host tables (large for rank-local
+      // runs of 125M DoFs per rank); keys, plans and counts stay for the exports
+      for (auto& v : h->local.lv) {
+        for (auto* t : {&v.cell_dofs, &v.fam_dofs, &v.xfer, &v.leaf_cells, &v.edge_fams, &v.gf_first}) {
+          t->clear();
+          t->shrink_to_fit();
+        }
+        for (auto* t : {&v.cls, &v.lam}) {
+          t->clear();
+          t->shrink_to_fit();
+        }
+        for (auto* t : {&v.eig_v, &v.cell_coef, &v.fam_coef, &v.cell_elem}) {
+          t->clear();
+          t->shrink_to_fit();
+        }
+        v.cell_global.clear();
+        v.cell_global.shrink_to_fit();
+      }
+      h->local.leaf_local.clear();
+      h->local.leaf_local.shrink_to_fit();
     }
     *out = h.release();
   });

@@ -42,6 +42,12 @@ struct DevLevel {
   i64 n_gf = 0, n_single = 0;       // grandfamily patches / families left to the family kernel
   int* gx = nullptr;                // [n_gf][GF_ROW] grandfamily tables (plan.hpp)
   int* gr1 = nullptr;               // [n_gf][2] the grandfamily's R1-row run (start, count)
+  // several ranks: interior / boundary patch lists (plan.hpp) for the overlap of the
+  // ghost import with the interior patches
+  int *fam_int = nullptr, *fam_bnd = nullptr, *gf_int = nullptr, *gf_bnd = nullptr;
+  i64 n_fam_int = 0, n_fam_bnd = 0, n_gf_int = 0, n_gf_bnd = 0;
+  bool split = false;
+  cudaEvent_t ev_pack = nullptr, ev_ghost = nullptr;
   int* singles = nullptr;           // families not in a grandfamily
   double* gcoef = nullptr;          // coefficient per grandfamily (config 4)
   bool fuse_pro = false;            // prolongation fused into the first post-smoothing step on EVERY rank
@@ -89,6 +95,8 @@ struct DeviceHierarchy {
   bool use_graph = true;
   bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
   int gf_slots = 1;             // grandfamilies per block of gfam_tensor_apply (GMG_GF_SLOTS = 1, 2, 3)
+  bool overlap = true;          // several ranks: interior patches overlap the ghost import (GMG_OVERLAP=0: off)
+  cudaStream_t cstream = nullptr;   // the import's side stream
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
   long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
@@ -275,7 +283,7 @@ static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t v
 
 template <int K, typename T, int TM, int SL>
 static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1,
-                      double c2, const T* xc, cudaStream_t s) {
+                      double c2, const T* xc, cudaStream_t s, const int* glist = nullptr, i64 ng = -1) {
   static const int per_sm = [] {
     CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)dev::gf_smem_bytes<K, T, SL>()));
@@ -295,37 +303,63 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
     return e ? std::atoi(e) : 0;
   }();
   const int wave = per_sm * d->sms;
-  const int grid = (int)((v.n_gf + SL - 1) / SL);
+  if (ng < 0) ng = v.n_gf;
+  if (ng == 0) return;
+  const int grid = (int)((ng + SL - 1) / SL);
   dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
-      (int)v.n_gf, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
-      prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr);
+      (int)ng, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
+      prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr, glist);
+  d->launches++;
 }
 
 // The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
 // plus the remaining families (fam_tensor_apply over the singles list), or all
 // families.  Epilogue mode TM, fused Chebyshev arguments as fam_tensor_apply.
+// phase: 0 all patches, 1 the interior ones (no ghost node), 2 the boundary ones.
 template <int K, typename T, int TM>
 static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1,
-                          double c2, const T* xc, cudaStream_t s) {
+                          double c2, const T* xc, cudaStream_t s, int phase = 0) {
   const int np = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), nn = (K + 1) * (K + 1) * (K + 1);
   if (v.n_gf > 0) {
-    if (d->gf_slots == 1) launch_gf<K, T, TM, 1>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
-    else if (d->gf_slots == 2) launch_gf<K, T, TM, 2>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
-    else launch_gf<K, T, TM, 3>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
-    d->launches++;
+    const int* gl = phase == 1 ? v.gf_int : (phase == 2 ? v.gf_bnd : nullptr);
+    const i64 ng = phase == 1 ? v.n_gf_int : (phase == 2 ? v.n_gf_bnd : v.n_gf);
+    if (d->gf_slots == 1) launch_gf<K, T, TM, 1>(d, v, x, y, g, dv, xw, c1, c2, xc, s, gl, ng);
+    else if (d->gf_slots == 2) launch_gf<K, T, TM, 2>(d, v, x, y, g, dv, xw, c1, c2, xc, s, gl, ng);
+    else launch_gf<K, T, TM, 3>(d, v, x, y, g, dv, xw, c1, c2, xc, s, gl, ng);
   }
-  const i64 nf = v.n_gf > 0 ? v.n_single : v.n_fam;
+  const int* fl = phase == 1 ? v.fam_int : (phase == 2 ? v.fam_bnd : (v.n_gf > 0 ? v.singles : nullptr));
+  const i64 nf = phase == 1 ? v.n_fam_int : (phase == 2 ? v.n_fam_bnd : (v.n_gf > 0 ? v.n_single : v.n_fam));
   if (nf > 0) {
     if constexpr (K == 2)
       dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
           (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
-          v.n_gf > 0 ? 0 : tensor_wave<K, T, TM>(d), v.n_gf > 0 ? v.singles : nullptr);
+          fl ? 0 : tensor_wave<K, T, TM>(d), fl);
     else
       dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc, 0,
-          v.n_gf > 0 ? v.singles : nullptr);
+          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc, 0, fl);
     d->launches++;
   }
+}
+
+// ghost import of x followed by the tensor operator on level l: with several
+// ranks and a split level, the import runs on the side stream while the interior
+// patches (no ghost node) compute, the boundary patches after it
+template <int K, typename T, int TM>
+static void import_and_tensor(DeviceHierarchy* d, int l, T* x, T* y, const T* g, T* dv, T* xw, double c1, double c2,
+                              const T* xc, cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  if (!(d->comm && d->overlap && v.split)) {
+    import_ghosts(d, l, x, s);
+    launch_tensor<K, T, TM>(d, v, x, y, g, dv, xw, c1, c2, xc, s);
+    return;
+  }
+  CK(cudaEventRecord(v.ev_pack, s));
+  CK(cudaStreamWaitEvent(d->cstream, v.ev_pack, 0));
+  import_ghosts(d, l, x, d->cstream);
+  CK(cudaEventRecord(v.ev_ghost, d->cstream));
+  launch_tensor<K, T, TM>(d, v, x, y, g, dv, xw, c1, c2, xc, s, 1);
+  CK(cudaStreamWaitEvent(s, v.ev_ghost, 0));
+  launch_tensor<K, T, TM>(d, v, x, y, g, dv, xw, c1, c2, xc, s, 2);
 }
 
 template <typename T>
@@ -378,8 +412,17 @@ static void k_apply(DeviceHierarchy* d, int l, const int* list, i64 n, const T* 
 // t = K_l x on owned rows: ghost import of x, local family apply, export-add of t
 template <typename T>
 static void apply_full(DeviceHierarchy* d, int l, T* x, T* t, cudaStream_t s) {
-  import_ghosts(d, l, x, s);
-  k_apply(d, l, nullptr, d->lv[l].n_cells, x, t, s);
+  DevLevel& v = d->lv[l];
+  if (d->comm && d->overlap && v.split) {        // 3D tensor level split into interior / boundary patches
+    Prof pr(d, s, GMG_K_APPLY, l, apply_bytes(d, v, sizeof(T)), apply_layout(d, v, sizeof(T)));
+    if (d->k == 2)
+      import_and_tensor<2, T, dev::TA_APPLY>(d, l, x, t, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+    else
+      import_and_tensor<1, T, dev::TA_APPLY>(d, l, x, t, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+  } else {
+    import_ghosts(d, l, x, s);
+    k_apply(d, l, nullptr, v.n_cells, x, t, s);
+  }
   export_add(d, l, t, s);
 }
 
@@ -446,7 +489,6 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
                             cudaStream_t s, const T* xc = nullptr) {
   constexpr bool PRO = TM == dev::TA_CHEB_P01;   // x + P x_{l-1} (xc) fused in; only called where n_r1 > 0
   DevLevel& v = d->lv[l];
-  import_ghosts(d, l, x, s);
   if (v.n_r1 > 0) {
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
     // the operator's x gather and index rows, t (reduced) on the rows outside R1,
@@ -462,9 +504,9 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
                    : TM == dev::TA_CHEB_01 ? GMG_K_CHEB_01 : GMG_K_CHEB_00;
     Prof pr(d, s, kind, l, fb + idx, fb + idx_layout);
     if (d->k == 2)
-      launch_tensor<2, T, TM>(d, v, x, t, g, dv, x, c1, c2, xc, s);
+      import_and_tensor<2, T, TM>(d, l, x, t, g, dv, x, c1, c2, xc, s);
     else
-      launch_tensor<1, T, TM>(d, v, x, t, g, dv, x, c1, c2, xc, s);
+      import_and_tensor<1, T, TM>(d, l, x, t, g, dv, x, c1, c2, xc, s);
     pr.end();
     export_add(d, l, t, s);
     const i64 n = v.n_pad - v.n_r1;
@@ -477,6 +519,7 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     }
   } else {
     if (PRO) throw Error(GMG_E_STATE, "fused prolongation on a level without R1");
+    import_ghosts(d, l, x, s);
     k_apply(d, l, nullptr, v.n_cells, (const T*)x, t, s);
     export_add(d, l, t, s);
     k_cheb<T, true, RDV, WDV, false, DVX>(d, v, g, t, dv, x, c1, c2, s);
@@ -815,6 +858,8 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     if (const char* e = std::getenv("GMG_GF_SLOTS")) d->gf_slots = std::max(1, std::min(3, std::atoi(e)));
     GMG_REQUIRE(d->m >= 1 && d->m <= 16, GMG_E_INVALID_ARG, "cheb_degree must be in [1,16]");
     CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d->cstream, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("GMG_OVERLAP")) d->overlap = !(e[0] == '0');
     const int nn = Tp.dim == 2 ? (Tp.k + 1) * (Tp.k + 1) : (Tp.k + 1) * (Tp.k + 1) * (Tp.k + 1);
     d->lv.resize(Tp.L + 1);
     i64 off = 0, xmax = 1;
@@ -853,6 +898,19 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       v.leaf_cells = d->upload(t.leaf_cells);
       v.n_r1 = plan.n_r1[l];
       v.perm = d->upload(plan.perm[l]);
+      v.n_fam_int = (i64)plan.fam_int[l].size();
+      v.n_fam_bnd = (i64)plan.fam_bnd[l].size();
+      v.n_gf_int = (i64)plan.gf_int[l].size();
+      v.n_gf_bnd = (i64)plan.gf_bnd[l].size();
+      v.split = v.n_fam_int + v.n_gf_int > 0;
+      if (v.split) {
+        v.fam_int = d->upload(plan.fam_int[l]);
+        v.fam_bnd = d->upload(plan.fam_bnd[l]);
+        v.gf_int = d->upload(plan.gf_int[l]);
+        v.gf_bnd = d->upload(plan.gf_bnd[l]);
+        CK(cudaEventCreateWithFlags(&v.ev_pack, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&v.ev_ghost, cudaEventDisableTiming));
+      }
       v.n_gf = plan.n_gf[l];
       if (v.n_gf > 0) {
         v.gx = d->upload(plan.gx[l]);
@@ -1071,6 +1129,11 @@ void device_destroy(DeviceHierarchy* d) {
   cudaDeviceSynchronize();
   if (d->vgraph) cudaGraphExecDestroy(d->vgraph);
   for (cudaEvent_t e : d->evpool) cudaEventDestroy(e);
+  for (auto& v : d->lv) {
+    if (v.ev_pack) cudaEventDestroy(v.ev_pack);
+    if (v.ev_ghost) cudaEventDestroy(v.ev_ghost);
+  }
+  if (d->cstream) cudaStreamDestroy(d->cstream);
   for (auto& a : d->allocs) {
     if (d->dev_free) d->dev_free(a.first, a.second, nullptr, d->alloc_ctx);
     else cudaFree(a.first);

@@ -674,12 +674,12 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
                   const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                   const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
                   double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
-                  int xpf = 0, const int2* __restrict__ r1run = nullptr) {
+                  int xpf = 0, const int2* __restrict__ r1run = nullptr, const int* __restrict__ glist = nullptr) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   using S = GfShape<K>;
-  if (pf > 0) {   // the table rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
+  if (pf > 0 && !glist) {   // the table rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
     const long fb = ((long)blockIdx.x + pf) * GF_SLOTS;
     const long bytes = (long)GF_SLOTS * GfShape<K>::ROW * 4, off = (long)threadIdx.x * 128;
     if (fb < ngf && off < bytes && fb * GfShape<K>::ROW * 4 + off < (long)ngf * GfShape<K>::ROW * 4)
@@ -687,7 +687,7 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
   }
   using LY = GfLayout<K>;
   constexpr int N1 = S::N1, NL = S::NL, ROW = S::ROW, NP = S::NP;
-  if (xpf > 0) {
+  if (xpf > 0 && !glist) {
     // the x values (and, r1run, the epilogue's g, D^-1, dv runs) of the block xpf
     // blocks ahead -> L2: its table row is already in L2 (prefetched pf > xpf ahead),
     // so these requests turn its DRAM-latency gathers into L2 hits
@@ -716,8 +716,10 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
   T* s1 = s0 + GF_SLOTS * LY::SLOT;
   T* cbase = s1 + GF_SLOTS * LY::SLOT;             // PRO: G's coarse patch per slot
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;
-  const long q0 = (long)blockIdx.x * GF_SLOTS + slot;
-  const bool act = slot < GF_SLOTS && q0 < ngf;
+  const long qi = (long)blockIdx.x * GF_SLOTS + slot;
+  const bool act = slot < GF_SLOTS && qi < ngf;
+  // glist: a subset of the grandfamilies (interior / boundary ones, overlap with the import)
+  const long q0 = glist ? (act ? (long)__ldg(glist + qi) : 0) : qi;
   const int* rp = gx + (act ? q0 : 0) * (long)ROW;
   T* const a0 = s0 + (act ? slot : 0) * LY::SLOT;
   T* const a1 = s1 + (act ? slot : 0) * LY::SLOT;

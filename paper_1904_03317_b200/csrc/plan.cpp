@@ -43,6 +43,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
   P.gx.resize(L + 1);
   P.singles.resize(L + 1);
   P.gr1.resize(L + 1);
+  for (auto* v : {&P.fam_int, &P.fam_bnd, &P.gf_int, &P.gf_bnd}) v->resize(L + 1);
   P.gcoef.resize(L + 1);
   // per level: grandfamilies in use (first local family of each) and a family ->
   // grandfamily map (-1: single)
@@ -201,6 +202,26 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
     for (i64 f = 0; f < v.n_fam; ++f)
       if (fg[f] < 0) P.singles[l].push_back((i32)f);
   }
+  // ---------------- interior / boundary patches (several ranks: overlap with the import)
+  if (T.n_ranks > 1)
+    for (int l = 1; l <= L; ++l) {
+      const LocalLevel& v = T.lv[l];
+      const bool tensor3 = d == 3 && v.n_fam > 0 && v.cell_elem.empty() && (v.cell_coef.empty() || !v.fam_coef.empty());
+      if (!tensor3) continue;
+      auto ghost_in = [&](const i32* row, int n) {
+        for (int a = 0; a < n; ++a)
+          if (dec(row[a]) >= v.n_owned) return true;
+        return false;
+      };
+      const std::vector<i32>* fams = P.n_gf[l] > 0 ? &P.singles[l] : nullptr;
+      const i64 nf = fams ? (i64)fams->size() : v.n_fam;
+      for (i64 i = 0; i < nf; ++i) {
+        const i64 f = fams ? (*fams)[i] : i;
+        (ghost_in(v.fam_dofs.data() + (size_t)f * np, np) ? P.fam_bnd : P.fam_int)[l].push_back((i32)f);
+      }
+      for (i64 q = 0; q < P.n_gf[l]; ++q)
+        (ghost_in(P.gx[l].data() + (size_t)q * GROW, GNP) ? P.gf_bnd : P.gf_int)[l].push_back((i32)q);
+    }
   return P;
 }
 

@@ -38,6 +38,10 @@ struct DevicePlan {
   std::vector<i64> n_gf;
   std::vector<std::vector<i32>> gx, singles;
   std::vector<std::vector<i32>> gr1;     // per grandfamily: (first R1 row, R1 rows) -- contiguous by construction
+  // n_ranks > 1: executed patches split into interior (no ghost node: can run while
+  // the ghost import is in flight) and boundary ones -- family indices (over the
+  // families the family kernel runs) and grandfamily indices; empty for one rank
+  std::vector<std::vector<i32>> fam_int, fam_bnd, gf_int, gf_bnd;
   std::vector<std::vector<double>> gcoef;
 };
 

@@ -20,7 +20,11 @@ ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--tag", default="")
 args = ap.parse_args()
 cfg = config_c5(1) if args.config == "c5" else config(args.config)
-_, _, h = G.build_config(cfg, mixed=args.mixed)
+coef = None
+if cfg.get("coef") == "level2_log_uniform":          # config 4: a per level-2 cell
+    from gmg_inputs import log_uniform_coef
+    coef = log_uniform_coef(4 ** cfg["dim"] * len(cfg["trees"]))
+_, _, h = G.build_config(cfg, mixed=args.mixed, coef_level2=coef)
 info = h.info()
 b = torch.tensor(uniform_pm1(info["n_leaf_free"]), device="cuda", dtype=torch.float64)
 x = torch.zeros_like(b)
