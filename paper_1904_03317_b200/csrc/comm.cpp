@@ -50,8 +50,8 @@ void LocalWorld::barrier() {
   }
 }
 
-void ThreadComm::exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
-                          double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) {
+void ThreadComm::exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff,
+                          void* recvbuf, const std::vector<i64>& roff, size_t esize, cudaStream_t s) {
   auto& me = w->slot[r];
   me.sendbuf = sendbuf;
   me.peers = &peers;
@@ -69,8 +69,8 @@ void ThreadComm::exchange(const std::vector<int>& peers, const double* sendbuf, 
     GMG_REQUIRE(cnt == roff[i + 1] - roff[i], GMG_E_STATE, "exchange count mismatch");
     if (cnt == 0) continue;
     CKC(cudaStreamWaitEvent(s, other.packed, 0));
-    CKC(cudaMemcpyAsync(recvbuf + roff[i], other.sendbuf + (*other.soff)[j], cnt * sizeof(double),
-                        cudaMemcpyDeviceToDevice, s));
+    CKC(cudaMemcpyAsync((char*)recvbuf + roff[i] * esize, (const char*)other.sendbuf + (*other.soff)[j] * esize,
+                        cnt * esize, cudaMemcpyDeviceToDevice, s));
   }
   CKC(cudaEventRecord(me.copied, s));
   w->barrier();                       // every rank has enqueued its copies
@@ -152,18 +152,18 @@ void HostWorld::barrier() {
   }
 }
 
-void HostComm::exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
-                        double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) {
+void HostComm::exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff,
+                        void* recvbuf, const std::vector<i64>& roff, size_t esize, cudaStream_t s) {
   const int me = w->rank;
   i64* dir = w->dir(me);
   for (int q = 0; q < w->n; ++q) dir[2 * q] = dir[2 * q + 1] = 0;
   const i64 ns = soff.empty() ? 0 : soff.back();
-  GMG_REQUIRE((size_t)ns <= w->payload_cap(), GMG_E_OOM, "host world slot too small for an exchange");
+  GMG_REQUIRE((size_t)ns * esize <= w->payload_bytes(), GMG_E_OOM, "host world slot too small for an exchange");
   for (size_t i = 0; i < peers.size(); ++i) {
     dir[2 * peers[i]] = soff[i];
     dir[2 * peers[i] + 1] = soff[i + 1] - soff[i];
   }
-  if (ns) CKC(cudaMemcpyAsync(w->payload(me), sendbuf, ns * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (ns) CKC(cudaMemcpyAsync(w->payload(me), sendbuf, ns * esize, cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
   w->barrier();                       // every slot is written
   for (size_t i = 0; i < peers.size(); ++i) {
@@ -172,8 +172,8 @@ void HostComm::exchange(const std::vector<int>& peers, const double* sendbuf, co
     const i64 cnt = od[2 * me + 1];
     GMG_REQUIRE(cnt == roff[i + 1] - roff[i], GMG_E_STATE, "exchange count mismatch");
     if (cnt)
-      CKC(cudaMemcpyAsync(recvbuf + roff[i], w->payload(q) + od[2 * me], cnt * sizeof(double),
-                          cudaMemcpyHostToDevice, s));
+      CKC(cudaMemcpyAsync((char*)recvbuf + roff[i] * esize, (const char*)w->payload(q) + od[2 * me] * esize,
+                          cnt * esize, cudaMemcpyHostToDevice, s));
   }
   CKC(cudaStreamSynchronize(s));
   w->barrier();                       // every slot is read: it may be rewritten
@@ -197,7 +197,7 @@ namespace {
 typedef int ncclResult_t;
 typedef void* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
-constexpr int ncclFloat64 = 8, ncclSum = 0;
+constexpr int ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0;
 struct NcclApi {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
@@ -251,15 +251,17 @@ NcclComm::NcclComm(void* c) : comm(c) {
   ckn(nccl().CommCount(comm, &n), "ncclCommCount");
 }
 
-void NcclComm::exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
-                        double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) {
+void NcclComm::exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff,
+                        void* recvbuf, const std::vector<i64>& roff, size_t esize, cudaStream_t s) {
   if (peers.empty()) return;
   auto& a = nccl();
+  const int dt = esize == 4 ? ncclFloat32 : ncclFloat64;
+  GMG_REQUIRE(esize == 4 || esize == 8, GMG_E_INVALID_ARG, "wire element size");
   ckn(a.GroupStart(), "ncclGroupStart");
   for (size_t i = 0; i < peers.size(); ++i) {
     const i64 sc = soff[i + 1] - soff[i], rc = roff[i + 1] - roff[i];
-    if (sc) ckn(a.Send(sendbuf + soff[i], (size_t)sc, ncclFloat64, peers[i], comm, s), "ncclSend");
-    if (rc) ckn(a.Recv(recvbuf + roff[i], (size_t)rc, ncclFloat64, peers[i], comm, s), "ncclRecv");
+    if (sc) ckn(a.Send((const char*)sendbuf + soff[i] * esize, (size_t)sc, dt, peers[i], comm, s), "ncclSend");
+    if (rc) ckn(a.Recv((char*)recvbuf + roff[i] * esize, (size_t)rc, dt, peers[i], comm, s), "ncclRecv");
   }
   ckn(a.GroupEnd(), "ncclGroupEnd");
 }

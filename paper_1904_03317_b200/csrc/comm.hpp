@@ -24,9 +24,10 @@ struct Comm {
   virtual int rank() const = 0;
   virtual int size() const = 0;
   // Exchange one contiguous chunk per peer: to peers[i] send sendbuf[soff[i], soff[i+1]),
-  // from peers[i] receive into recvbuf[roff[i], roff[i+1]).  Stream-ordered.
-  virtual void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff,
-                        double* recvbuf, const std::vector<i64>& roff, cudaStream_t s) = 0;
+  // from peers[i] receive into recvbuf[roff[i], roff[i+1]) -- offsets in elements of
+  // esize bytes (8: fp64, 4: fp32 wire format).  Stream-ordered.
+  virtual void exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff,
+                        void* recvbuf, const std::vector<i64>& roff, size_t esize, cudaStream_t s) = 0;
   // in-place sum over ranks of n doubles (device memory), stream-ordered
   virtual void allreduce(double* buf, int n, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;   // may be captured in a CUDA graph
@@ -43,7 +44,7 @@ struct LocalWorld {
   long long generation = 0;
   void barrier();
   struct Slot {
-    const double* sendbuf = nullptr;
+    const void* sendbuf = nullptr;
     const std::vector<int>* peers = nullptr;
     const std::vector<i64>* soff = nullptr;
     cudaEvent_t packed = nullptr, copied = nullptr;
@@ -59,8 +60,8 @@ struct ThreadComm : Comm {
   int r;
   int rank() const override { return r; }
   int size() const override { return w->n; }
-  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
-                const std::vector<i64>& roff, cudaStream_t s) override;
+  void exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff, void* recvbuf,
+                const std::vector<i64>& roff, size_t esize, cudaStream_t s) override;
   void allreduce(double* buf, int n, cudaStream_t s) override;
   bool capturable() const override { return false; }
 };
@@ -85,7 +86,8 @@ struct HostWorld {
   // slot q: [directory: n x (offset, count) as i64][payload doubles]
   i64* dir(int q) const { return (i64*)(base + 4096 + (size_t)q * slot_bytes); }
   double* payload(int q) const { return (double*)(base + 4096 + (size_t)q * slot_bytes + 16 * (size_t)n); }
-  size_t payload_cap() const { return (slot_bytes - 16 * (size_t)n) / sizeof(double); }
+  size_t payload_bytes() const { return slot_bytes - 16 * (size_t)n; }
+  size_t payload_cap() const { return payload_bytes() / sizeof(double); }
 };
 
 struct HostComm : Comm {
@@ -93,8 +95,8 @@ struct HostComm : Comm {
   HostWorld* w;
   int rank() const override { return w->rank; }
   int size() const override { return w->n; }
-  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
-                const std::vector<i64>& roff, cudaStream_t s) override;
+  void exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff, void* recvbuf,
+                const std::vector<i64>& roff, size_t esize, cudaStream_t s) override;
   void allreduce(double* buf, int n, cudaStream_t s) override;
   bool capturable() const override { return false; }
 };
@@ -106,8 +108,8 @@ struct NcclComm : Comm {
   int r = 0, n = 1;
   int rank() const override { return r; }
   int size() const override { return n; }
-  void exchange(const std::vector<int>& peers, const double* sendbuf, const std::vector<i64>& soff, double* recvbuf,
-                const std::vector<i64>& roff, cudaStream_t s) override;
+  void exchange(const std::vector<int>& peers, const void* sendbuf, const std::vector<i64>& soff, void* recvbuf,
+                const std::vector<i64>& roff, size_t esize, cudaStream_t s) override;
   void allreduce(double* buf, int n, cudaStream_t s) override;
   bool capturable() const override { return true; }
 };

@@ -214,13 +214,15 @@ static void import_ghosts(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
   Prof pr(d, s, GMG_K_EXCHANGE, l, (double)(v.n_send + v.n_recv) * (sizeof(T) + 4 + 8));
+  T* sb = reinterpret_cast<T*>(d->sbuf);
+  T* rb = reinterpret_cast<T*>(d->rbuf);
   if (v.n_send) {
-    dev::pack<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, d->sbuf);
+    dev::pack<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, vec, sb);
     d->launches++;
   }
-  d->comm->exchange(v.peers, d->sbuf, v.send_off, d->rbuf, v.recv_off, s);
+  d->comm->exchange(v.peers, sb, v.send_off, rb, v.recv_off, sizeof(T), s);   // wire format = the vector's type
   if (v.n_recv) {
-    dev::unpack_set<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, d->rbuf, vec);
+    dev::unpack_set<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, rb, vec);
     d->launches++;
   }
 }
@@ -230,13 +232,15 @@ static void export_add(DeviceHierarchy* d, int l, T* vec, cudaStream_t s) {
   if (!d->comm) return;
   DevLevel& v = d->lv[l];
   Prof pr(d, s, GMG_K_EXCHANGE, l, (double)(v.n_send + v.n_recv) * (2 * sizeof(T) + 4 + 8));
+  T* sb = reinterpret_cast<T*>(d->sbuf);
+  T* rb = reinterpret_cast<T*>(d->rbuf);
   if (v.n_recv) {
-    dev::pack_zero<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, d->sbuf);
+    dev::pack_zero<T><<<(int)((v.n_recv + 255) / 256), 256, 0, s>>>(v.n_recv, v.recv_idx, vec, sb);
     d->launches++;
   }
-  d->comm->exchange(v.peers, d->sbuf, v.recv_off, d->rbuf, v.send_off, s);
+  d->comm->exchange(v.peers, sb, v.recv_off, rb, v.send_off, sizeof(T), s);
   if (v.n_send) {
-    dev::unpack_add<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, d->rbuf, vec);
+    dev::unpack_add<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, rb, vec);
     d->launches++;
   }
 }

@@ -1316,32 +1316,32 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
 }
 
 // ------------------------------------------------------------- ghost exchange
-// (the wire format is fp64 for every vector precision)
+// (the wire format is the vector's precision: fp32 ghosts in the mixed-precision V-cycle)
 template <typename T>
-__global__ void pack(long n, const int* __restrict__ idx, const T* __restrict__ v, double* __restrict__ buf) {
+__global__ void pack(long n, const int* __restrict__ idx, const T* __restrict__ v, T* __restrict__ buf) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) buf[i] = (double)v[idx[i]];
+  if (i < n) buf[i] = v[idx[i]];
 }
 // ghosts -> buffer, ghost entries reset (data-dependent, see cheb_step)
 template <typename T>
-__global__ void pack_zero(long n, const int* __restrict__ idx, T* __restrict__ v, double* __restrict__ buf) {
+__global__ void pack_zero(long n, const int* __restrict__ idx, T* __restrict__ v, T* __restrict__ buf) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const T a = v[idx[i]];
-    buf[i] = (double)a;
+    buf[i] = a;
     v[idx[i]] = a - a;
   }
 }
 template <typename T>
-__global__ void unpack_set(long n, const int* __restrict__ idx, const double* __restrict__ buf, T* __restrict__ v) {
+__global__ void unpack_set(long n, const int* __restrict__ idx, const T* __restrict__ buf, T* __restrict__ v) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[idx[i]] = (T)buf[i];
+  if (i < n) v[idx[i]] = buf[i];
 }
 // an owned DoF may be a ghost of several peers: atomic add
 template <typename T>
-__global__ void unpack_add(long n, const int* __restrict__ idx, const double* __restrict__ buf, T* __restrict__ v) {
+__global__ void unpack_add(long n, const int* __restrict__ idx, const T* __restrict__ buf, T* __restrict__ v) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(v + idx[i], (T)buf[i]);
+  if (i < n) atomicAdd(v + idx[i], buf[i]);
 }
 
 // ------------------------------------------------------------- misc vector kernels
