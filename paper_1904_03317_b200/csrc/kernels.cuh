@@ -630,10 +630,13 @@ __host__ __device__ __forceinline__ constexpr double Mt4(int i, int j) {
 #ifndef GF_LOAD_AT_DEFAULT
 #define GF_LOAD_AT_DEFAULT 2
 #endif
-constexpr int GF_LOAD_AT = GF_LOAD_AT_DEFAULT;   // fused epilogue loads: 1 after the z pass, 2 after the x pass
+constexpr int GF_LOAD_AT = GF_LOAD_AT_DEFAULT;   // fused epilogue loads: 1 after the z pass, 2 after the x pass, 3 per row in the scatter
+#ifndef GF_REG_CAP
+#define GF_REG_CAP 80
+#endif
 template <int SLOTS> struct GfBlock {
   static constexpr int THREADS = SLOTS == 1 ? 96 : (SLOTS == 2 ? 192 : 256);
-  static constexpr int MIN_BLOCKS = 65536 / (THREADS * 80);
+  static constexpr int MIN_BLOCKS = 65536 / (THREADS * GF_REG_CAP);
 };
 template <int K> struct GfShape {
   static constexpr int N1 = 4 * K + 1, NL = N1 * N1, NP = N1 * N1 * N1;
@@ -904,6 +907,11 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
       if (i < 0) continue;
       const T v = a0[bn + LY::nz * z];
       if (TM != TA_APPLY && i < n_r1) {
+        if (GF_LOAD_AT == 3) {   // requested here, one row at a time (fewer live registers)
+          pg[z] = __ldg(g + i);
+          pd[z] = __ldg(Dinv + i);
+          if (RDV && !DVX) pv[z] = dv[i];
+        }
         T dd = (T)c2_ * pd[z] * (pg[z] - v);
         if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
         if (WDV) dv[i] = dd;
