@@ -76,3 +76,67 @@ def test_rank_local_global_exports_refused():
         h.level_dofs(1)
     with pytest.raises(G.GmgError):
         h.leaf_dofs()
+
+
+# ------------------------------------------------------------------ gloo, world size 2 and 3
+def _plan_worker(rank, world, port, name, coarse, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cfg, passes = _cfg(name)
+        f = G.gmg_forest_generate(G.recipe_from_config(cfg, passes))
+        part = G.gmg_partition(f, world, coarse_cells=coarse)
+        h = G.gmg_setup(f, part, k=cfg["k"], rank=rank, host_only=True, rank_local=True)
+        mine = []
+        for l in range(h.info()["n_levels"]):
+            lv = h.local_level(l)
+            sends = {}
+            for i, peer in enumerate(lv["peers"]):
+                idx = lv["send_idx"][lv["send_off"][i]:lv["send_off"][i + 1]]
+                sends[int(peer)] = lv["owned_key"][idx].tolist()
+            recvs = {}
+            for i, peer in enumerate(lv["peers"]):
+                idx = lv["recv_idx"][lv["recv_off"][i]:lv["recv_off"][i + 1]] - lv["owned_key"].size
+                recvs[int(peer)] = lv["ghost_key"][idx].tolist()
+                assert (lv["ghost_owner"][idx] == peer).all()
+            mine.append((sends, recvs, lv["owned_key"].tolist()))
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        # the plans of every pair match key by key, and no DoF is owned twice
+        for l in range(len(mine)):
+            for r in range(world):
+                for peer, keys in allv[r][l][0].items():
+                    assert allv[peer][l][1].get(r, []) == keys, (l, r, peer)
+                for peer, keys in allv[r][l][1].items():
+                    assert allv[peer][l][0].get(r, []) == keys, (l, r, peer)
+            owned = [k for r in range(world) for k in allv[r][l][2]]
+            assert len(owned) == len(set(owned))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("name,world,coarse", [("c3p2", 2, 0), ("c4s", 3, 0), ("c3p2", 3, 600)])
+def test_gloo_rank_local_exchange_plans_match(name, world, coarse):
+    """Each rank builds only its own part (rank-local); over gloo the ranks check
+    that what r sends to q is, key by key and in order, what q expects from r, and
+    that the owned sets are disjoint."""
+    import multiprocessing as mp
+    import socket
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ps = [ctx.Process(target=_plan_worker, args=(r, world, port, name, coarse, q)) for r in range(world)]
+    for p_ in ps:
+        p_.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p_ in ps:
+        p_.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res
