@@ -200,7 +200,9 @@ gmg_status gmg_export_level_cells(const gmg_partitioning *p, int level, int64_t 
                                  stream each, same GPU); params.nccl_comm is a gmg_local_world */
 #define GMG_RANK_LOCAL 32u    /* build only this rank's part of the level topology:
                                  no global level numbering (global exports -> GMG_E_STATE), global
-                                 sizes summed over the communicator; implies GMG_EIG_KEY */
+                                 sizes summed over the communicator (with GMG_HOST_ONLY and
+                                 n_ranks > 1 there is none: gmg_info's global sizes are -1);
+                                 implies GMG_EIG_KEY */
 #define GMG_EIG_KEY 64u       /* eigen start vector -5.5 + (level-lattice Morton key mod 12) on the
                                  S DoFs (reading R10b, rank-local) instead of the canonical-rank
                                  pattern of R10 */
