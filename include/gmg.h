@@ -458,7 +458,8 @@ typedef enum {
   GMG_K_EXCHANGE = 12,
   GMG_K_COPY_MG = 13,       /* copy_to_mg / copy_from_mg */
   GMG_K_LEAF_APPLY = 14,
-  GMG_K_OTHER = 15
+  GMG_K_OTHER = 15,
+  GMG_K_SMALL = 16          /* the small levels' V-cycle in one persistent kernel (small_vcycle) */
 } gmg_kernel_kind;
 typedef struct {
   int kind;                 /* gmg_kernel_kind */

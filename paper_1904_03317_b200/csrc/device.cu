@@ -96,6 +96,12 @@ struct DeviceHierarchy {
   bool tensor_apply = true;     // family-patch tensor apply (GMG_APPLY=cell: per-cell in families)
   int gf_slots = 1;             // grandfamilies per block of gfam_tensor_apply (GMG_GF_SLOTS = 1, 2, 3)
   bool overlap = true;          // several ranks: interior patches overlap the ghost import (GMG_OVERLAP=0: off)
+  // small levels 1..slk_ls (+ the coarse solve) run as one persistent kernel (small_vcycle);
+  // 0 = off.  Chosen at setup: one rank, family-patch levels, constant coefficient,
+  // Cholesky coarse solver, every level 1..slk_ls with <= GMG_SLK_FAM families (2048)
+  int slk_ls = 0;
+  int slk_grid = 0;
+  dev::SlkLevel* slk_dev = nullptr;
   cudaStream_t cstream = nullptr;   // the import's side stream
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap = nullptr;
@@ -586,12 +592,29 @@ static bool prolong_fusable(DeviceHierarchy* d, int l) {
   return on && d->lv[l].fuse_pro && d->lv[l].c1.size() > 1;
 }
 
+// V(slk_ls) in one cooperative kernel (kernels.cuh small_vcycle)
+template <typename T>
+static void run_small_levels(DeviceHierarchy* d, cudaStream_t s) {
+  T *D = MG<T>::D(d), *X = MG<T>::X(d), *Tb = MG<T>::T(d), *DV = MG<T>::DV(d);
+  int ls = d->slk_ls, nS0 = d->nS0;
+  const int* cidx = d->coarse_idx;
+  const double* cinv = d->coarse_inv;
+  const dev::SlkLevel* lv = d->slk_dev;
+  void* args[] = {(void*)&lv, (void*)&ls, (void*)&D, (void*)&X, (void*)&Tb, (void*)&DV, (void*)&nS0, (void*)&cidx,
+                  (void*)&cinv};
+  Prof pr(d, s, GMG_K_SMALL, ls, 0.0);
+  void* fn = nullptr;
+  DISPATCH_DK(d->dim, d->k, fn = (void*)dev::small_vcycle<D_, K_, T>);
+  CK(cudaLaunchCooperativeKernel(fn, dim3(d->slk_grid), dim3(dev::SLK_THREADS), args, 0, s));
+  d->launches++;
+}
+
 // The V-cycle on the MG-layout buffers D (defects, copy_to_mg done), X (out).
 template <typename T>
 static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
-  const int L = d->L;
+  const int L = d->L, l0 = d->slk_ls + 1;
   T *D = MG<T>::D(d), *X = MG<T>::X(d), *Tb = MG<T>::T(d), *DV = MG<T>::DV(d);
-  for (int l = L; l >= 1; --l) {
+  for (int l = L; l >= l0; --l) {
     DevLevel& v = d->lv[l];
     T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
     T* gc = D + d->lv[l - 1].off;
@@ -600,8 +623,9 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
     k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
     export_add(d, l - 1, gc, s);
   }
-  coarse(d, D + d->lv[0].off, X + d->lv[0].off, Tb + d->lv[0].off, DV + d->lv[0].off, s);   // 4: coarse solve
-  for (int l = 1; l <= L; ++l) {
+  if (d->slk_ls > 0) run_small_levels<T>(d, s);                                 // V(l_s), coarse solve included
+  else coarse(d, D + d->lv[0].off, X + d->lv[0].off, Tb + d->lv[0].off, DV + d->lv[0].off, s);   // 4: coarse solve
+  for (int l = l0; l <= L; ++l) {
     DevLevel& v = d->lv[l];
     T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
     T* xc = X + d->lv[l - 1].off;
@@ -615,13 +639,47 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
   }
 }
 
+// the per-level parameters of small_vcycle (Chebyshev coefficients change with
+// gmg_set_eigen): uploaded before every capture and eager cycle
+static void upload_slk(DeviceHierarchy* d, cudaStream_t s) {
+  if (d->slk_ls == 0) return;
+  std::vector<dev::SlkLevel> h(d->slk_ls + 1);
+  for (int l = 0; l <= d->slk_ls; ++l) {
+    DevLevel& v = d->lv[l];
+    dev::SlkLevel& q = h[l];
+    std::memset(&q, 0, sizeof q);
+    q.xfer = v.xfer;
+    q.cls = v.cls;
+    q.Dinv = d->mixed ? (const void*)v.Dinv32 : (const void*)v.Dinv;
+    q.n_fam = v.n_fam;
+    q.n_r1 = v.n_r1;
+    q.n_pad = v.n_pad;
+    q.n_owned = v.n_owned;
+    q.off = v.off;
+    q.off_c = l > 0 ? d->lv[l - 1].off : 0;
+    q.scale = v.scale;
+    const int np = d->dim == 3 ? (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1) : (2 * d->k + 1) * (2 * d->k + 1);
+    q.row = np + nn_of(d);
+    q.m = (int)v.c1.size();
+    q.fuse_pro = l > 0 && prolong_fusable(d, l) ? 1 : 0;
+    for (int j = 0; j < q.m && j < 16; ++j) {
+      q.c1[j] = v.c1[j];
+      q.c2[j] = v.c2[j];
+    }
+  }
+  CK(cudaMemcpyAsync(d->slk_dev, h.data(), h.size() * sizeof(dev::SlkLevel), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
 static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s) {
   if (!d->use_graph) {
+    upload_slk(d, s);
     if (d->mixed) vcycle_levels<float>(d, s);
     else vcycle_levels<double>(d, s);
     return;
   }
   if (!d->vgraph) {
+    upload_slk(d, s);
     long long before = d->launches;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal));
@@ -836,7 +894,26 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       const char* e = std::getenv("GMG_GFAM");
       return !(e && e[0] == '0');
     }();
-    const DevicePlan plan = plan_device_order(Tp, gfam);   // device order of the level vectors (rewrites Tp)
+    // small levels in one persistent kernel (small_vcycle): levels 1..ls, see DeviceHierarchy
+    int ls = 0;
+    {
+      const char* e = std::getenv("GMG_SLK");
+      const bool on = !(e && e[0] == '0');
+      i64 fam_max = 2048;
+      if (const char* f = std::getenv("GMG_SLK_FAM")) fam_max = std::atoll(f);
+      bool tensor_ok = true;
+      if (const char* a = std::getenv("GMG_APPLY")) tensor_ok = std::string(a) != "cell";
+      if (on && !comm && prm.coarse_solver == GMG_COARSE_CHOLESKY && tensor_ok && Tp.lv[0].cell_elem.empty())
+        for (int l = 1; l <= Tp.L; ++l) {
+          const LocalLevel& t = Tp.lv[l];
+          if (!(t.n_fam > 0 && t.n_fam <= fam_max && t.cell_elem.empty() && t.cell_coef.empty() && t.fam_coef.empty()))
+            break;
+          ls = l;
+        }
+      if (ls >= Tp.L) ls = Tp.L - 1;   // the finest level stays outside (the copies to/from the MG layout)
+      if (ls < 1) ls = 0;
+    }
+    const DevicePlan plan = plan_device_order(Tp, gfam, ls + 1);   // device order of the level vectors (rewrites Tp)
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
@@ -942,6 +1019,23 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     }
     d->N = off;
     const i64 N = d->N;
+    d->slk_ls = ls;
+    if (ls > 0) {
+      d->slk_dev = d->alloc<dev::SlkLevel>(ls + 1);
+      int per_sm = 0;
+      void* fn = nullptr;
+      const bool f32 = (prm.flags & GMG_MIXED_PRECISION) != 0;
+      if (f32) {
+        DISPATCH_DK(d->dim, d->k, fn = (void*)dev::small_vcycle<D_, K_, float>);
+      } else {
+        DISPATCH_DK(d->dim, d->k, fn = (void*)dev::small_vcycle<D_, K_, double>);
+      }
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::SLK_THREADS, 0));
+      int bps = 2;
+      if (const char* e = std::getenv("GMG_SLK_BPS")) bps = std::max(1, std::atoi(e));
+      d->slk_grid = std::max(1, std::min(per_sm, bps)) * d->sms;
+      if (per_sm < 1) d->slk_ls = 0;
+    }
     for (double** p : {&d->D, &d->X, &d->T, &d->DV, &d->W, &d->Y, &d->cx, &d->cr, &d->cp, &d->cq, &d->cz}) {
       *p = d->alloc<double>(N);
       CK(cudaMemset(*p, 0, N * sizeof(double)));

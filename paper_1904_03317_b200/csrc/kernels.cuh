@@ -24,7 +24,9 @@
 // (for transfers) by this family; v == -1: Dirichlet node; v <= -2: DoF -2-v
 // owned by an earlier family.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace gmg {
 namespace dev {
@@ -356,28 +358,36 @@ constexpr int TA_LOAD_AT = TA_LOAD_AT_DEFAULT;
 enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5,
              TA_CHEB_P01 = 6 };
 
-template <int K, typename T, int TM = TA_APPLY>
-__global__ void __launch_bounds__(32 * TG_WARPS)
-fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
-                 const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
-                 const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
-                 const int* __restrict__ flist = nullptr) {
+// the body of fam_tensor_apply for virtual block vb, shared memory passed in
+// (s0, s1: TensorCfg<K>::NS entries each; cbf: FPB * ((k+1)^3 + 1) for TA_CHEB_P01), so
+// that the persistent small-level kernel (small_vcycle) can run it too
+template <int K, typename T> struct TensorSmem {
+  static constexpr int NS = TensorCfg<K>::FPB * (PatchLayout<K, T>::sab > PatchLayout<K, T>::sn
+                                                     ? PatchLayout<K, T>::sab : PatchLayout<K, T>::sn);
+  static constexpr int NCB = TensorCfg<K>::FPB * ((K + 1) * (K + 1) * (K + 1) + 1);
+};
+template <int K, typename T, int TM>
+__device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* __restrict__ s1, T* __restrict__ cbf,
+                 int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
+                 const T* __restrict__ x, T* __restrict__ y, long n_r1, const T* __restrict__ g,
+                 const T* __restrict__ Dinv, T* __restrict__ dv, T* xw,
+                 double c1_, double c2_, const T* __restrict__ xc, int pf,
+                 const int* __restrict__ flist) {
   constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   constexpr int NP1 = 2 * K + 1, S2 = NP1 * NP1, NL = TensorCfg<K>::NL, FPB = TensorCfg<K>::FPB;
   using LY = PatchLayout<K, T>;
   constexpr int NS = FPB * (LY::sab > LY::sn ? LY::sab : LY::sn);
-  __shared__ T s0[NS], s1[NS];
-  __shared__ T cb[PRO ? FPB : 1][(K + 1) * (K + 1) * (K + 1) + 1];   // PRO: the parents' values
+  (void)NS;
+  constexpr int NCB1 = (K + 1) * (K + 1) * (K + 1) + 1;   // PRO: the parents' values, per slot
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
-  const long fi = (long)blockIdx.x * FPB + slot;
+  const long fi = vb * FPB + slot;
   const bool act = slot < FPB && fi < nfam;
   // flist: the families not covered by grandfamily patches (gfam_tensor_apply)
   const long f = flist ? (act ? (long)__ldg(flist + fi) : 0) : fi;
   if (pf > 0 && !flist) {   // the patch rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
-    const long fb = ((long)blockIdx.x + pf) * FPB;
+    const long fb = (vb + pf) * FPB;
     const long bytes = (long)FPB * row * 4, off = (long)threadIdx.x * 128;
     if (fb < nfam && off < bytes && fb * row * 4 + off < (long)nfam * row * 4)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(xfer + fb * (long)row) + off));
@@ -413,7 +423,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
     if (act) {
       for (int c = lane; c < NC; c += NL) {    // 27 values, 25 lines
         const int ci = __ldg(rp + NPT + c);
-        cb[slot][c] = ci >= 0 ? __ldg(xc + ci) : T(0);
+        cbf[slot * NCB1 + c] = ci >= 0 ? __ldg(xc + ci) : T(0);
       }
     }
     __syncthreads();
@@ -437,7 +447,7 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
         for (int b = 0; b < N; ++b) {
           T sx = T(0);
 #pragma unroll
-          for (int a = 0; a < N; ++a) sx = fma(wx[a], cb[slot][a + N * b + N * N * c], sx);
+          for (int a = 0; a < N; ++a) sx = fma(wx[a], cbf[slot * NCB1 + a + N * b + N * N * c], sx);
           w[c] = fma(wy[b], sx, w[c]);
         }
       }
@@ -588,6 +598,20 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
       }
     }
   }
+}
+
+template <int K, typename T, int TM = TA_APPLY>
+__global__ void __launch_bounds__(32 * TG_WARPS)
+fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
+                 const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
+                 const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
+                 double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
+                 const int* __restrict__ flist = nullptr) {
+  using SM = TensorSmem<K, T>;
+  __shared__ T s0[SM::NS], s1[SM::NS];
+  __shared__ T cb[TM == TA_CHEB_P01 ? SM::NCB : 1];
+  fam_tensor_body<K, T, TM>(blockIdx.x, s0, s1, cb, nfam, xfer, row, fcoef, scale_, x, y, n_r1, g, Dinv, dv, xw, c1_,
+                            c2_, xc, pf, flist);
 }
 
 // ------------------------------------------------------------- grandfamily patches
@@ -930,15 +954,17 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
 // 27 (29) lanes idle.  Lines along x first (gathered into registers), one
 // transposition through shared memory, lines along y; interior patch nodes
 // stored, the others reduced.
+// one warp's work (global warp index gw; s0w, s1w: this warp's FPW x (2k+1)^2 slots)
 template <int K, typename T>
-__global__ void __launch_bounds__(32 * TENSOR_WARPS)
-fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef,
-                   double scale_, const T* __restrict__ x, T* __restrict__ y) {
+__device__ __forceinline__ void fam2d_warp(long gw, T* __restrict__ s0w, T* __restrict__ s1w, int nfam,
+                                           const int* __restrict__ xfer, int row, const double* __restrict__ fcoef,
+                                           double scale_, const T* __restrict__ x, T* __restrict__ y) {
   constexpr int NP1 = 2 * K + 1, NP = NP1 * NP1, FPW = 32 / NP1;
-  __shared__ T s0[TENSOR_WARPS][FPW][NP], s1[TENSOR_WARPS][FPW][NP];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int j = lane / NP1, line = lane % NP1;
-  const long f = ((long)blockIdx.x * TENSOR_WARPS + w) * FPW + j;
+  const long f = gw * FPW + j;
+  T* const s0j = s0w + (j < FPW ? j : 0) * NP;
+  T* const s1j = s1w + (j < FPW ? j : 0) * NP;
   const bool active = j < FPW && f < nfam;
   const int* rp = xfer + (active ? f : 0) * (long)row;
   const T scale = (T)(active && fcoef ? scale_ * __ldg(fcoef + f) : scale_);
@@ -958,8 +984,8 @@ fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double
         if (Kt<K>(xx, q) != 0.0) a = fma((T)Kt<K>(xx, q), u[q], a);
         if (Mt<K>(xx, q) != 0.0) bb = fma((T)Mt<K>(xx, q), u[q], bb);
       }
-      s0[w][j][b + xx] = a;
-      s1[w][j][b + xx] = bb;
+      s0j[b + xx] = a;
+      s1j[b + xx] = bb;
     }
   }
   __syncwarp();
@@ -967,8 +993,8 @@ fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double
     T a[NP1], bb[NP1];
 #pragma unroll
     for (int q = 0; q < NP1; ++q) {
-      a[q] = s0[w][j][line + q * NP1];
-      bb[q] = s1[w][j][line + q * NP1];
+      a[q] = s0j[line + q * NP1];
+      bb[q] = s1j[line + q * NP1];
     }
 #pragma unroll
     for (int yy = 0; yy < NP1; ++yy) {
@@ -984,6 +1010,17 @@ fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double
       else atomicAdd(y + i, scale * o);
     }
   }
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(32 * TENSOR_WARPS)
+fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef,
+                   double scale_, const T* __restrict__ x, T* __restrict__ y) {
+  constexpr int NP1 = 2 * K + 1, NP = NP1 * NP1, FPW = 32 / NP1;
+  __shared__ T s0[TENSOR_WARPS][FPW][NP], s1[TENSOR_WARPS][FPW][NP];
+  const int w = threadIdx.x >> 5;
+  fam2d_warp<K, T>((long)blockIdx.x * TENSOR_WARPS + w, &s0[w][0][0], &s1[w][0][0], nfam, xfer, row, fcoef, scale_, x,
+                   y);
 }
 
 // cell_dofs is SoA: dof of local node b of cell c at cell_dofs[b * ldc + c]
@@ -1111,6 +1148,22 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
 
 // The Chebyshev step on [a, n) only (the rows not finished by the fused apply):
 // scalar form of cheb_step<T, READ_T = 1, ..., X_ZERO = 0>.
+// one row of cheb_range (used by the persistent small-level kernel)
+template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X, bool PRO>
+__device__ __forceinline__ void cheb_row(long i, const T* __restrict__ g, const T* __restrict__ Dinv, T* __restrict__ t,
+                                         T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_, long n_own) {
+  const T G = g[i], Tv = t[i], Di = Dinv[i];
+  T X = x[i];
+  if (PRO && i < n_own) X = X + dv[i];
+  T V = 0;
+  if (READ_DV) V = DV_IS_X ? X : dv[i];
+  t[i] = Tv - Tv;
+  T dd = (T)c2_ * Di * (G - Tv);
+  if (READ_DV) dd = fma((T)c1_, V, dd);
+  if (WRITE_DV) dv[i] = dd;
+  x[i] = X + dd;
+}
+
 template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false, bool PRO = false>
 __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __restrict__ g,
                                                      const T* __restrict__ Dinv, T* __restrict__ t,
@@ -1176,25 +1229,25 @@ __device__ __forceinline__ void row_fetch(const int* __restrict__ xfer, const in
 }
 
 template <int D, int K, int MODE, typename T>
-__global__ void __launch_bounds__(32 * XFER_WARPS)
-warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
+__device__ __forceinline__ void warp_prolongate_body(int bid, int nblocks, int* __restrict__ srow, T* __restrict__ b0, T* __restrict__ b1, int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
                 const unsigned char* __restrict__ cls_fine, const T* __restrict__ xc, T* __restrict__ xf) {
   using S = XferShape<D, K>;
   constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
-  __shared__ int srow[XFER_WARPS][S::ROW];
-  __shared__ T b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
-  if (gw >= nfam) return;
+  const int gw = bid * XFER_WARPS + w, GW = nblocks * XFER_WARPS;
+  int* const srw = srow + w * S::ROW;
+  T* const b0w = b0 + w * NP;
+  T* const b1w = b1 + w * NP;
+  if (gw >= nfam) return;   // (no block-wide barrier below)
   int nxt[S::NR];
   row_fetch<D, K>(xfer, fam_list, gw, lane, nxt);
   for (int tt = gw; tt < nfam; tt += GW) {
 #pragma unroll
     for (int q = 0; q < S::NR; ++q)
-      if (lane + 32 * q < S::ROW) srow[w][lane + 32 * q] = nxt[q];
+      if (lane + 32 * q < S::ROW) srw[lane + 32 * q] = nxt[q];
     __syncwarp();
     if (tt + GW < nfam) row_fetch<D, K>(xfer, fam_list, tt + GW, lane, nxt);
-    const int* rw = srow[w];
+    const int* rw = srw;
     // one memory round trip per family: the parent's values and the owned fine
     // values (read-modify-write below) are requested together, before the passes
     constexpr int NIT = (NP + 31) / 32;
@@ -1212,23 +1265,23 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
     }
     if (lane < NC) {
       const int ci = rw[NP + lane];
-      b0[w][lane] = ci >= 0 ? __ldg(xc + ci) : T(0);
+      b0w[lane] = ci >= 0 ? __ldg(xc + ci) : T(0);
     }
     __syncwarp();
     T* fine;
     if constexpr (D == 3) {
       // x: c[jz][jy][jx] -> b1[jz][jy][ax];  y: -> b0[jz][ay][ax];  z: -> b1[az][ay][ax]
-      xfer_pass<K, true, N * N, 1>(lane, b0[w], b1[w], N, 1, 0, NP1, 1, 0);
+      xfer_pass<K, true, N * N, 1>(lane, b0w, b1w, N, 1, 0, NP1, 1, 0);
       __syncwarp();
-      xfer_pass<K, true, N, NP1>(lane, b1[w], b0[w], N * NP1, NP1, 1, NP1 * NP1, NP1, 1);
+      xfer_pass<K, true, N, NP1>(lane, b1w, b0w, N * NP1, NP1, 1, NP1 * NP1, NP1, 1);
       __syncwarp();
-      xfer_pass<K, true, 1, NP1 * NP1>(lane, b0[w], b1[w], 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
-      fine = b1[w];
+      xfer_pass<K, true, 1, NP1 * NP1>(lane, b0w, b1w, 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
+      fine = b1w;
     } else {
-      xfer_pass<K, true, N, 1>(lane, b0[w], b1[w], N, 1, 0, NP1, 1, 0);
+      xfer_pass<K, true, N, 1>(lane, b0w, b1w, N, 1, 0, NP1, 1, 0);
       __syncwarp();
-      xfer_pass<K, true, 1, NP1>(lane, b1[w], b0[w], 0, NP1, 1, 0, NP1, 1);
-      fine = b0[w];
+      xfer_pass<K, true, 1, NP1>(lane, b1w, b0w, 0, NP1, 1, 0, NP1, 1);
+      fine = b0w;
     }
     __syncwarp();
 #pragma unroll
@@ -1247,25 +1300,35 @@ warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restric
 
 template <int D, int K, int MODE, typename T>
 __global__ void __launch_bounds__(32 * XFER_WARPS)
-warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
+warp_prolongate(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
+                const unsigned char* __restrict__ cls_fine, const T* __restrict__ xc, T* __restrict__ xf) {
+  using S = XferShape<D, K>;
+  __shared__ int srow[XFER_WARPS * S::ROW];
+  __shared__ T b0[XFER_WARPS * S::NP], b1[XFER_WARPS * S::NP];
+  warp_prolongate_body<D, K, MODE, T>(blockIdx.x, gridDim.x, srow, b0, b1, nfam, fam_list, xfer, cls_fine, xc, xf);
+}
+
+template <int D, int K, int MODE, typename T>
+__device__ __forceinline__ void warp_restrict_body(int bid, int nblocks, int* __restrict__ srow, T* __restrict__ b0, T* __restrict__ b1, int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
               const unsigned char* __restrict__ cls_fine, const T* __restrict__ v, T* __restrict__ t,
               T* __restrict__ dc) {
   using S = XferShape<D, K>;
   constexpr int N = S::N, NP1 = S::NP1, NC = S::NC, NP = S::NP;
-  __shared__ int srow[XFER_WARPS][S::ROW];
-  __shared__ T b0[XFER_WARPS][NP], b1[XFER_WARPS][NP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gw = blockIdx.x * XFER_WARPS + w, GW = gridDim.x * XFER_WARPS;
-  if (gw >= nfam) return;
+  const int gw = bid * XFER_WARPS + w, GW = nblocks * XFER_WARPS;
+  int* const srw = srow + w * S::ROW;
+  T* const b0w = b0 + w * NP;
+  T* const b1w = b1 + w * NP;
+  if (gw >= nfam) return;   // (no block-wide barrier below)
   int nxt[S::NR];
   row_fetch<D, K>(xfer, fam_list, gw, lane, nxt);
   for (int tt = gw; tt < nfam; tt += GW) {
 #pragma unroll
     for (int q = 0; q < S::NR; ++q)
-      if (lane + 32 * q < S::ROW) srow[w][lane + 32 * q] = nxt[q];
+      if (lane + 32 * q < S::ROW) srw[lane + 32 * q] = nxt[q];
     __syncwarp();
     if (tt + GW < nfam) row_fetch<D, K>(xfer, fam_list, tt + GW, lane, nxt);
-    const int* rw = srow[w];
+    const int* rw = srw;
     // residual on the family's owned fine nodes (0 elsewhere); all loads first
     constexpr int NIT = (NP + 31) / 32;
     int ii[NIT];
@@ -1296,23 +1359,23 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
           r = va[q];
         }
       }
-      if (a < NP) b0[w][a] = r;
+      if (a < NP) b0w[a] = r;
     }
     __syncwarp();
     T* coarse;
     if constexpr (D == 3) {
       // z: r[az][ay][ax] -> b1[jz][ay][ax];  y: -> b0[jz][jy][ax];  x: -> b1[jz][jy][jx]
-      xfer_pass<K, false, 1, NP1 * NP1>(lane, b0[w], b1[w], 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
+      xfer_pass<K, false, 1, NP1 * NP1>(lane, b0w, b1w, 0, NP1 * NP1, 1, 0, NP1 * NP1, 1);
       __syncwarp();
-      xfer_pass<K, false, N, NP1>(lane, b1[w], b0[w], NP1 * NP1, NP1, 1, N * NP1, NP1, 1);
+      xfer_pass<K, false, N, NP1>(lane, b1w, b0w, NP1 * NP1, NP1, 1, N * NP1, NP1, 1);
       __syncwarp();
-      xfer_pass<K, false, N * N, 1>(lane, b0[w], b1[w], NP1, 1, 0, N, 1, 0);
-      coarse = b1[w];
+      xfer_pass<K, false, N * N, 1>(lane, b0w, b1w, NP1, 1, 0, N, 1, 0);
+      coarse = b1w;
     } else {
-      xfer_pass<K, false, 1, NP1>(lane, b0[w], b1[w], 0, NP1, 1, 0, NP1, 1);
+      xfer_pass<K, false, 1, NP1>(lane, b0w, b1w, 0, NP1, 1, 0, NP1, 1);
       __syncwarp();
-      xfer_pass<K, false, N, 1>(lane, b1[w], b0[w], NP1, 1, 0, N, 1, 0);
-      coarse = b0[w];
+      xfer_pass<K, false, N, 1>(lane, b1w, b0w, NP1, 1, 0, N, 1, 0);
+      coarse = b0w;
     }
     __syncwarp();
     if (lane < NC) {
@@ -1320,6 +1383,188 @@ warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict_
       if (ci >= 0) atomicAdd(dc + ci, coarse[lane]);
     }
     __syncwarp();
+  }
+}
+
+template <int D, int K, int MODE, typename T>
+__global__ void __launch_bounds__(32 * XFER_WARPS)
+warp_restrict(int nfam, const int* __restrict__ fam_list, const int* __restrict__ xfer,
+              const unsigned char* __restrict__ cls_fine, const T* __restrict__ v, T* __restrict__ t,
+              T* __restrict__ dc) {
+  using S = XferShape<D, K>;
+  __shared__ int srow[XFER_WARPS * S::ROW];
+  __shared__ T b0[XFER_WARPS * S::NP], b1[XFER_WARPS * S::NP];
+  warp_restrict_body<D, K, MODE, T>(blockIdx.x, gridDim.x, srow, b0, b1, nfam, fam_list, xfer, cls_fine, v, t, dc);
+}
+
+
+// ------------------------------------------------------------- small levels in one persistent kernel
+// small_vcycle: the whole V(l_s) -- pre-smoothing, residual, restriction on
+// levels l_s .. 1, the coarse solve, prolongation and post-smoothing on 1 .. l_s
+// -- as ONE cooperative kernel whose phases are separated by grid-wide barriers,
+// instead of ~17 launches per level of 2-5 us each (the small levels are launch-
+// latency bound).  One rank; levels run by the family-patch kernels (3D tensor
+// or 2D), constant coefficient, Cholesky coarse solver.  Every phase is the same
+// device body the separate kernels run (fam_tensor_body, fam2d_warp,
+// warp_restrict_body, warp_prolongate_body, cheb_row), in the same order as
+// vcycle_levels / smooth (device.cu), so results match the launch-per-step cycle.
+struct SlkLevel {
+  const int* xfer;
+  const unsigned char* cls;
+  const void* Dinv;        // T*
+  long n_fam, n_r1, n_pad, n_owned, off, off_c;
+  double scale;
+  int row, m, fuse_pro, pad_;
+  double c1[16], c2[16];
+};
+constexpr int SLK_THREADS = 128;
+
+template <int D, int K, typename T>
+struct SlkSmem {
+  using XS = XferShape<D, K>;
+  static constexpr int NP1 = 2 * K + 1, NP2 = NP1 * NP1, FPW2 = 32 / NP1;
+  static constexpr size_t tensor = D == 3 ? sizeof(T) * (2 * TensorSmem<K, T>::NS + TensorSmem<K, T>::NCB) : 0;
+  static constexpr size_t fam2d = D == 2 ? sizeof(T) * 2 * 4 * FPW2 * NP2 : 0;
+  static constexpr size_t xfer = 4 * sizeof(int) * XS::ROW + 2 * 4 * sizeof(T) * XS::NP + 16;
+  static constexpr size_t bytes = tensor > fam2d ? (tensor > xfer ? tensor : xfer) : (fam2d > xfer ? fam2d : xfer);
+};
+
+// Phase functions of small_vcycle: __noinline__ so that each keeps the register
+// budget of its own body (inlining all of them into one kernel exceeds 255
+// registers and spills).
+template <int D, int K, typename T, int TM>
+__device__ __noinline__ void slk_tensor(const SlkLevel* v, unsigned char* smem, T* Dm, T* Xm, T* Tm, T* DVm,
+                                        const T* xc, double c1, double c2) {
+  T *g = Dm + v->off, *x = Xm + v->off, *t = Tm + v->off, *dv = DVm + v->off;
+  if constexpr (D == 3) {
+    using TS = TensorSmem<K, T>;
+    T* s0 = reinterpret_cast<T*>(smem);
+    T* s1 = s0 + TS::NS;
+    T* cb = s1 + TS::NS;
+    const long nvb = (v->n_fam + TensorCfg<K>::FPB - 1) / TensorCfg<K>::FPB;
+    for (long vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+      fam_tensor_body<K, T, TM>(vb, s0, s1, cb, (int)v->n_fam, v->xfer, v->row, nullptr, v->scale, x, t, v->n_r1, g,
+                                (const T*)v->Dinv, dv, x, c1, c2, xc, 0, nullptr);
+  } else {
+    constexpr int NP1 = 2 * K + 1, NP = NP1 * NP1, FPW = 32 / NP1;
+    const int w = threadIdx.x >> 5;
+    T* s0 = reinterpret_cast<T*>(smem) + w * FPW * NP;
+    T* s1 = reinterpret_cast<T*>(smem) + (4 + w) * FPW * NP;
+    const long nw = (v->n_fam + FPW - 1) / FPW;
+    for (long gw = (long)blockIdx.x * 4 + w; gw < nw; gw += (long)gridDim.x * 4)
+      fam2d_warp<K, T>(gw, s0, s1, (int)v->n_fam, v->xfer, v->row, nullptr, v->scale, x, t);
+  }
+}
+
+template <int D, typename T, bool RDV, bool WDV, bool DVX, bool PRO>
+__device__ __noinline__ void slk_finish(const SlkLevel* v, T* Dm, T* Xm, T* Tm, T* DVm, double c1, double c2) {
+  const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x, gstride = (long)gridDim.x * blockDim.x;
+  const long a = D == 3 ? v->n_r1 : 0;
+  for (long i = a + gtid; i < v->n_pad; i += gstride)
+    cheb_row<T, RDV, WDV, DVX, PRO>(i, Dm + v->off, (const T*)v->Dinv, Tm + v->off, DVm + v->off, Xm + v->off, c1, c2,
+                                    v->n_owned);
+}
+
+template <int D, int K, typename T, bool RESTRICT>
+__device__ __noinline__ void slk_transfer(const SlkLevel* v, unsigned char* smem, T* Dm, T* Xm, T* Tm) {
+  using XS = XferShape<D, K>;
+  int* srow = reinterpret_cast<int*>(smem);
+  T* b0 = reinterpret_cast<T*>(smem + ((4 * sizeof(int) * XS::ROW + 15) / 16) * 16);
+  T* b1 = b0 + 4 * XS::NP;
+  if (RESTRICT)
+    warp_restrict_body<D, K, RES_VCYCLE, T>(blockIdx.x, gridDim.x, srow, b0, b1, (int)v->n_fam, nullptr, v->xfer, v->cls,
+                                            Dm + v->off, Tm + v->off, Dm + v->off_c);
+  else
+    warp_prolongate_body<D, K, XFER_ADD, T>(blockIdx.x, gridDim.x, srow, b0, b1, (int)v->n_fam, nullptr, v->xfer,
+                                            v->cls, Xm + v->off_c, Xm + v->off);
+}
+
+template <int D, int K, typename T>
+__global__ void __launch_bounds__(SLK_THREADS, 4)
+small_vcycle(const SlkLevel* __restrict__ lvs, int ls, T* __restrict__ Dm, T* __restrict__ Xm, T* __restrict__ Tm,
+             T* __restrict__ DVm, int nS0, const int* __restrict__ coarse_idx, const double* __restrict__ coarse_inv) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using SM = SlkSmem<D, K, T>;
+  __shared__ __align__(16) unsigned char smem[SM::bytes];
+  const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x, gstride = (long)gridDim.x * blockDim.x;
+  // one Chebyshev step: t = K x with the fused epilogue (3D) / t = K x (2D), then
+  // the rows the epilogue did not finish
+  auto step = [&](const SlkLevel* v, auto tm, auto rdv, auto wdv, auto dvx, auto pro, const T* xc, double c1,
+                  double c2) {
+    constexpr int TM = decltype(tm)::value;
+    if constexpr (D == 3) slk_tensor<D, K, T, TM>(v, smem, Dm, Xm, Tm, DVm, xc, c1, c2);
+    else slk_tensor<D, K, T, TA_APPLY>(v, smem, Dm, Xm, Tm, DVm, nullptr, 0.0, 0.0);
+    grid.sync();
+    slk_finish<D, T, decltype(rdv)::value, decltype(wdv)::value, decltype(dvx)::value, decltype(pro)::value>(
+        v, Dm, Xm, Tm, DVm, c1, c2);
+    grid.sync();
+  };
+  using F = std::false_type;
+  using Tr = std::true_type;
+  using X1 = std::integral_constant<int, TA_CHEB_X1>;
+  using C11 = std::integral_constant<int, TA_CHEB_11>;
+  using C10 = std::integral_constant<int, TA_CHEB_10>;
+  using C01 = std::integral_constant<int, TA_CHEB_01>;
+  using C00 = std::integral_constant<int, TA_CHEB_00>;
+  using P01 = std::integral_constant<int, TA_CHEB_P01>;
+  auto tail_steps = [&](const SlkLevel* v, int j0) {
+    for (int j = j0; j < v->m; ++j) {
+      if (j == v->m - 1) step(v, C10{}, Tr{}, F{}, F{}, F{}, nullptr, v->c1[j], v->c2[j]);
+      else step(v, C11{}, Tr{}, Tr{}, F{}, F{}, nullptr, v->c1[j], v->c2[j]);
+    }
+  };
+  // ---------------- down
+  for (int l = ls; l >= 1; --l) {
+    const SlkLevel* v = lvs + l;
+    T *g = Dm + v->off, *x = Xm + v->off;
+    const T* Dv = (const T*)v->Dinv;
+    if (v->m > 1) {
+      // x_1 = c2_0 D^-1 g (cheb_step<..., X_ZERO>), then the fused steps with dv_0 = x_1
+      for (long i = gtid; i < v->n_pad; i += gstride) x[i] = (T)v->c2[0] * Dv[i] * g[i];
+      grid.sync();
+      step(v, X1{}, Tr{}, Tr{}, Tr{}, F{}, nullptr, v->c1[1], v->c2[1]);
+      tail_steps(v, 2);
+    } else {
+      for (long i = gtid; i < v->n_pad; i += gstride) {
+        const T dd = (T)v->c2[0] * Dv[i] * g[i];
+        DVm[v->off + i] = dd;
+        x[i] = dd;
+      }
+      grid.sync();
+    }
+    slk_tensor<D, K, T, TA_APPLY>(v, smem, Dm, Xm, Tm, DVm, nullptr, 0.0, 0.0);   // residual t = K x
+    grid.sync();
+    slk_transfer<D, K, T, true>(v, smem, Dm, Xm, Tm);                             // d_{l-1} += P^T (d - t)
+    grid.sync();
+  }
+  // ---------------- coarse solve (dense inverse of A_0^S)
+  if (blockIdx.x == 0 && nS0 > 0) {
+    const T* d0 = Dm + lvs[0].off;
+    T* x0 = Xm + lvs[0].off;
+    for (int i = threadIdx.x; i < nS0; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < nS0; ++j) s = fma(coarse_inv[(long)i * nS0 + j], (double)d0[coarse_idx[j]], s);
+      x0[coarse_idx[i]] = (T)s;
+    }
+  }
+  grid.sync();
+  // ---------------- up
+  for (int l = 1; l <= ls; ++l) {
+    const SlkLevel* v = lvs + l;
+    if (D == 3 && v->fuse_pro && v->m > 1) {
+      step(v, P01{}, F{}, Tr{}, F{}, Tr{}, Xm + v->off_c, 0.0, v->c2[0]);
+      tail_steps(v, 1);
+    } else {
+      slk_transfer<D, K, T, false>(v, smem, Dm, Xm, Tm);                          // x_l += P x_{l-1}
+      grid.sync();
+      if (v->m == 1) {
+        step(v, C00{}, F{}, F{}, F{}, F{}, nullptr, 0.0, v->c2[0]);
+      } else {
+        step(v, C01{}, F{}, Tr{}, F{}, F{}, nullptr, 0.0, v->c2[0]);
+        tail_steps(v, 1);
+      }
+    }
   }
 }
 

@@ -19,7 +19,7 @@ static inline void gf_pos(int k, int X, int Y, int Z, int& j, int& a) {
   a = (X - 2 * k * cx) + NP1 * (Y - 2 * k * cy) + NP1 * NP1 * (Z - 2 * k * cz);
 }
 
-DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
+DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level) {
   const int d = T.dim, k = T.k, L = T.L;
   const int NP1 = 2 * k + 1;
   int nn = 1, np = 1;
@@ -65,7 +65,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies) {
       // grandfamily patches in use: Q2, one coefficient for all 8 families
       std::vector<i32>& fg = fam_gf[l];
       fg.assign(v.n_fam, -1);
-      if (grandfamilies && k == 2)
+      if (grandfamilies && k == 2 && l >= gf_min_level)
         for (i32 f0 : v.gf_first) {
           bool ok = true;
           if (!v.fam_coef.empty())

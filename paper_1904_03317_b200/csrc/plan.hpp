@@ -47,6 +47,6 @@ struct DevicePlan {
 
 // Computes the device order from T's tables and rewrites T in place (every
 // local DoF index of every table is mapped through perm).
-DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies = true);
+DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies = true, int gf_min_level = 2);
 
 }  // namespace gmg
