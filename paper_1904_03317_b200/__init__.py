@@ -103,7 +103,8 @@ class Info(C.Structure):
                 ("level_families", C.c_int64 * MAX_LEVELS), ("level_S", C.c_int64 * MAX_LEVELS),
                 ("level_E", C.c_int64 * MAX_LEVELS), ("level_B", C.c_int64 * MAX_LEVELS),
                 ("level_leaf_cells", C.c_int64 * MAX_LEVELS), ("mg_vector_len", C.c_int64),
-                ("level_r1", C.c_int64 * MAX_LEVELS), ("level_gf", C.c_int64 * MAX_LEVELS)]
+                ("level_r1", C.c_int64 * MAX_LEVELS), ("level_gf", C.c_int64 * MAX_LEVELS),
+                ("small_levels", C.c_int64)]
 
 
 class KernelStat(C.Structure):

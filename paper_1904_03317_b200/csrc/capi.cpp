@@ -418,6 +418,7 @@ gmg_status gmg_hierarchy_info(const gmg_hierarchy* h, gmg_info* o) {
       mg += (h->local.lv[l].n_local() + 511) / 512 * 512;
     }
     o->mg_vector_len = h->dev ? gmg::device_mg_len(h->dev) : mg;
+    o->small_levels = h->dev ? gmg::device_small_levels(h->dev) : 0;
   });
 }
 

@@ -1193,6 +1193,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
 }
 
 long long device_mg_len(const DeviceHierarchy* d) { return d ? (long long)d->N : 0; }
+long long device_small_levels(const DeviceHierarchy* d) { return d ? (long long)d->slk_ls : 0; }
 
 void comm_allreduce_host(Comm* comm, std::vector<double>& v) {
   if (!comm || v.empty()) return;

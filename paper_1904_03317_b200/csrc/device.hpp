@@ -32,6 +32,7 @@ void device_coarse_chebyshev(const DeviceHierarchy* d, double* lo, double* hi, i
 void device_set_eigen(DeviceHierarchy* d, int level, double lam);
 long long device_launches(const DeviceHierarchy* d);
 long long device_mg_len(const DeviceHierarchy* d);
+long long device_small_levels(const DeviceHierarchy* d);
 // sum of v over the ranks of comm (host vector in, host vector out; setup-time)
 void comm_allreduce_host(Comm* comm, std::vector<double>& v);
 int device_profile_vcycle(DeviceHierarchy* d, const double* b, double* x, int n_rep, gmg_kernel_stat* out,

@@ -61,7 +61,7 @@ def test_r1_is_rows_touched_by_one_family(name, passes, over):
         n = info["level_dofs"][l]
         tensor = info["dim"] == 3 and not (coef is not None and l <= 2)   # R15: levels 0-2 carry per-cell data
         keys = h.part.level_cells(l)[0]
-        use_gf = tensor and info["k"] == 2 and l >= 2 and (coef is None or l >= 4)
+        use_gf = tensor and info["k"] == 2 and l >= 2 and (coef is None or l >= 4) and l > info["small_levels"]
         pid, ngf = patches(keys, nch, use_gf)
         assert info["level_gf"][l] == ngf, (l, info["level_gf"][l], ngf)
         expect = int((touch_counts(h.cell_dofs(l), n, nch, pid) == 1).sum()) if tensor and n else 0
