@@ -307,8 +307,9 @@ typedef struct {
   int64_t level_gf[GMG_MAX_LEVELS];
   /* levels 1..small_levels (and the coarse solve) run as one persistent kernel
    * (small_vcycle; 0 = none): one rank, family-patch levels with <= GMG_SLK_FAM
-   * (2048) families each, constant coefficient, Cholesky coarse solver;
-   * GMG_SLK=0 turns it off.  Grandfamily patches are not formed on these levels. */
+   * (2048) families each, constant coefficient, Cholesky coarse solver; opt-in
+   * with GMG_SLK=1 (measured slower than the graph of per-step kernels).
+   * Grandfamily patches are not formed on these levels. */
   int64_t small_levels;
 } gmg_info;
 gmg_status gmg_hierarchy_info(const gmg_hierarchy *h, gmg_info *out);

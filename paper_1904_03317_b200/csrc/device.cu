@@ -897,8 +897,10 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
     // small levels in one persistent kernel (small_vcycle): levels 1..ls, see DeviceHierarchy
     int ls = 0;
     {
+      // off by default: measured slower than the graph-launched per-step kernels
+      // (grid barriers cost more than kernel boundaries inside a CUDA graph)
       const char* e = std::getenv("GMG_SLK");
-      const bool on = !(e && e[0] == '0');
+      const bool on = e && e[0] == '1';
       i64 fam_max = 2048;
       if (const char* f = std::getenv("GMG_SLK_FAM")) fam_max = std::atoll(f);
       bool tensor_ok = true;
