@@ -351,7 +351,7 @@ gmg_status gmg_setup(const gmg_forest* f, const gmg_partitioning* p, const gmg_p
       // the device holds its own copies: drop the host tables (large for rank-local
       // runs of 125M DoFs per rank); keys, plans and counts stay for the exports
       for (auto& v : h->local.lv) {
-        for (auto* t : {&v.cell_dofs, &v.fam_dofs, &v.xfer, &v.leaf_cells, &v.edge_fams, &v.gf_first}) {
+        for (auto* t : {&v.cell_dofs, &v.xfer, &v.leaf_cells, &v.edge_fams, &v.gf_first}) {
           t->clear();
           t->shrink_to_fit();
         }
@@ -536,6 +536,7 @@ gmg_status gmg_export_local_tables(const gmg_hierarchy* h, int level, int64_t* n
     need_level(h, level);
     GMG_REQUIRE(h->dev == nullptr, GMG_E_STATE, "local tables are exported from GMG_HOST_ONLY hierarchies "
                                                 "(device setup reorders them)");
+    if (h->local.lv[level].eig_v.empty()) gmg::eig_start_from_keys(const_cast<gmg_hierarchy*>(h)->local);
     const auto& v = h->local.lv[level];
     if (n_cells) *n_cells = v.n_cells;
     if (n_fam) *n_fam = v.n_fam;

@@ -915,6 +915,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       if (ls >= Tp.L) ls = Tp.L - 1;   // the finest level stays outside (the copies to/from the MG layout)
       if (ls < 1) ls = 0;
     }
+    eig_start_from_keys(Tp);                                        // rank-local builds: R10b from the keys
     const DevicePlan plan = plan_device_order(Tp, gfam, ls + 1);   // device order of the level vectors (rewrites Tp)
     if (prm.device >= 0) CK(cudaSetDevice(prm.device));
     int dev_id = 0;
@@ -972,10 +973,11 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       if (!d->tensor_apply || (!t.cell_coef.empty() && t.fam_coef.empty())) {
         // cell-form family apply (config-4 level 2, or GMG_APPLY=cell): patch table
         // AoS (host) -> SoA [(2k+1)^d][n_fam] (device)
-        const size_t np = t.n_fam ? t.fam_dofs.size() / (size_t)t.n_fam : 0;
-        std::vector<int> fs(t.fam_dofs.size());
+        const size_t np = Tp.dim == 3 ? (2 * Tp.k + 1) * (2 * Tp.k + 1) * (2 * Tp.k + 1) : (2 * Tp.k + 1) * (2 * Tp.k + 1);
+        const size_t xr = np + nn;
+        std::vector<int> fs(np * t.n_fam);
         for (size_t f = 0; f < (size_t)t.n_fam; ++f)
-          for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.fam_dofs[f * np + a];
+          for (size_t a = 0; a < np; ++a) fs[a * t.n_fam + f] = t.xfer[f * xr + a];
         v.fam_dofs = d->upload(fs);
       }
       v.leaf_cells = d->upload(t.leaf_cells);

@@ -127,8 +127,10 @@ struct LocalLevel {
   std::vector<i32> recv_idx;               // local ghost indices, grouped by peer
   i64 n_cells = 0, n_fam = 0;
   std::vector<i32> cell_dofs;              // [n_cells][(k+1)^d] local index or -1
-  std::vector<i32> fam_dofs;               // [n_fam][(2k+1)^d] local, transfer-owner encoding
-  std::vector<i32> xfer;                   // [n_fam][(2k+1)^d + (k+1)^d] fine | parent (level l-1 local)
+  // [n_fam][(2k+1)^d + (k+1)^d]: the family patch in local indices with the transfer-owner
+  // encoding (v >= 0 this family owns the node for transfers, -2-v owned by another
+  // family, -1 Dirichlet), then the parent's (k+1)^d level-(l-1) local DoFs
+  std::vector<i32> xfer;
   std::vector<i32> leaf_cells, edge_fams;
   // complete grandfamilies (3D): local family index of the first of 8 consecutive
   // local families whose parents are the 8 children of one level-(l-2) cell
@@ -154,14 +156,8 @@ struct LocalTopo {
   std::vector<LocalLevel> lv;
   i64 n_leaf_owned = 0, leaf_first = 0, n_leaf_global = 0;
   std::vector<int8_t> leaf_level;          // per owned leaf DoF
-  std::vector<i64> leaf_local;             // local index at its level
-  std::vector<u64> leaf_key;               // rank-local builds: finest-lattice key per owned leaf DoF
-  struct LeafRec {
-    u64 key;
-    int8_t level;
-    i64 local;
-  };
-  std::vector<LeafRec> leaf_tmp;
+  std::vector<i32> leaf_local;             // local index at its level
+  std::vector<u64> leaf_key;               // finest-lattice key per owned leaf DoF
 };
 
 // eig_key: eigen start vector -5.5 + (level-lattice Morton key mod 12) on the
@@ -179,6 +175,9 @@ struct LocalCounts {
 };
 LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank, bool eig_key,
                             LocalCounts* counts);
+// the key-based eigen start vector (R10b) of every level whose eig_v is empty (rank-local
+// builds store none); needs the local order (before the device reordering)
+void eig_start_from_keys(LocalTopo& T);
 
 // Piecewise-constant coefficient per level-2 cell (config 4): coef2[i] belongs to
 // the i-th cell of C_2 in SFC order.  Fills the coefficient fields of every level.

@@ -195,7 +195,6 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     }
     if (l > 0) {
       const int row = np + nn;
-      v.fam_dofs.resize((size_t)v.n_fam * np);
       v.xfer.resize((size_t)v.n_fam * row);
       const LevelTopo& tc = T.lv[l - 1];
       for (i64 lf = 0; lf < v.n_fam; ++lf) {
@@ -213,7 +212,6 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
               if (t.dof_cls[g] == CLS_E) edge = true;
             }
           }
-          v.fam_dofs[(size_t)lf * np + a] = enc;
           v.xfer[(size_t)lf * row + a] = enc;
         }
         const i64 pc = t.fam_parent[fi];
@@ -231,7 +229,7 @@ LocalTopo make_local(const Forest& f, const Partition& p, const Topology& T, int
     const int l = T.leaf_lambda[g];
     Lt.leaf_level.push_back((int8_t)l);
     Lt.leaf_key.push_back(T.leaf_key[g]);
-    Lt.leaf_local.push_back(T.leaf_level_index[g] - Lt.lv[l].first_owned);
+    Lt.leaf_local.push_back((i32)(T.leaf_level_index[g] - Lt.lv[l].first_owned));
     GMG_REQUIRE(Lt.leaf_local.back() >= 0 && Lt.leaf_local.back() < Lt.lv[l].n_owned, GMG_E_STATE,
                 "leaf DoF not owned at its lambda level");
   }

@@ -24,6 +24,7 @@
 // those computing the next-finer family of a containing refined cell) are all
 // decided inside the halo.  Construction as topology.cpp: occurrences (key,
 // halo family, patch position) radix-sorted by key, one pass over equal keys.
+#include <cstdlib>
 #include <numeric>
 
 #include "patch.hpp"
@@ -71,6 +72,22 @@ struct LevelKeep {
 };
 
 }  // namespace
+
+void eig_start_from_keys(LocalTopo& T) {
+  // R10b: -5.5 + (Morton key of the node on the level-l lattice mod 12) on owned S DoFs
+  for (int l = 0; l <= T.L; ++l) {
+    LocalLevel& v = T.lv[l];
+    if (!v.eig_v.empty()) continue;
+    v.eig_v.assign(v.n_local(), 0.0);
+    for (i64 i = 0; i < v.n_owned; ++i) {
+      if (v.cls[i] != CLS_S) continue;
+      const Vec3 X = unmorton(T.dim, v.owned_key[i]);
+      Vec3 Y{0, 0, 0};
+      for (int j = 0; j < T.dim; ++j) Y[j] = X[j] >> (T.L - l);
+      v.eig_v[i] = -5.5 + (double)(morton(T.dim, Y) % 12);
+    }
+  }
+}
 
 LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank, bool eig_key,
                             LocalCounts* counts) {
@@ -129,6 +146,7 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
       if (comp(l, fi) == rank) mine[l].push_back(fi);
 
   LevelKeep prev;   // level l-1
+  std::vector<std::vector<i32>> leaf_run(L + 1);   // owned free leaf DoFs per level (local index)
   for (int l = 0; l <= L; ++l) {
     LocalLevel& v = Lt.lv[l];
     v.level = l;
@@ -202,30 +220,50 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
           if (c1 >= 0) hnext[h][c] = comp(l + 1, c1 / nch);
         }
     }
-    // ---------------- occurrences, sorted by key
+    // ---------------- occurrences, sorted by key -- in key-range chunks of at most
+    // ~64M occurrences so that the sort buffers stay bounded (the finest level of a
+    // config-5 rank has ~270M occurrences); every key falls into exactly one chunk,
+    // so the nodes come out in key order across chunks
     const i64 n_occ = nh * stride;
     GMG_REQUIRE(n_occ < ((i64)1 << 32), GMG_E_OOM, "halo too large for 32-bit occurrence ids");
-    std::vector<u64> okey(n_occ);
-    std::vector<u32> oid(n_occ);
-    for (i64 h = 0; h < nh; ++h) {
+    auto occ_key = [&](i64 h, int a) {
       const Vec3 G = unmorton(d, l == 0 ? p.levels[0].key[H[h]] : parent_key(l, H[h]));
+      const Vec3 X = l == 0 ? X_of(G, 0, off0[a], 1) : X_of(G, l, pt.pa[a], 2);
+      return morton(d, X);
+    };
+    u64 kmin = ~0ull, kmax = 0;
+    for (i64 h = 0; h < nh; ++h)
       for (int a = 0; a < stride; ++a) {
-        const Vec3 X = l == 0 ? X_of(G, 0, off0[a], 1) : X_of(G, l, pt.pa[a], 2);
-        okey[h * stride + a] = morton(d, X);
-        oid[h * stride + a] = (u32)(h * stride + a);
+        const u64 kk = occ_key(h, a);
+        kmin = std::min(kmin, kk);
+        kmax = std::max(kmax, kk);
       }
-    }
-    radix_sort_pairs32(okey, oid, kbits);
-    // ---------------- unique nodes: flags, owner, transfer owner, need, ranks that need it
+    i64 chunk_target = (i64)1 << 26;
+    if (const char* e = std::getenv("GMG_OCC_CHUNK")) chunk_target = std::max<i64>(64, std::atoll(e));   // tests
+    const i64 n_chunks = n_occ == 0 ? 1 : std::max<i64>(1, (n_occ + chunk_target - 1) / chunk_target);
+    const u64 span = n_occ == 0 ? 1 : (kmax - kmin) / (u64)n_chunks + 1;
     cur.node_of_occ.assign(n_occ, -1);
     std::vector<u64> nkey;
     std::vector<uint8_t> nfl, nneed, nmine;
     std::vector<i32> nown, ntpos;      // owner; transfer-owner family as halo position
     std::vector<std::vector<i32>> sidx(P);   // filled after local numbering: (node, peer)
     std::vector<std::pair<i32, i32>> sends;   // (peer, node) for owned nodes
-    for (i64 s = 0; s < n_occ;) {
+    for (i64 ch = 0; ch < n_chunks; ++ch) {
+    const u64 lo = kmin + span * (u64)ch, hi = ch + 1 == n_chunks ? ~0ull : kmin + span * (u64)(ch + 1);
+    std::vector<u64> okey;
+    std::vector<u32> oid;
+    for (i64 h = 0; h < nh; ++h)
+      for (int a = 0; a < stride; ++a) {
+        const u64 kk = occ_key(h, a);
+        if (kk < lo || kk >= hi) continue;
+        okey.push_back(kk);
+        oid.push_back((u32)(h * stride + a));
+      }
+    radix_sort_pairs32(okey, oid, kbits);
+    const i64 n_run = (i64)okey.size();
+    for (i64 s = 0; s < n_run;) {
       i64 e = s;
-      while (e < n_occ && okey[e] == okey[s]) ++e;
+      while (e < n_run && okey[e] == okey[s]) ++e;
       uint8_t fl = 0, need = 0, inmine = 0;
       i32 own = INT32_MAX;
       const i32 node = (i32)nkey.size();
@@ -286,10 +324,7 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
       nmine.push_back(inmine);
       s = e;
     }
-    okey.clear();
-    okey.shrink_to_fit();
-    oid.clear();
-    oid.shrink_to_fit();
+    }   // chunk
     const i64 nnodes = (i64)nkey.size();
     // ---------------- counts: each node by its owner (B nodes by the min computing rank)
     {
@@ -378,16 +413,13 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     // ---------------- local cells, classes, lambda, eigen start vector
     v.cls.resize(nloc);
     v.lam.assign(nloc, 0);
-    v.eig_v.assign(nloc, 0.0);
+    // eig_v stays empty: the key-based start vector (R10b) is formed from owned_key
+    // where it is needed (eig_start_from_keys), not stored for all local DoFs
     auto fill_node = [&](i64 li, i64 i) {
       const uint8_t fl = nfl[i];
       v.cls[li] = (fl & F_EREG) ? CLS_E : CLS_S;
       if (li >= v.n_owned || v.cls[li] != CLS_S) return;
       v.lam[li] = (fl & F_LEAF) ? 1 : 0;   // S here, in a level-l leaf: not S on level l+1
-      const Vec3 X = unmorton(d, nkey[i]);
-      Vec3 Y{0, 0, 0};
-      for (int j = 0; j < d; ++j) Y[j] = X[j] >> (L - l);
-      v.eig_v[li] = -5.5 + (double)(morton(d, Y) % 12);   // R10b
     };
     for (i64 i = 0; i < v.n_owned; ++i) fill_node(i, owned[i]);
     for (i64 i = 0; i < v.n_ghost; ++i) fill_node(v.n_owned + i, ghosts[i]);
@@ -413,7 +445,6 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     }
     if (l > 0) {
       const int row = np + nn;
-      v.fam_dofs.resize((size_t)v.n_fam * np);
       v.xfer.resize((size_t)v.n_fam * row);
       for (i64 lf = 0; lf < v.n_fam; ++lf) {
         const i64 fi = mine[l][lf];
@@ -432,7 +463,6 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
               if (nfl[i] & F_EREG) edge = true;
             }
           }
-          v.fam_dofs[(size_t)lf * np + a] = enc;
           v.xfer[(size_t)lf * row + a] = enc;
         }
         // the parent's (k+1)^d nodes on level l-1
@@ -460,23 +490,38 @@ LocalTopo make_local_direct(const Forest& f, const Partition& p, int k, int rank
     }
     // ---------------- owned free leaf DoFs of this level
     for (i64 i = 0; i < v.n_owned; ++i)
-      if (v.lam[i]) Lt.leaf_tmp.push_back({v.owned_key[i], (int8_t)l, i});
+      if (v.lam[i]) leaf_run[l].push_back((i32)i);   // owned order = key order
     cnt.own_dofs[l] = (double)v.n_owned;
     // the Dirichlet nodes have local -1: prev.local gives -1 for them (xfer parent part)
     for (i64 i = 0; i < nnodes; ++i)
       if (nfl[i] & F_B) cur.local[i] = -1;
     prev = std::move(cur);
   }
-  // leaf order (owner, key): this rank's leaf DoFs by key
-  std::sort(Lt.leaf_tmp.begin(), Lt.leaf_tmp.end(),
-            [](const LocalTopo::LeafRec& a, const LocalTopo::LeafRec& b) { return a.key < b.key; });
-  for (const auto& r : Lt.leaf_tmp) {
-    Lt.leaf_level.push_back(r.level);
-    Lt.leaf_local.push_back(r.local);
-    Lt.leaf_key.push_back(r.key);
+  // leaf order (owner, key): merge the per-level runs (each in key order) by key
+  {
+    size_t total = 0;
+    for (auto& r : leaf_run) total += r.size();
+    Lt.leaf_level.reserve(total);
+    Lt.leaf_local.reserve(total);
+    Lt.leaf_key.reserve(total);
+    std::vector<size_t> pos(L + 1, 0);
+    for (size_t c = 0; c < total; ++c) {
+      int best = -1;
+      u64 bk = ~0ull;
+      for (int l = 0; l <= L; ++l)
+        if (pos[l] < leaf_run[l].size()) {
+          const u64 kk = Lt.lv[l].owned_key[leaf_run[l][pos[l]]];
+          if (best < 0 || kk < bk) {
+            best = l;
+            bk = kk;
+          }
+        }
+      Lt.leaf_level.push_back((int8_t)best);
+      Lt.leaf_local.push_back(leaf_run[best][pos[best]]);
+      Lt.leaf_key.push_back(bk);
+      ++pos[best];
+    }
   }
-  Lt.leaf_tmp.clear();
-  Lt.leaf_tmp.shrink_to_fit();
   Lt.n_leaf_owned = (i64)Lt.leaf_level.size();
   Lt.leaf_first = -1;          // set from the other ranks' counts (LocalCounts)
   Lt.n_leaf_global = -1;

@@ -28,6 +28,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
     np *= NP1;
   }
   const int G1 = 4 * k + 1, GNP = G1 * G1 * G1;
+  const int xr = np + nn;   // xfer row: the family patch, then the parent's DoFs
   // interior patch positions, z-major (ascending patch index)
   std::vector<int> inner;
   for (int a = 0; a < np; ++a) {
@@ -79,14 +80,14 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
       auto for_patches = [&](auto&& fn) {
         for (i64 f = 0; f < v.n_fam; ++f) {
           if (fg[f] < 0) {
-            for (int a = 0; a < np; ++a) fn(dec(v.fam_dofs[(size_t)f * np + a]));
+            for (int a = 0; a < np; ++a) fn(dec(v.xfer[(size_t)f * xr + a]));
           } else if (gfs[l][fg[f]] == f) {
             for (int Z = 0; Z < G1; ++Z)
               for (int Y = 0; Y < G1; ++Y)
                 for (int X = 0; X < G1; ++X) {
                   int j, a;
                   gf_pos(k, X, Y, Z, j, a);
-                  fn(dec(v.fam_dofs[(size_t)(f + j) * np + a]));
+                  fn(dec(v.xfer[(size_t)(f + j) * xr + a]));
                 }
           }
         }
@@ -98,7 +99,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
       });
       for (i64 f = 0; f < v.n_fam; ++f)
         for (int a : inner)
-          GMG_REQUIRE(dec(v.fam_dofs[(size_t)f * np + a]) >= 0, GMG_E_STATE, "interior patch node without a DoF");
+          GMG_REQUIRE(dec(v.xfer[(size_t)f * xr + a]) >= 0, GMG_E_STATE, "interior patch node without a DoF");
       for_patches([&](i64 g) {
         if (g >= 0 && g < no && touch[g] == 1 && !remote[g] && perm[g] < 0) perm[g] = (i32)pos++;
       });
@@ -120,7 +121,6 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
     const i64 n = v.n_local();
     for (auto& c : v.cell_dofs)
       if (c >= 0) c = p[c];
-    for (auto& e : v.fam_dofs) e = remap_enc(e, p);
     if (l > 0) {
       const int row = np + nn;
       const std::vector<i32>& pc = P.perm[l - 1];
@@ -163,7 +163,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
           for (int X = 0; X < G1; ++X) {
             int j, a;
             gf_pos(k, X, Y, Z, j, a);
-            const i64 g = dec(v.fam_dofs[(size_t)(f0 + j) * np + a]);
+            const i64 g = dec(v.xfer[(size_t)(f0 + j) * xr + a]);
             // transfer owner inside the grandfamily: some family containing the node
             // holds it with a non-negative entry
             bool own = false;
@@ -172,7 +172,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
                 for (int cx = 0; cx < 2; ++cx) {
                   const int lx = X - 2 * k * cx, ly = Y - 2 * k * cy, lz = Z - 2 * k * cz;
                   if (lx < 0 || lx > 2 * k || ly < 0 || ly > 2 * k || lz < 0 || lz > 2 * k) continue;
-                  const i32 e = v.fam_dofs[(size_t)(f0 + cx + 2 * cy + 4 * cz) * np + lx + NP1 * ly + NP1 * NP1 * lz];
+                  const i32 e = v.xfer[(size_t)(f0 + cx + 2 * cy + 4 * cz) * xr + lx + NP1 * ly + NP1 * NP1 * lz];
                   if (e >= 0) own = true;
                 }
             row[X + G1 * Y + G1 * G1 * Z] = g < 0 ? -1 : (own ? (i32)g : (i32)(-2 - g));
@@ -217,7 +217,7 @@ DevicePlan plan_device_order(LocalTopo& T, bool grandfamilies, int gf_min_level)
       const i64 nf = fams ? (i64)fams->size() : v.n_fam;
       for (i64 i = 0; i < nf; ++i) {
         const i64 f = fams ? (*fams)[i] : i;
-        (ghost_in(v.fam_dofs.data() + (size_t)f * np, np) ? P.fam_bnd : P.fam_int)[l].push_back((i32)f);
+        (ghost_in(v.xfer.data() + (size_t)f * xr, np) ? P.fam_bnd : P.fam_int)[l].push_back((i32)f);
       }
       for (i64 q = 0; q < P.n_gf[l]; ++q)
         (ghost_in(P.gx[l].data() + (size_t)q * GROW, GNP) ? P.gf_bnd : P.gf_int)[l].push_back((i32)q);

@@ -140,3 +140,22 @@ def test_gloo_rank_local_exchange_plans_match(name, world, coarse):
     for p_ in ps:
         p_.join(timeout=60)
     assert all(r[1] == "ok" for r in res), res
+
+
+def test_rank_local_chunked_occurrence_sort(monkeypatch):
+    """The rank-local builder sorts the halo's node occurrences in key-range chunks
+    (bounded memory for config 5); forcing tiny chunks must give the same layout."""
+    cfg, passes = _cfg("c3p2")
+    f = G.gmg_forest_generate(G.recipe_from_config(cfg, passes))
+    part = G.gmg_partition(f, 3)
+    ref = [G.gmg_setup(f, part, k=2, rank=r, host_only=True, rank_local=True) for r in range(3)]
+    monkeypatch.setenv("GMG_OCC_CHUNK", "1000")
+    for r in range(3):
+        h = G.gmg_setup(f, part, k=2, rank=r, host_only=True, rank_local=True)
+        for l in range(h.info()["n_levels"]):
+            a, b = ref[r].local_level(l), h.local_level(l)
+            for key in a:
+                assert np.array_equal(a[key], b[key]), (r, l, key)
+            ta, tb = ref[r].local_tables(l), h.local_tables(l)
+            for key in ta:
+                assert np.array_equal(ta[key], tb[key]), (r, l, key)
