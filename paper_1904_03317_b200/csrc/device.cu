@@ -99,6 +99,7 @@ struct DeviceHierarchy {
   // small levels 1..slk_ls (+ the coarse solve) run as one persistent kernel (small_vcycle);
   // 0 = off.  Chosen at setup: one rank, family-patch levels, constant coefficient,
   // Cholesky coarse solver, every level 1..slk_ls with <= GMG_SLK_FAM families (2048)
+  double z1_c0 = 0;             // c2_0 of the TA_CHEB_Z1 step being launched (x_1 = c2_0 D^-1 g)
   int slk_ls = 0;
   int slk_grid = 0;
   dev::SlkLevel* slk_dev = nullptr;
@@ -318,7 +319,8 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
   const int grid = (int)((ng + SL - 1) / SL);
   dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
       (int)ng, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
-      prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr, glist);
+      prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr, glist,
+      d->z1_c0, v.n_owned);
   d->launches++;
 }
 
@@ -343,10 +345,11 @@ static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, con
     if constexpr (K == 2)
       dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
           (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
-          fl ? 0 : tensor_wave<K, T, TM>(d), fl);
+          fl ? 0 : tensor_wave<K, T, TM>(d), fl, d->z1_c0, v.n_owned);
     else
       dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
-          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc, 0, fl);
+          (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc, 0, fl,
+          d->z1_c0, v.n_owned);
     d->launches++;
   }
 }
@@ -496,9 +499,18 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
 // streaming step where the level has no R1 (2D, coefficient levels, level 0).
 template <typename T, int TM, bool RDV, bool WDV, bool DVX = false>
 static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, double c1, double c2,
-                            cudaStream_t s, const T* xc = nullptr) {
+                            cudaStream_t s, const T* xc = nullptr, double c0 = 0.0) {
   constexpr bool PRO = TM == dev::TA_CHEB_P01;   // x + P x_{l-1} (xc) fused in; only called where n_r1 > 0
+  constexpr bool Z1 = TM == dev::TA_CHEB_Z1;     // x_1 = c0 D^-1 g formed in the kernels; only where n_r1 > 0
   DevLevel& v = d->lv[l];
+  if (Z1) {
+    if (v.n_r1 == 0) throw Error(GMG_E_STATE, "TA_CHEB_Z1 on a level without R1");
+    d->z1_c0 = c0;
+    if (d->comm && v.n_send) {   // the owners' send rows carry x_1 for the ghost import
+      dev::x1_rows<T><<<(int)((v.n_send + 255) / 256), 256, 0, s>>>(v.n_send, v.send_idx, g, MG<T>::Dinv(v), x, c0);
+      d->launches++;
+    }
+  }
   if (v.n_r1 > 0) {
     const int np = (2 * d->k + 1) * (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1) * (d->k + 1);
     // the operator's x gather and index rows, t (reduced) on the rows outside R1,
@@ -509,7 +521,7 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     if (PRO) fb += vb * (double)d->lv[l - 1].n + vb * (double)(v.n_owned - v.n_r1);
     const double idx = 4.0 * nn * (double)v.n_cells + (PRO ? 4.0 * nn * (double)v.n_fam : 0.0);
     const double idx_layout = 4.0 * np * (double)v.n_fam + (PRO ? 4.0 * nn * (double)v.n_fam : 0.0);
-    const int kind = TM == dev::TA_CHEB_X1 ? GMG_K_CHEB_X1 : TM == dev::TA_CHEB_11 ? GMG_K_CHEB_11
+    const int kind = (TM == dev::TA_CHEB_X1 || Z1) ? GMG_K_CHEB_X1 : TM == dev::TA_CHEB_11 ? GMG_K_CHEB_11
                    : TM == dev::TA_CHEB_10 ? GMG_K_CHEB_10 : TM == dev::TA_CHEB_P01 ? GMG_K_CHEB_P01
                    : TM == dev::TA_CHEB_01 ? GMG_K_CHEB_01 : GMG_K_CHEB_00;
     Prof pr(d, s, kind, l, fb + idx, fb + idx_layout);
@@ -523,10 +535,11 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     if (n > 0) {
       const int nvec = 6 + (RDV && !DVX ? 1 : 0) + (WDV ? 1 : 0) + (PRO ? 1 : 0);   // g D t x (+dv) | t x (+dv)
       Prof pr2(d, s, GMG_K_CHEB_STREAM, l, (double)nvec * sizeof(T) * (double)n);
-      dev::cheb_range<T, RDV, WDV, DVX, PRO><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
-          v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2, v.n_owned);
+      dev::cheb_range<T, RDV, WDV, DVX, PRO, Z1><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
+          v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2, v.n_owned, c0);
       d->launches++;
     }
+    d->z1_c0 = 0;
   } else {
     if (PRO) throw Error(GMG_E_STATE, "fused prolongation on a level without R1");
     import_ghosts(d, l, x, s);
@@ -534,6 +547,16 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     export_add(d, l, t, s);
     k_cheb<T, true, RDV, WDV, false, DVX>(d, v, g, t, dv, x, c1, c2, s);
   }
+}
+
+// GMG_Z1=0: the first pre-smoothing step from 0 as its own pass (x_1 = c2_0 D^-1 g)
+// followed by TA_CHEB_X1, instead of TA_CHEB_Z1
+static bool z1_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GMG_Z1");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // Chebyshev-Jacobi smoothing on level l with rhs g, state x (x-form of the
@@ -548,6 +571,10 @@ static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, boo
   int j0 = 1;
   if (xc) {                            // post-smoothing with x + P x_{l-1} fused into step 0 (prolong_fusable)
     cheb_step_fused<T, dev::TA_CHEB_P01, false, true>(d, l, g, x, t, dv, 0.0, v.c2[0], s, xc);
+  } else if (x_zero && m > 1 && v.n_r1 > 0 && z1_enabled()) {
+    // x_1 = dv_0 = c2_0 D^-1 g is formed inside the step-1 kernels (TA_CHEB_Z1): no pass for it
+    cheb_step_fused<T, dev::TA_CHEB_Z1, true, true, true>(d, l, g, x, t, dv, v.c1[1], v.c2[1], s, nullptr, v.c2[0]);
+    j0 = 2;
   } else if (x_zero && m > 1) {
     // x_1 = dv_0 = c2_0 D^-1 g: only x is stored, the next step reads dv_0 from x
     k_cheb<T, false, false, false, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);

@@ -356,7 +356,10 @@ constexpr int TA_LOAD_AT = TA_LOAD_AT_DEFAULT;
 // rows are finished here; for the other rows the transfer-owner family leaves
 // P x_{l-1} in dv (dead before this step) and cheb_range<..., PRO> adds it.
 enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5,
-             TA_CHEB_P01 = 6 };
+             TA_CHEB_P01 = 6, TA_CHEB_Z1 = 7 };
+// TA_CHEB_Z1: TA_CHEB_X1 without the preceding pass x_1 = c2_0 D^-1 g (the first step
+// from x = 0): the gather forms x_1 = c0 D^-1 g itself on the owned rows (ghost rows:
+// imported x_1, materialised on the owners' send rows), cheb_range<..., Z1> likewise
 
 // the body of fam_tensor_apply for virtual block vb, shared memory passed in
 // (s0, s1: TensorCfg<K>::NS entries each; cbf: FPB * ((k+1)^3 + 1) for TA_CHEB_P01), so
@@ -372,8 +375,9 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
                  const T* __restrict__ x, T* __restrict__ y, long n_r1, const T* __restrict__ g,
                  const T* __restrict__ Dinv, T* __restrict__ dv, T* xw,
                  double c1_, double c2_, const T* __restrict__ xc, int pf,
-                 const int* __restrict__ flist) {
-  constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
+                 const int* __restrict__ flist, double c0_ = 0, long n_own = 0) {
+  constexpr bool Z1 = TM == TA_CHEB_Z1;
+  constexpr bool DVX = TM == TA_CHEB_X1 || Z1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   constexpr int NP1 = 2 * K + 1, S2 = NP1 * NP1, NL = TensorCfg<K>::NL, FPB = TensorCfg<K>::FPB;
@@ -411,7 +415,11 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
       if (PRO && e >= 0) own |= 1 << z;
     }
 #pragma unroll
-    for (int z = 0; z < NP1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+    for (int z = 0; z < NP1; ++z) {
+      const int i = gi[z];
+      if (Z1) u[z] = i < 0 ? T(0) : (i < n_own ? (T)c0_ * __ldg(Dinv + i) * __ldg(g + i) : __ldg(x + i));
+      else u[z] = i >= 0 ? __ldg(x + i) : T(0);
+    }
   }
   if constexpr (PRO) {
     // P x_{l-1} on this thread's z line, in registers: the parent's values are
@@ -606,12 +614,12 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
-                 const int* __restrict__ flist = nullptr) {
+                 const int* __restrict__ flist = nullptr, double c0_ = 0, long n_own = 0) {
   using SM = TensorSmem<K, T>;
   __shared__ T s0[SM::NS], s1[SM::NS];
   __shared__ T cb[TM == TA_CHEB_P01 ? SM::NCB : 1];
   fam_tensor_body<K, T, TM>(blockIdx.x, s0, s1, cb, nfam, xfer, row, fcoef, scale_, x, y, n_r1, g, Dinv, dv, xw, c1_,
-                            c2_, xc, pf, flist);
+                            c2_, xc, pf, flist, c0_, n_own);
 }
 
 // ------------------------------------------------------------- grandfamily patches
@@ -701,8 +709,10 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
                   const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
                   const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
                   double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
-                  int xpf = 0, const int2* __restrict__ r1run = nullptr, const int* __restrict__ glist = nullptr) {
-  constexpr bool DVX = TM == TA_CHEB_X1, PRO = TM == TA_CHEB_P01;
+                  int xpf = 0, const int2* __restrict__ r1run = nullptr, const int* __restrict__ glist = nullptr,
+                  double c0_ = 0, long n_own = 0) {
+  constexpr bool Z1 = TM == TA_CHEB_Z1;
+  constexpr bool DVX = TM == TA_CHEB_X1 || Z1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
   using S = GfShape<K>;
@@ -766,7 +776,11 @@ gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict_
       if (PRO && e >= 0) own |= 1 << z;
     }
 #pragma unroll
-    for (int z = 0; z < N1; ++z) u[z] = gi[z] >= 0 ? __ldg(x + gi[z]) : T(0);
+    for (int z = 0; z < N1; ++z) {
+      const int i = gi[z];
+      if (Z1) u[z] = i < 0 ? T(0) : (i < n_own ? (T)c0_ * __ldg(Dinv + i) * __ldg(g + i) : __ldg(x + i));
+      else u[z] = i >= 0 ? __ldg(x + i) : T(0);
+    }
   }
   if constexpr (PRO) {
     // x + P x_{l-1}: every fine node from one parent containing it, in
@@ -1149,11 +1163,12 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
 // The Chebyshev step on [a, n) only (the rows not finished by the fused apply):
 // scalar form of cheb_step<T, READ_T = 1, ..., X_ZERO = 0>.
 // one row of cheb_range (used by the persistent small-level kernel)
-template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X, bool PRO>
+template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X, bool PRO, bool Z1 = false>
 __device__ __forceinline__ void cheb_row(long i, const T* __restrict__ g, const T* __restrict__ Dinv, T* __restrict__ t,
-                                         T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_, long n_own) {
+                                         T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_, long n_own,
+                                         double c0_ = 0) {
   const T G = g[i], Tv = t[i], Di = Dinv[i];
-  T X = x[i];
+  T X = Z1 ? (T)c0_ * Di * G : x[i];   // Z1: x_1 = c2_0 D^-1 g formed here (0 on ghosts / E rows)
   if (PRO && i < n_own) X = X + dv[i];
   T V = 0;
   if (READ_DV) V = DV_IS_X ? X : dv[i];
@@ -1164,15 +1179,15 @@ __device__ __forceinline__ void cheb_row(long i, const T* __restrict__ g, const 
   x[i] = X + dd;
 }
 
-template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false, bool PRO = false>
+template <typename T, bool READ_DV, bool WRITE_DV, bool DV_IS_X = false, bool PRO = false, bool Z1 = false>
 __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __restrict__ g,
                                                      const T* __restrict__ Dinv, T* __restrict__ t,
                                                      T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_,
-                                                     long n_own = 0) {
+                                                     long n_own = 0, double c0_ = 0) {
   const long i = a + (long)blockIdx.x * VEC_NT + threadIdx.x;
   if (i >= n) return;
   const T G = g[i], Tv = t[i], Di = Dinv[i];
-  T X = x[i];
+  T X = Z1 ? (T)c0_ * Di * G : x[i];   // Z1: x_1 = c2_0 D^-1 g (see TA_CHEB_Z1)
   if (PRO && i < n_own) X = X + dv[i];   // x + P x_{l-1} (fam_tensor_apply<TA_CHEB_P01> left it in dv)
   T V = 0;
   if (READ_DV) V = DV_IS_X ? X : dv[i];      // DV_IS_X: dv_0 = x_1 after the first step from 0
@@ -1181,6 +1196,17 @@ __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __
   if (READ_DV) dd = fma((T)c1_, V, dd);
   if (WRITE_DV) dv[i] = dd;
   x[i] = X + dd;
+}
+
+// x_1 = c0 D^-1 g on the rows in idx (the send rows before a TA_CHEB_Z1 import)
+template <typename T>
+__global__ void x1_rows(long n, const int* __restrict__ idx, const T* __restrict__ g, const T* __restrict__ Dinv,
+                        T* __restrict__ x, double c0) {
+  const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int i = idx[k];
+    x[i] = (T)c0 * Dinv[i] * g[i];
+  }
 }
 
 // dst[perm[i]] = src[i] (level order -> device order, plan.hpp) and the inverse
