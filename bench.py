@@ -517,7 +517,8 @@ def run_ours(args):
                           f"on rank 0, {args.transport} ghost exchange",
                           "partition": args.partition, "partition_eta": main["partition_eta"],
                           "ghost_children_ratio": main["ghost_children_ratio"], "setup_s": main["setup_s"],
-                          "setup": main["setup"]},
+                          "setup": main["setup"], "grandfamily_patches": sum(info["level_gf"]),
+                          "r1_rows_finest": info["level_r1"][-1]},
                "roofline": main["roofline"], "apply_plain": main["apply_plain"], "kernels": main["kernels"],
                "cpu_baseline": cpu, "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
                "launches_per_vcycle": main["launches_per_vcycle"], "clocks": main["clocks"], "cg": main["cg"]}
