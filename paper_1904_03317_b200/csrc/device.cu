@@ -549,12 +549,14 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
   }
 }
 
-// GMG_Z1=0: the first pre-smoothing step from 0 as its own pass (x_1 = c2_0 D^-1 g)
-// followed by TA_CHEB_X1, instead of TA_CHEB_Z1
+// GMG_Z1=1: TA_CHEB_Z1 instead of the pass x_1 = c2_0 D^-1 g followed by TA_CHEB_X1.
+// Off by default: the doubled gather (D^-1 and g at every patch node) slows the
+// step-1 kernels by about what the saved pass costs (c5 19.24 vs 19.34 ms, c3 7.58
+// vs 7.55 ms)
 static bool z1_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("GMG_Z1");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

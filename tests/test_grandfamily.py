@@ -92,3 +92,20 @@ def test_grandfamily_vcycle_vs_oracle():
     ref = mg.vcycle(oh, b)
     err = np.abs(x.cpu().numpy() - ref).max() / np.abs(ref).max()
     assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("name,passes,over", [("c3", 3, {}), ("c5", 2, {"shell": (96, 1024)})], ids=["c3p3", "c5-thick"])
+def test_z1_step_matches_separate_pass(tmp_path, name, passes, over):
+    """TA_CHEB_Z1 (x_1 formed inside the step-1 kernels, GMG_Z1=1) gives the
+    V-cycle of the separate pass + TA_CHEB_X1."""
+    outs = []
+    for z1 in ("1", "0"):
+        out = str(tmp_path / f"z{z1}.npz")
+        code = SCRIPT.format(root=ROOT, name=name, over=over, passes=passes, mixed=False, out=out)
+        env = dict(os.environ, GMG_Z1=z1)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(np.load(out))
+    a, b = outs[0]["x"], outs[1]["x"]
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+    assert int(outs[0]["it"]) == int(outs[1]["it"])
