@@ -324,6 +324,34 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
   d->launches++;
 }
 
+// GMG_COL: families per block of the plain operator's column kernel (16 or 32,
+// fp32 always 32); 0 (default) = fam_tensor_apply<TA_APPLY>.  Measured slower
+// (c3 finest level 283 vs 274 us, DESIGN.md section 6 experiment 13)
+static int col_fpc() {
+  static const int n = [] {
+    const char* e = std::getenv("GMG_COL");
+    const int v = e ? std::atoi(e) : 0;
+    return v == 0 ? 0 : (v == 32 ? 32 : 16);
+  }();
+  return n;
+}
+template <int K, typename T, int FPC>
+static void launch_col(DeviceHierarchy* d, DevLevel& v, i64 nf, const int* fl, const T* x, T* y, cudaStream_t s) {
+  constexpr size_t smem = dev::col_smem_bytes<K, T, FPC>();
+  static const int per_sm = [] {
+    CK(cudaFuncSetAttribute(dev::fam_col_apply<K, T, FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::fam_col_apply<K, T, FPC>, dev::ColCfg<K, FPC>::THREADS,
+                                                     smem));
+    return std::max(nb, 1);
+  }();
+  const int np = (2 * K + 1) * (2 * K + 1) * (2 * K + 1), nn = (K + 1) * (K + 1) * (K + 1);
+  const int grid = (int)((nf + FPC - 1) / FPC);
+  dev::fam_col_apply<K, T, FPC><<<grid, dev::ColCfg<K, FPC>::THREADS, smem, s>>>(
+      (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, fl ? 0 : per_sm * d->sms, fl);
+  d->launches++;
+}
+
 // The 3D tensor operator of one level: grandfamily patches (gfam_tensor_apply)
 // plus the remaining families (fam_tensor_apply over the singles list), or all
 // families.  Epilogue mode TM, fused Chebyshev arguments as fam_tensor_apply.
@@ -342,6 +370,13 @@ static void launch_tensor(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, con
   const int* fl = phase == 1 ? v.fam_int : (phase == 2 ? v.fam_bnd : (v.n_gf > 0 ? v.singles : nullptr));
   const i64 nf = phase == 1 ? v.n_fam_int : (phase == 2 ? v.n_fam_bnd : (v.n_gf > 0 ? v.n_single : v.n_fam));
   if (nf > 0) {
+    if constexpr (TM == dev::TA_APPLY) {
+      if (col_fpc() > 0) {   // the plain operator: column kernel (fam_col_apply)
+        if (col_fpc() == 16 && sizeof(T) == 8) launch_col<K, T, 16>(d, v, nf, fl, x, y, s);
+        else launch_col<K, T, 32>(d, v, nf, fl, x, y, s);
+        return;
+      }
+    }
     if constexpr (K == 2)
       dev::fam_tensor_apply<K, T, TM><<<tensor_grid<K>(nf), 32 * dev::TG_WARPS, 0, s>>>(
           (int)nf, v.xfer, np + nn, v.fcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,

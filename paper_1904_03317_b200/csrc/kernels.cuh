@@ -622,6 +622,128 @@ fam_tensor_apply(int nfam, const int* __restrict__ xfer, int row, const double* 
                             c2_, xc, pf, flist, c0_, n_own);
 }
 
+// fam_col_apply: the plain operator (TA_APPLY) on family patches with one thread
+// per x-column of the patch (2k+1 threads per family, each holding the (2k+1)^2
+// nodes (y, z) of its column in registers).  The same Kronecker sum as
+// fam_tensor_apply, ordered so that two of the three 1-D passes run in registers:
+//   c1 = (M_y (x) M_z) u,  c2 = (K_y (x) M_z + M_y (x) K_z) u   per column (registers),
+//   out = K_x c1 + M_x c2                                        along x lines (shared),
+// i.e. one transposition of two arrays and one back instead of fam_tensor_apply's
+// three (2 + 2 + 1 arrays): 6 shared-memory accesses per patch node instead of 10.
+// Gather and scatter run along the columns with the DoF indices in registers
+// (lanes (family, px) read x-consecutive nodes, as fam_tensor_apply's z lines do).
+// Shared layout, per array: node (x, j = y + (2k+1) z) of block family f at
+// j S + (2k+1) f + x with S = (2k+1) FPC + 1 = 1 mod 16: the column writes and
+// reads hit consecutive addresses (thread t = (2k+1) f + px), the x-line reads
+// of thread (f, r) -- lines (y = r, z) -- hit r + 5 f + const (mod 16): no bank
+// conflicts on any pass.  The x-line thread writes its result over the c1 entries
+// it alone read.  FPC families per block.
+template <int K, int FPC> struct ColCfg {
+  static constexpr int NP1 = 2 * K + 1, NJ = NP1 * NP1, THREADS = NP1 * FPC, S = NP1 * FPC + 1;
+  static constexpr int NS = NJ * S;
+};
+template <int K, typename T, int FPC>
+__global__ void __launch_bounds__(ColCfg<K, FPC>::THREADS)
+fam_col_apply(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
+              const T* __restrict__ x, T* __restrict__ y, long n_r1, int pf, const int* __restrict__ flist) {
+  using C = ColCfg<K, FPC>;
+  constexpr int NP1 = C::NP1, NJ = C::NJ, S = C::S;
+  extern __shared__ __align__(16) unsigned char col_smem[];
+  T* const c1s = reinterpret_cast<T*>(col_smem);
+  T* const c2s = c1s + C::NS;
+  const int t = threadIdx.x, fl = t / NP1, px = t % NP1;
+  const long fi = (long)blockIdx.x * FPC + fl;
+  const bool act = fi < nfam;
+  const long f = flist ? (act ? (long)__ldg(flist + fi) : 0) : fi;
+  if (pf > 0 && !flist) {   // the patch rows of the block one resident wave ahead -> L2
+    const long fb = ((long)blockIdx.x + pf) * FPC;
+    const long bytes = (long)FPC * row * 4, off = (long)t * 128;
+    if (fb < nfam && off < bytes && fb * row * 4 + off < (long)nfam * row * 4)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(xfer + fb * (long)row) + off));
+  }
+  const int* rp = xfer + (act ? f : 0) * (long)row;
+  int gi[NJ];
+  T u[NJ];
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) gi[j] = decode_dof(__ldg(rp + j * NP1 + px));   // node (px, y, z), j = y + NP1 z
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) u[j] = gi[j] >= 0 ? __ldg(x + gi[j]) : T(0);
+    // z pass per y row: m = M_z u, k = K_z u
+    T m[NJ], kz[NJ];
+#pragma unroll
+    for (int yy = 0; yy < NP1; ++yy)
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) {
+        T a = 0, b = 0;
+#pragma unroll
+        for (int q = 0; q < NP1; ++q) {
+          if (Mt<K>(z, q) != 0.0) a = fma((T)Mt<K>(z, q), u[yy + NP1 * q], a);
+          if (Kt<K>(z, q) != 0.0) b = fma((T)Kt<K>(z, q), u[yy + NP1 * q], b);
+        }
+        m[yy + NP1 * z] = a;
+        kz[yy + NP1 * z] = b;
+      }
+    // y pass per z: c1 = M_y m, c2 = K_y m + M_y k -> shared
+#pragma unroll
+    for (int z = 0; z < NP1; ++z)
+#pragma unroll
+      for (int yy = 0; yy < NP1; ++yy) {
+        T a = 0, b = 0;
+#pragma unroll
+        for (int q = 0; q < NP1; ++q) {
+          if (Mt<K>(yy, q) != 0.0) {
+            a = fma((T)Mt<K>(yy, q), m[q + NP1 * z], a);
+            b = fma((T)Mt<K>(yy, q), kz[q + NP1 * z], b);
+          }
+          if (Kt<K>(yy, q) != 0.0) b = fma((T)Kt<K>(yy, q), m[q + NP1 * z], b);
+        }
+        const int j = yy + NP1 * z;
+        c1s[j * S + t] = a;
+        c2s[j * S + t] = b;
+      }
+  }
+  __syncthreads();
+  if (act) {   // x lines (y = px, z): out = scale (K_x c1 + M_x c2), over c1
+    const T scale = (T)(fcoef ? scale_ * __ldg(fcoef + f) : scale_);
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) {
+      const int base = (px + NP1 * z) * S + NP1 * fl;
+      T a[NP1], b[NP1];
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        a[q] = c1s[base + q];
+        b[q] = c2s[base + q];
+      }
+#pragma unroll
+      for (int xx = 0; xx < NP1; ++xx) {
+        T o = 0;
+#pragma unroll
+        for (int q = 0; q < NP1; ++q) {
+          if (Kt<K>(xx, q) != 0.0) o = fma((T)Kt<K>(xx, q), a[q], o);
+          if (Mt<K>(xx, q) != 0.0) o = fma((T)Mt<K>(xx, q), b[q], o);
+        }
+        c1s[base + xx] = scale * o;
+      }
+    }
+  }
+  __syncthreads();
+  if (act) {   // scatter along the column: rows only this family touches stored, the others reduced at L2
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int i = gi[j];
+      if (i < 0) continue;
+      const T v = c1s[j * S + t];
+      const int yy = j % NP1, z = j / NP1;
+      const bool inner = px > 0 && px < 2 * K && yy > 0 && yy < 2 * K && z > 0 && z < 2 * K;
+      if (i < n_r1 || inner) y[i] = v;
+      else atomicAdd(y + i, v);
+    }
+  }
+}
+template <int K, typename T, int FPC>
+constexpr size_t col_smem_bytes() { return 2 * sizeof(T) * ColCfg<K, FPC>::NS; }
+
 // ------------------------------------------------------------- grandfamily patches
 // gfam_tensor_apply: the level operator on the (4k+1)^3 patch of a complete
 // grandfamily -- the 64 level-l cells below one level-(l-2) cell G all of whose 8

@@ -26,4 +26,12 @@ ncu --profile-from-start off --set full --clock-control none --import-source on 
     --launch-skip 6 --launch-count 2 -o $OUT/ncu_c5_apply -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full_c5a.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply \
     --launch-skip 1 --launch-count 1 -o $OUT/ncu_c3_cheb11 -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3b.log 2>&1
+
+# the reports themselves stay on the box (gpurun copies back <= 64 MiB): raw metrics
+# and the details page of each, as text
+for r in $OUT/*.ncu-rep; do
+  ncu -i $r --page raw --csv > ${r%.ncu-rep}.raw.csv 2>/dev/null
+  ncu -i $r --page details > ${r%.ncu-rep}.details.txt 2>/dev/null
+  rm -f $r
+done
 echo done

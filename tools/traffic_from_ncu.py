@@ -4,7 +4,7 @@ that make up one launch of that kind (a grandfamily-patch kernel plus the
 family kernel of the remaining families), into profiles/<round>_traffic.json
 keyed config/precision/kind/level -- bench.py's roofline.traffic.
 
-    python tools/traffic_from_ncu.py REPORT.ncu-rep CONFIG PRECISION KIND LEVEL OUT.json [FIRST [COUNT]]
+    python tools/traffic_from_ncu.py REPORT.ncu-rep|REPORT.raw.csv CONFIG PRECISION KIND LEVEL OUT.json [FIRST [COUNT]]
 
 FIRST/COUNT select the report rows (0-based, default all rows).
 """
@@ -17,7 +17,10 @@ import sys
 
 
 def main(rep, config, precision, kind, level, out, first=0, count=None):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):     # the raw page exported on the GPU box (tools/profile_round.sh)
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, u = rows[0], rows[1]
     data = rows[2:][int(first):]
