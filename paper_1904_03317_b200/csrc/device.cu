@@ -292,15 +292,29 @@ static double apply_layout(const DeviceHierarchy* d, const DevLevel& v, size_t v
   return 2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam;
 }
 
+// GMG_GF_R96=0: TA_CHEB_11 / TA_CHEB_10 grandfamily kernels at the 80-register cap
+// (spilling) instead of gfam_tensor_apply_r96
+static bool gf_r96() {
+  static const bool on = [] {
+    const char* e = std::getenv("GMG_GF_R96");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 template <int K, typename T, int TM, int SL>
 static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T* g, T* dv, T* xw, double c1,
                       double c2, const T* xc, cudaStream_t s, const int* glist = nullptr, i64 ng = -1) {
-  static const int per_sm = [] {
-    CK(cudaFuncSetAttribute(dev::gfam_tensor_apply<K, T, TM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)dev::gf_smem_bytes<K, T, SL>()));
+  using KernelT = decltype(&dev::gfam_tensor_apply<K, T, TM, SL>);
+  constexpr bool R96_MODE = (TM == dev::TA_CHEB_11 || TM == dev::TA_CHEB_10) && SL == 1;
+  KernelT kern = &dev::gfam_tensor_apply<K, T, TM, SL>;
+  if constexpr (R96_MODE) {
+    if (gf_r96()) kern = &dev::gfam_tensor_apply_r96<K, T, TM, SL>;
+  }
+  static const int per_sm = [kern] {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dev::gf_smem_bytes<K, T, SL>()));
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::gfam_tensor_apply<K, T, TM, SL>,
-                                                     dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, dev::GfBlock<SL>::THREADS,
+                                                     dev::gf_smem_bytes<K, T, SL>()));
     return std::max(nb, 1);
   }();
   static const bool prefetch = [] {
@@ -317,7 +331,7 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
   if (ng < 0) ng = v.n_gf;
   if (ng == 0) return;
   const int grid = (int)((ng + SL - 1) / SL);
-  dev::gfam_tensor_apply<K, T, TM, SL><<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
+  kern<<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
       (int)ng, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
       prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr, glist,
       d->z1_c0, v.n_owned);

@@ -825,265 +825,21 @@ constexpr size_t gf_smem_bytes() {
   return sizeof(T) * 2 * SLOTS * GfLayout<K>::SLOT + (size_t)sizeof(T) * SLOTS * (GfShape<K>::NCP + 1);
 }
 
-template <int K, typename T, int TM, int GF_SLOTS>
-__global__ void __launch_bounds__(GfBlock<GF_SLOTS>::THREADS, GfBlock<GF_SLOTS>::MIN_BLOCKS)
-gfam_tensor_apply(int ngf, const int* __restrict__ gx, const double* __restrict__ gcoef, double scale_,
-                  const T* __restrict__ x, T* __restrict__ y, long n_r1 = 0, const T* __restrict__ g = nullptr,
-                  const T* __restrict__ Dinv = nullptr, T* __restrict__ dv = nullptr, T* xw = nullptr,
-                  double c1_ = 0, double c2_ = 0, const T* __restrict__ xc = nullptr, int pf = 0,
-                  int xpf = 0, const int2* __restrict__ r1run = nullptr, const int* __restrict__ glist = nullptr,
-                  double c0_ = 0, long n_own = 0) {
-  constexpr bool Z1 = TM == TA_CHEB_Z1;
-  constexpr bool DVX = TM == TA_CHEB_X1 || Z1, PRO = TM == TA_CHEB_P01;
-  constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
-  constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
-  using S = GfShape<K>;
-  if (pf > 0 && !glist) {   // the table rows of the block one resident wave ahead -> L2 (their first touch is DRAM latency)
-    const long fb = ((long)blockIdx.x + pf) * GF_SLOTS;
-    const long bytes = (long)GF_SLOTS * GfShape<K>::ROW * 4, off = (long)threadIdx.x * 128;
-    if (fb < ngf && off < bytes && fb * GfShape<K>::ROW * 4 + off < (long)ngf * GfShape<K>::ROW * 4)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(gx + fb * (long)GfShape<K>::ROW) + off));
-  }
-  using LY = GfLayout<K>;
-  constexpr int N1 = S::N1, NL = S::NL, ROW = S::ROW, NP = S::NP;
-  if (xpf > 0 && !glist) {
-    // the x values (and, r1run, the epilogue's g, D^-1, dv runs) of the block xpf
-    // blocks ahead -> L2: its table row is already in L2 (prefetched pf > xpf ahead),
-    // so these requests turn its DRAM-latency gathers into L2 hits
-    const long qb = ((long)blockIdx.x + xpf) * GF_SLOTS + threadIdx.x / NL;
-    if (threadIdx.x / NL < GF_SLOTS && qb < ngf) {
-      const int* rq = gx + qb * (long)ROW;
-      const int ln = threadIdx.x % NL;
-#pragma unroll
-      for (int z = 0; z < N1; ++z) {
-        const int i = decode_dof(__ldg(rq + z * NL + ln));
-        if (i >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(x + i));
-      }
-      if (TM != TA_APPLY && r1run) {
-        const int2 run = __ldg(r1run + qb);
-        const int per_line = 128 / (int)sizeof(T);
-        for (int c = ln * per_line; c < run.y; c += NL * per_line) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(g + run.x + c));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(Dinv + run.x + c));
-          if (RDV && !DVX) asm volatile("prefetch.global.L2 [%0];" ::"l"(dv + run.x + c));
-        }
-      }
-    }
-  }
-  extern __shared__ __align__(16) unsigned char gf_smem[];
-  T* s0 = reinterpret_cast<T*>(gf_smem);
-  T* s1 = s0 + GF_SLOTS * LY::SLOT;
-  T* cbase = s1 + GF_SLOTS * LY::SLOT;             // PRO: G's coarse patch per slot
-  const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;
-  const long qi = (long)blockIdx.x * GF_SLOTS + slot;
-  const bool act = slot < GF_SLOTS && qi < ngf;
-  // glist: a subset of the grandfamilies (interior / boundary ones, overlap with the import)
-  const long q0 = glist ? (act ? (long)__ldg(glist + qi) : 0) : qi;
-  const int* rp = gx + (act ? q0 : 0) * (long)ROW;
-  T* const a0 = s0 + (act ? slot : 0) * LY::SLOT;
-  T* const a1 = s1 + (act ? slot : 0) * LY::SLOT;
-  T* const cb = cbase + (act ? slot : 0) * (S::NCP + 1);
-  const T scale = (T)(act && gcoef ? scale_ * __ldg(gcoef + q0) : scale_);
-  const int px = lane % N1, py = lane / N1;
-  int gi[N1];
-  T u[N1], ukeep[N1];
-  T inc[PRO ? N1 : 1];
-  T pg[N1], pd[N1], pv[N1];   // fused modes: g, D^-1, dv of the R1 rows
-  int own = 0;
-  if (act) {              // z lines: lane = (px, py)
-#pragma unroll
-    for (int z = 0; z < N1; ++z) {
-      const int e = __ldg(rp + z * NL + lane);
-      gi[z] = decode_dof(e);
-      if (PRO && e >= 0) own |= 1 << z;
-    }
-#pragma unroll
-    for (int z = 0; z < N1; ++z) {
-      const int i = gi[z];
-      if (Z1) u[z] = i < 0 ? T(0) : (i < n_own ? (T)c0_ * __ldg(Dinv + i) * __ldg(g + i) : __ldg(x + i));
-      else u[z] = i >= 0 ? __ldg(x + i) : T(0);
-    }
-  }
-  if constexpr (PRO) {
-    // x + P x_{l-1}: every fine node from one parent containing it, in
-    // warp_prolongate's order (x, y, z passes, fma chains over ascending coarse
-    // index); nodes on a face between two parents get the same bits from either
-    // (the 1-D weight across the face is an exact pick of the shared coarse node)
-    constexpr int N = K + 1, NC1 = 2 * K + 1;
-    if (act)
-      for (int c = lane; c < S::NCP; c += NL) {
-        const int ci = __ldg(rp + NP + c);
-        cb[c] = ci >= 0 ? __ldg(xc + ci) : T(0);
-      }
-    __syncthreads();
-    if (act) {
-      const int cx = px <= 2 * K ? 0 : 1, cy = py <= 2 * K ? 0 : 1;   // a containing parent in x, y
-      const int lx = px - 2 * K * cx, ly = py - 2 * K * cy;
-      T wx[N], wy[N];
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        wx[a] = wy[a] = T(0);
-#pragma unroll
-        for (int p = 0; p < NC1; ++p) {
-          if (lx == p) wx[a] = (T)Q<K>::P(p, a);
-          if (ly == p) wy[a] = (T)Q<K>::P(p, a);
-        }
-      }
-      T w[2][N];
-#pragma unroll
-      for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-          w[cz][c] = T(0);
-#pragma unroll
-          for (int b = 0; b < N; ++b) {
-            T sx = T(0);
-#pragma unroll
-            for (int a = 0; a < N; ++a)
-              sx = fma(wx[a], cb[(K * cx + a) + NC1 * (K * cy + b) + NC1 * NC1 * (K * cz + c)], sx);
-            w[cz][c] = fma(wy[b], sx, w[cz][c]);
-          }
-        }
-#pragma unroll
-      for (int z = 0; z < N1; ++z) {
-        const int cz = z <= 2 * K ? 0 : 1, lz = z - 2 * K * cz;
-        T sz = T(0);
-#pragma unroll
-        for (int c = 0; c < N; ++c)
-          if (Q<K>::P(lz, c) != 0.0) sz = fma((T)Q<K>::P(lz, c), w[cz][c], sz);
-        inc[z] = sz;
-      }
-    }
-  }
-  if (act) {
-    if constexpr (PRO) {
-#pragma unroll
-      for (int z = 0; z < N1; ++z)
-        if (gi[z] >= 0) u[z] = u[z] + inc[z];
-    }
-#pragma unroll
-    for (int z = 0; z < N1; ++z) ukeep[z] = u[z];
-#pragma unroll
-    for (int z = 0; z < N1; ++z) {
-      T t1 = 0, t2 = 0;
-#pragma unroll
-      for (int q = 0; q < N1; ++q) {
-        if (Mt4<K>(z, q) != 0.0) t1 = fma((T)Mt4<K>(z, q), u[q], t1);
-        if (Kt4<K>(z, q) != 0.0) t2 = fma((T)Kt4<K>(z, q), u[q], t2);
-      }
-      const int ia = LY::ax * px + LY::ay * py + LY::az * z;
-      a0[ia] = t1;
-      a1[ia] = t2;
-    }
-    if (TM != TA_APPLY && GF_LOAD_AT == 1) {   // in flight across the y and x passes
-#pragma unroll
-      for (int z = 0; z < N1; ++z) {
-        const int i = gi[z];
-        pg[z] = pd[z] = pv[z] = T(0);
-        if (i >= 0 && i < n_r1) {
-          pg[z] = __ldg(g + i);
-          pd[z] = __ldg(Dinv + i);
-          if (RDV && !DVX) pv[z] = dv[i];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  T t1[N1], t2[N1];
-  const int pz = lane / N1;     // y lines: lane = (px, pz)
-  if (act) {
-    const int ba = LY::ax * px + LY::az * pz;
-#pragma unroll
-    for (int q = 0; q < N1; ++q) {
-      t1[q] = a0[ba + LY::ay * q];
-      t2[q] = a1[ba + LY::ay * q];
-    }
-  }
-  __syncthreads();
-  if (act) {
-    const int bb_ = LY::bx * px + LY::bz * pz;
-#pragma unroll
-    for (int yy = 0; yy < N1; ++yy) {
-      T a = 0, bb = 0;
-#pragma unroll
-      for (int q = 0; q < N1; ++q) {
-        if (Mt4<K>(yy, q) != 0.0) {
-          a = fma((T)Mt4<K>(yy, q), t1[q], a);
-          bb = fma((T)Mt4<K>(yy, q), t2[q], bb);
-        }
-        if (Kt4<K>(yy, q) != 0.0) bb = fma((T)Kt4<K>(yy, q), t1[q], bb);
-      }
-      a0[bb_ + LY::by * yy] = a;
-      a1[bb_ + LY::by * yy] = bb;
-    }
-  }
-  __syncthreads();
-  T out[N1];
-  if (act) {              // x lines: lane = (py, pz)
-    const int qy = lane % N1, qz = lane / N1;
-    const int bx = LY::by * qy + LY::bz * qz;
-#pragma unroll
-    for (int q = 0; q < N1; ++q) {
-      t1[q] = a0[bx + LY::bx * q];
-      t2[q] = a1[bx + LY::bx * q];
-    }
-#pragma unroll
-    for (int xx = 0; xx < N1; ++xx) {
-      T o = 0;
-#pragma unroll
-      for (int q = 0; q < N1; ++q) {
-        if (Kt4<K>(xx, q) != 0.0) o = fma((T)Kt4<K>(xx, q), t1[q], o);
-        if (Mt4<K>(xx, q) != 0.0) o = fma((T)Mt4<K>(xx, q), t2[q], o);
-      }
-      out[xx] = scale * o;
-    }
-  }
-  __syncthreads();        // every lane has read layout B
-  if (act) {              // x-line results -> layout N (first buffer, reused), read back along z lines
-    const int qy = lane % N1, qz = lane / N1;
-    const int bn = LY::ny * qy + LY::nz * qz;
-#pragma unroll
-    for (int q = 0; q < N1; ++q) a0[bn + LY::nx * q] = out[q];
-  }
-  if (TM != TA_APPLY && GF_LOAD_AT == 2 && act) {
-#pragma unroll
-    for (int z = 0; z < N1; ++z) {
-      const int i = gi[z];
-      pg[z] = pd[z] = pv[z] = T(0);
-      if (i >= 0 && i < n_r1) {
-        pg[z] = __ldg(g + i);
-        pd[z] = __ldg(Dinv + i);
-        if (RDV && !DVX) pv[z] = dv[i];
-      }
-    }
-  }
-  __syncthreads();
-  if (act) {
-    const bool inner = px > 0 && px < 4 * K && py > 0 && py < 4 * K;
-    const int bn = LY::nx * px + LY::ny * py;
-#pragma unroll
-    for (int z = 0; z < N1; ++z) {
-      const int i = gi[z];
-      if (i < 0) continue;
-      const T v = a0[bn + LY::nz * z];
-      if (TM != TA_APPLY && i < n_r1) {
-        if (GF_LOAD_AT == 3) {   // requested here, one row at a time (fewer live registers)
-          pg[z] = __ldg(g + i);
-          pd[z] = __ldg(Dinv + i);
-          if (RDV && !DVX) pv[z] = dv[i];
-        }
-        T dd = (T)c2_ * pd[z] * (pg[z] - v);
-        if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
-        if (WDV) dv[i] = dd;
-        xw[i] = ukeep[z] + dd;
-      } else {
-        if (PRO && ((own >> z) & 1)) dv[i] = inc[z];
-        if (i < n_r1 || (inner && z > 0 && z < 4 * K)) y[i] = v;   // only this patch touches the node
-        else atomicAdd(y + i, v);
-      }
-    }
-  }
-}
+// The kernel, register-capped two ways: through the minimum-blocks bound (8 blocks
+// of 96 threads, 80 registers; the modes whose working set fits -- plain, X1, 01,
+// P01 -- and keep their occupancy), or (_r96) at 96 registers and 7 blocks: TA_CHEB_11
+// and TA_CHEB_10 hold g, D^-1 and dv of the epilogue (27 more values) and spill at 80
+// (44 bytes; 3.5 % / 2 % slower on c5's finest level).
+#define GFAM_NAME gfam_tensor_apply
+#define GFAM_ATTR __launch_bounds__(GfBlock<GF_SLOTS>::THREADS, GfBlock<GF_SLOTS>::MIN_BLOCKS)
+#include "gfam_kernel.inc"
+#undef GFAM_NAME
+#undef GFAM_ATTR
+#define GFAM_NAME gfam_tensor_apply_r96
+#define GFAM_ATTR __maxnreg__(96)
+#include "gfam_kernel.inc"
+#undef GFAM_NAME
+#undef GFAM_ATTR
 
 // 2D form of fam_tensor_apply: a (2k+1)^2 patch has only 2k+1 lines, so one warp
 // packs FPW = 32 / (2k+1) families (6 for Q2, 10 for Q1) instead of leaving
