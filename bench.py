@@ -55,7 +55,7 @@ WORKLOADS = {
           "per GPU (reading R21)",
 }
 SAMPLE = "c3p4"
-KIND_ORDER = ["apply", "cheb_x1", "cheb_11", "cheb_10", "cheb_01", "cheb_00", "cheb_p01", "cheb_stream",
+KIND_ORDER = ["res_restrict", "apply", "cheb_x1", "cheb_11", "cheb_10", "cheb_01", "cheb_00", "cheb_p01", "cheb_stream",
               "cheb_stream_full", "restrict", "prolongate", "coarse"]
 
 

@@ -465,7 +465,9 @@ typedef enum {
   GMG_K_COPY_MG = 13,       /* copy_to_mg / copy_from_mg */
   GMG_K_LEAF_APPLY = 14,
   GMG_K_OTHER = 15,
-  GMG_K_SMALL = 16          /* the small levels' V-cycle in one persistent kernel (small_vcycle) */
+  GMG_K_SMALL = 16,         /* the small levels' V-cycle in one persistent kernel (small_vcycle) */
+  GMG_K_RES_RESTRICT = 17   /* residual + restriction in one operator pass, d_{l-1} += P^T (d_l - K_l x_l)
+                               (TA_RES; replaces APPLY + RESTRICT on 3D tensor levels, GMG_FUSE_RES=0 off) */
 } gmg_kernel_kind;
 typedef struct {
   int kind;                 /* gmg_kernel_kind */

@@ -114,7 +114,7 @@ class KernelStat(C.Structure):
 
 KERNEL_KINDS = ["apply", "cheb_x1", "cheb_11", "cheb_10", "cheb_01", "cheb_00", "cheb_p01", "cheb_stream",
                 "cheb_stream_full", "restrict", "prolongate", "coarse", "exchange", "copy_mg", "leaf_apply", "other",
-                "small_levels"]
+                "small_levels", "res_restrict"]
 
 _vp = C.c_void_p
 _i64p = C.POINTER(C.c_int64)

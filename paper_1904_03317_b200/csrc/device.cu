@@ -51,6 +51,7 @@ struct DevLevel {
   int* singles = nullptr;           // families not in a grandfamily
   double* gcoef = nullptr;          // coefficient per grandfamily (config 4)
   bool fuse_pro = false;            // prolongation fused into the first post-smoothing step on EVERY rank
+  bool fuse_res = false;            // residual + restriction fused (TA_RES) on EVERY rank
   int* perm = nullptr;              // rank-local level index -> device index (API boundary)
   int* leaf_cells = nullptr;
   int* edge_fams = nullptr;
@@ -670,6 +671,34 @@ static bool prolong_fusable(DeviceHierarchy* d, int l) {
   return on && d->lv[l].fuse_pro && d->lv[l].c1.size() > 1;
 }
 
+// The V-cycle's residual and restriction as one operator pass (kernels.cuh TA_RES):
+// d_{l-1} += P^T (d_l - K_l x_l) with every family / grandfamily patch restricting
+// its own contribution, on the levels the 3D tensor kernels run (GMG_FUSE_RES=0:
+// plain operator + export-add of t + warp_restrict).  The decision is collective
+// (fuse_res, set at setup): the level's t is neither written nor export-added,
+// so ranks choosing differently would mismatch their exchanges; d_{l-1} is
+// export-added by the caller as before.
+static bool res_fusable(DeviceHierarchy* d, int l) {
+  static const bool on = [] {
+    const char* e = std::getenv("GMG_FUSE_RES");
+    return !(e && e[0] == '0');
+  }();
+  return on && d->lv[l].fuse_res;
+}
+template <typename T>
+static void res_restrict(DeviceHierarchy* d, int l, T* x, const T* g, T* gc, cudaStream_t s) {
+  DevLevel& v = d->lv[l];
+  // x gathered and d read per level DoF, the operator's index per cell, the parents'
+  // (k+1)^d coarse DoFs per family, d_{l-1} read-modify-written per coarse row
+  const double vb = sizeof(T), coarse = 2.0 * vb * (double)d->lv[l - 1].n + 4.0 * nn_of(d) * (double)v.n_fam;
+  Prof pr(d, s, GMG_K_RES_RESTRICT, l, 2.0 * vb * (double)v.n + 4.0 * nn_of(d) * (double)v.n_cells + coarse,
+          2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam + coarse);
+  if (d->k == 2)
+    import_and_tensor<2, T, dev::TA_RES>(d, l, x, gc, g, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+  else
+    import_and_tensor<1, T, dev::TA_RES>(d, l, x, gc, g, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+}
+
 // V(slk_ls) in one cooperative kernel (kernels.cuh small_vcycle)
 template <typename T>
 static void run_small_levels(DeviceHierarchy* d, cudaStream_t s) {
@@ -697,8 +726,12 @@ static void vcycle_levels(DeviceHierarchy* d, cudaStream_t s) {
     T *g = D + v.off, *x = X + v.off, *t = Tb + v.off, *dv = DV + v.off;
     T* gc = D + d->lv[l - 1].off;
     smooth(d, l, g, x, t, dv, true, s);                                     // 1: pre-smooth from 0
-    apply_full(d, l, x, t, s);                                              // 2: t = K x
-    k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);       // 3: d_{l-1} += P^T (d - t)
+    if (res_fusable(d, l)) {                                                // 2 + 3 in one pass over the level
+      res_restrict(d, l, x, g, gc, s);
+    } else {
+      apply_full(d, l, x, t, s);                                            // 2: t = K x
+      k_restrict<dev::RES_VCYCLE>(d, l, nullptr, v.n_fam, g, t, gc, s);     // 3: d_{l-1} += P^T (d - t)
+    }
     export_add(d, l - 1, gc, s);
   }
   if (d->slk_ls > 0) run_small_levels<T>(d, s);                                 // V(l_s), coarse solve included
@@ -1244,6 +1277,18 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       CK(cudaMemcpyAsync(miss.data(), d->partial, nl * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       for (int l = 0; l < nl; ++l) d->lv[l].fuse_pro = l > 0 && miss[l] == 0.0;
+      // residual + restriction fusion (TA_RES) per level, collectively: it drops the
+      // level's export-add of t, so either every rank runs it or none
+      for (int l = 0; l < nl; ++l) {
+        const DevLevel& v = d->lv[l];
+        miss[l] = l > 0 && Tp.dim == 3 && d->tensor_apply && !v.elem && (v.coef == nullptr || v.fcoef != nullptr)
+                      ? 0.0 : 1.0;
+      }
+      CK(cudaMemcpyAsync(d->partial, miss.data(), nl * sizeof(double), cudaMemcpyHostToDevice, s));
+      allreduce(d, d->partial, nl, s);
+      CK(cudaMemcpyAsync(miss.data(), d->partial, nl * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int l = 0; l < nl; ++l) d->lv[l].fuse_res = miss[l] == 0.0;
     }
     if (d->coarse_cheb) {
       DevLevel& v0 = d->lv[0];

@@ -356,7 +356,26 @@ constexpr int TA_LOAD_AT = TA_LOAD_AT_DEFAULT;
 // rows are finished here; for the other rows the transfer-owner family leaves
 // P x_{l-1} in dv (dead before this step) and cheb_range<..., PRO> adds it.
 enum : int { TA_APPLY = 0, TA_CHEB_01 = 1, TA_CHEB_11 = 2, TA_CHEB_10 = 3, TA_CHEB_00 = 4, TA_CHEB_X1 = 5,
-             TA_CHEB_P01 = 6, TA_CHEB_Z1 = 7 };
+             TA_CHEB_P01 = 6, TA_CHEB_Z1 = 7, TA_RES = 8 };
+// TA_RES: the V-cycle's residual and restriction, d_{l-1} += P^T (d_l - K_l x_l)
+// (P:427-437), in ONE pass over the level instead of the plain operator
+// (t = K x, L2 reductions on shared rows), t's export-add and warp_restrict (which
+// re-reads the patch rows, d and t).  By linearity P^T (d - K x) = sum over patches
+// f of P_f^T (d|_{own f} - K_f x): each fine node's interpolation row is the same
+// functional of the coarse DoFs from every parent whose closure holds it (continuity
+// of the coarse Q_k space; the same exact-pick argument as TA_CHEB_P01), d enters
+// once, through the node's transfer-owner patch (table entry >= 0, R26), and each
+// patch's local operator result enters through its own parent(s).  So every patch
+// restricts its own contribution -- P^T along z in registers on the scatter's z
+// lines, then y and x through shared memory -- and adds (k+1)^3 (family) or
+// (2k+1)^3 (grandfamily) coarse values at L2; y is the coarse defect d_{l-1}, g is
+// d_l.  The level's t is neither written nor read.
+// P over a grandfamily's two parents per direction: fine a in 0..4k, coarse j in 0..2k
+template <int K>
+__host__ __device__ __forceinline__ constexpr double P2(int a, int j) {
+  const int c = a <= 2 * K ? 0 : 1, la = a - 2 * K * c, lj = j - K * c;
+  return lj >= 0 && lj <= K ? Q<K>::P(la, lj) : 0.0;
+}
 // TA_CHEB_Z1: TA_CHEB_X1 without the preceding pass x_1 = c2_0 D^-1 g (the first step
 // from x = 0): the gather forms x_1 = c0 D^-1 g itself on the owned rows (ghost rows:
 // imported x_1, materialised on the owners' send rows), cheb_range<..., Z1> likewise
@@ -380,6 +399,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
   constexpr bool DVX = TM == TA_CHEB_X1 || Z1, PRO = TM == TA_CHEB_P01;
   constexpr bool RDV = TM == TA_CHEB_11 || TM == TA_CHEB_10 || DVX;
   constexpr bool WDV = TM == TA_CHEB_01 || TM == TA_CHEB_11 || DVX || PRO;
+  constexpr bool RES = TM == TA_RES, CHEB = TM != TA_APPLY && !RES;
   constexpr int NP1 = 2 * K + 1, S2 = NP1 * NP1, NL = TensorCfg<K>::NL, FPB = TensorCfg<K>::FPB;
   using LY = PatchLayout<K, T>;
   constexpr int NS = FPB * (LY::sab > LY::sn ? LY::sab : LY::sn);
@@ -412,7 +432,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
     for (int z = 0; z < NP1; ++z) {
       const int e = __ldg(rp + z * S2 + lane);
       gi[z] = decode_dof(e);
-      if (PRO && e >= 0) own |= 1 << z;
+      if ((PRO || RES) && e >= 0) own |= 1 << z;
     }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) {
@@ -477,7 +497,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
     }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
-    if (TM != TA_APPLY && TA_LOAD_AT == 0) {   // requested with the gather: one memory round trip
+    if (CHEB && TA_LOAD_AT == 0) {   // requested with the gather: one memory round trip
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         const int i = gi[z];
@@ -501,7 +521,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
       a0[ia] = t1;
       a1[ia] = t2;
     }
-    if (TM != TA_APPLY && TA_LOAD_AT == 1) {   // in flight across the y and x passes
+    if (CHEB && TA_LOAD_AT == 1) {   // in flight across the y and x passes
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         const int i = gi[z];
@@ -571,7 +591,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
 #pragma unroll
     for (int q = 0; q < NP1; ++q) n0[bn + LY::nx * q] = out[q];
   }
-  if (TM != TA_APPLY && TA_LOAD_AT == 2 && act) {   // the epilogue's loads after the passes (fewer live registers)
+  if (CHEB && TA_LOAD_AT == 2 && act) {   // the epilogue's loads after the passes (fewer live registers)
 #pragma unroll
     for (int z = 0; z < NP1; ++z) {
       const int i = gi[z];
@@ -583,7 +603,68 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
       }
     }
   }
+  if (RES && act) {   // d on the patch nodes this family restricts (transfer owner, R26)
+#pragma unroll
+    for (int z = 0; z < NP1; ++z) pg[z] = ((own >> z) & 1) ? __ldg(g + gi[z]) : T(0);
+  }
   __syncthreads();
+  if constexpr (RES) {
+    // r = d|_own - K_f x on the z line (N read), P^T along z in registers -> s1 as
+    // [jz][py][px]; y pass -> s0 as [jz][jy][px]; x pass -> (k+1)^3 coarse values
+    constexpr int N = K + 1;
+    T* const c1s = s1 + (act ? slot : 0) * LY::sab;
+    if (act) {
+      const int py = lane / NP1;
+      const int bn = LY::nx * px + LY::ny * py;
+      T rc[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) rc[c] = T(0);
+#pragma unroll
+      for (int z = 0; z < NP1; ++z) {
+        if (gi[z] < 0) continue;
+        const T r = pg[z] - n0[bn + LY::nz * z];
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          if (Q<K>::P(z, c) != 0.0) rc[c] = fma((T)Q<K>::P(z, c), r, rc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < N; ++c) c1s[lane + S2 * c] = rc[c];
+    }
+    __syncthreads();     // every lane has read layout N (s0)
+    T* const c0s = s0 + (act ? slot : 0) * LY::sab;
+    if (act && lane < NP1 * N) {   // y lines: (qx, jz)
+      const int qx = lane % NP1, jz = lane / NP1;
+      T w[NP1];
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) w[q] = c1s[qx + NP1 * q + S2 * jz];
+#pragma unroll
+      for (int jy = 0; jy < N; ++jy) {
+        T a = T(0);
+#pragma unroll
+        for (int q = 0; q < NP1; ++q)
+          if (Q<K>::P(q, jy) != 0.0) a = fma((T)Q<K>::P(q, jy), w[q], a);
+        c0s[qx + NP1 * jy + NP1 * N * jz] = a;
+      }
+    }
+    __syncthreads();
+    if (act && lane < N * N) {     // x lines: (jy, jz)
+      const int jy = lane % N, jz = lane / N;
+      T w[NP1];
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) w[q] = c0s[q + NP1 * jy + NP1 * N * jz];
+      constexpr int NPT = NP1 * NP1 * NP1;
+#pragma unroll
+      for (int jx = 0; jx < N; ++jx) {
+        T a = T(0);
+#pragma unroll
+        for (int q = 0; q < NP1; ++q)
+          if (Q<K>::P(q, jx) != 0.0) a = fma((T)Q<K>::P(q, jx), w[q], a);
+        const int ci = __ldg(rp + NPT + jx + N * jy + N * N * jz);
+        if (ci >= 0) atomicAdd(y + ci, a);
+      }
+    }
+    return;
+  }
   if (act) {
     const int py = lane / NP1;
     const bool inner = px > 0 && px < 2 * K && py > 0 && py < 2 * K;
@@ -593,7 +674,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
       const int i = gi[z];
       if (i < 0) continue;
       const T v = n0[bn + LY::nz * z];
-      if (TM != TA_APPLY && i < n_r1) {
+      if (CHEB && i < n_r1) {
         // complete row of an R1 node: Chebyshev step right here
         T dd = (T)c2_ * pd[z] * (pg[z] - v);
         if (RDV) dd = fma((T)c1_, DVX ? ukeep[z] : pv[z], dd);
