@@ -315,6 +315,44 @@ def kernel_table(recs, n_rep, step_s, peak, config, precision):
     return rows
 
 
+def time_level_vmult(ctx, h, info, L, mixed, peak, reps=10):
+    """The plain level operator y = K_L x on the finest level (the paper's "level
+    vmult") timed on its own through gmg_level_apply_kernel: the V-cycle
+    has none since its residual runs fused with the restriction (TA_RES).  CUDA
+    events around each launch on the launching stream; y is zeroed between
+    launches outside the events.  Bytes as DESIGN.md section 6 (kind apply)."""
+    torch = ctx.torch
+    dt = torch.float32 if mixed else torch.float64
+    vb = 4 if mixed else 8
+    n = info["level_dofs"][L]
+    k, dim = info["k"], info["dim"]
+    nn, npch = (k + 1) ** dim, (2 * k + 1) ** dim
+    g = torch.Generator(device=ctx.dev).manual_seed(190403317)
+    xl = (2 * torch.rand(n, device=ctx.dev, dtype=torch.float64, generator=g) - 1).to(dt)
+    yl = torch.zeros_like(xl)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        yl.zero_()
+        h.level_apply_kernel(L, xl, yl)
+    ts = []
+    for _ in range(reps):
+        yl.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h.level_apply_kernel(L, xl, yl)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    t = sum(ts) / len(ts)
+    survey = 2.0 * vb * n + 4.0 * nn * info["level_cells"][L]
+    layout = 2.0 * vb * n + 4.0 * npch * info["level_families"][L]
+    return {"level": L, "launch_us": 1e6 * t, "achieved_gbs": survey / t / 1e9,
+            "frac_survey_bytes": survey / t / 1e9 / peak, "frac_layout_bytes": layout / t / 1e9 / peak,
+            "survey_bytes": survey, "layout_bytes": layout,
+            "source": "gmg_level_apply_kernel on the finest level, %d launches (not in the V-cycle: "
+                      "its residual is fused with the restriction)" % reps}
+
+
 def measure(ctx, args, name, main=True):
     import numpy as np
     torch, G = ctx.torch, ctx.G
@@ -399,7 +437,10 @@ def measure(ctx, args, name, main=True):
         a = plain[0]
         apply_plain = {"level": L, "launch_us": a["launch_us"], "achieved_gbs": a["achieved_gbs"],
                        "frac_survey_bytes": a["frac"], "frac_layout_bytes": a["frac_layout"],
-                       "survey_bytes": a["algorithmic_bytes"], "layout_bytes": a["layout_bytes"]}
+                       "survey_bytes": a["algorithmic_bytes"], "layout_bytes": a["layout_bytes"],
+                       "source": "V-cycle profile"}
+    elif ctx.world == 1:
+        apply_plain = time_level_vmult(ctx, h, info, L, mixed, peak)
     kernels = [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in rows[:10]]
     res = {"config": name, "n_leaf_dofs": n_dofs, "n_free_dofs": info["n_leaf_free"], "levels": info["n_levels"],
            "setup_s": round(setup_s, 2), "value": value, "ms_per_step": 1e3 * step_s, "gpu_launches": launches,
