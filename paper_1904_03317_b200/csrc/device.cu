@@ -311,11 +311,11 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
   if constexpr (R96_MODE) {
     if (gf_r96()) kern = &dev::gfam_tensor_apply_r96<K, T, TM, SL>;
   }
+  constexpr size_t smem = dev::gf_smem_bytes<K, T, SL, TM>();
   static const int per_sm = [kern] {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dev::gf_smem_bytes<K, T, SL>()));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, dev::GfBlock<SL>::THREADS,
-                                                     dev::gf_smem_bytes<K, T, SL>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, dev::GfBlock<SL>::THREADS, smem));
     return std::max(nb, 1);
   }();
   static const bool prefetch = [] {
@@ -332,7 +332,7 @@ static void launch_gf(DeviceHierarchy* d, DevLevel& v, const T* x, T* y, const T
   if (ng < 0) ng = v.n_gf;
   if (ng == 0) return;
   const int grid = (int)((ng + SL - 1) / SL);
-  kern<<<grid, dev::GfBlock<SL>::THREADS, dev::gf_smem_bytes<K, T, SL>(), s>>>(
+  kern<<<grid, dev::GfBlock<SL>::THREADS, smem, s>>>(
       (int)ng, v.gx, v.gcoef, v.scale, x, y, v.n_r1, g, MG<T>::Dinv(v), dv, xw, c1, c2, xc,
       prefetch ? wave : 0, prefetch && xmode > 0 ? wave / 2 : 0, xmode > 1 ? (const int2*)v.gr1 : nullptr, glist,
       d->z1_c0, v.n_owned);

@@ -901,9 +901,12 @@ template <int K> struct GfLayout {
   static constexpr int SS = SA > SB ? (SA > SN ? SA : SN) : (SB > SN ? SB : SN);
   static constexpr int SLOT = SS + ((17 - SS % 16) % 16);   // = 1 mod 16
 };
-template <int K, typename T, int SLOTS>
+// (the coarse patch region only for TA_CHEB_P01: a smaller footprint lets the
+// driver choose a smaller shared-memory carveout, i.e. a larger L1)
+template <int K, typename T, int SLOTS, int TM = TA_CHEB_P01>
 constexpr size_t gf_smem_bytes() {
-  return sizeof(T) * 2 * SLOTS * GfLayout<K>::SLOT + (size_t)sizeof(T) * SLOTS * (GfShape<K>::NCP + 1);
+  return sizeof(T) * 2 * SLOTS * GfLayout<K>::SLOT +
+         (TM == TA_CHEB_P01 ? (size_t)sizeof(T) * SLOTS * (GfShape<K>::NCP + 1) : 0);
 }
 
 // The kernel, register-capped two ways: through the minimum-blocks bound (8 blocks
