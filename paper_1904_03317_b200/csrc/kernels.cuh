@@ -386,7 +386,11 @@ __host__ __device__ __forceinline__ constexpr double P2(int a, int j) {
 template <int K, typename T> struct TensorSmem {
   static constexpr int NS = TensorCfg<K>::FPB * (PatchLayout<K, T>::sab > PatchLayout<K, T>::sn
                                                      ? PatchLayout<K, T>::sab : PatchLayout<K, T>::sn);
-  static constexpr int NCB = TensorCfg<K>::FPB * ((K + 1) * (K + 1) * (K + 1) + 1);
+  // TA_CHEB_P01 per slot: the parent's (k+1)^3 values (+1 pad), then the separable
+  // P passes' results: x pass (2k+1)(k+1)^2, y pass (2k+1)^2 (k+1)
+  static constexpr int NCB1 = (K + 1) * (K + 1) * (K + 1) + 1 + (2 * K + 1) * (K + 1) * (K + 1) +
+                              (2 * K + 1) * (2 * K + 1) * (K + 1);
+  static constexpr int NCB = TensorCfg<K>::FPB * NCB1;
 };
 template <int K, typename T, int TM>
 __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* __restrict__ s1, T* __restrict__ cbf,
@@ -404,7 +408,7 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
   using LY = PatchLayout<K, T>;
   constexpr int NS = FPB * (LY::sab > LY::sn ? LY::sab : LY::sn);
   (void)NS;
-  constexpr int NCB1 = (K + 1) * (K + 1) * (K + 1) + 1;   // PRO: the parents' values, per slot
+  constexpr int NCB1 = TensorSmem<K, T>::NCB1;   // PRO: the parents' values and the P passes, per slot
   const int slot = threadIdx.x / NL, lane = threadIdx.x % NL;   // lane: line of the family's patch
   const long fi = vb * FPB + slot;
   const bool act = slot < FPB && fi < nfam;
@@ -427,6 +431,15 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
   T inc[PRO ? NP1 : 1];          // PRO: (P x_{l-1}) on the z line
   int own = 0;                   // PRO: bit z = the family is the row's transfer owner
   T u[NP1];
+  // PRO: the parent's coarse indices requested first (the coarse gather then goes
+  // out with the fine one)
+  constexpr int NCL = PRO ? ((K + 1) * (K + 1) * (K + 1) + NL - 1) / NL : 1;
+  int cidx[NCL];
+  if (PRO && act) {
+#pragma unroll
+    for (int j = 0; j < NCL; ++j)
+      cidx[j] = lane + j * NL < (K + 1) * (K + 1) * (K + 1) ? __ldg(rp + NP1 * S2 + lane + j * NL) : -1;
+  }
   if (act) {             // z lines: lane = (px, py), gathered straight into registers
 #pragma unroll
     for (int z = 0; z < NP1; ++z) {
@@ -442,43 +455,55 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
     }
   }
   if constexpr (PRO) {
-    // P x_{l-1} on this thread's z line, in registers: the parent's values are
-    // staged once per family, then (P (x) P (x) P) restricted to (px, py, *) in
-    // warp_prolongate's order (x, then y, then z; fma chains over ascending
-    // coarse index; a zero weight adds an exact 0), so the result is its
-    // bit pattern
+    // P x_{l-1} on this thread's z line: the parent's values are staged once per
+    // family, then (P (x) P (x) P) by separable passes in warp_prolongate's order
+    // (x, then y, then z; fma chains over ascending coarse index; a zero weight
+    // adds an exact 0), so the result is its bit pattern
     constexpr int N = K + 1, NC = N * N * N, NPT = NP1 * NP1 * NP1;
-    if (act) {
-      for (int c = lane; c < NC; c += NL) {    // 27 values, 25 lines
-        const int ci = __ldg(rp + NPT + c);
-        cbf[slot * NCB1 + c] = ci >= 0 ? __ldg(xc + ci) : T(0);
+    if (act) {             // 27 values, 25 lines
+#pragma unroll
+      for (int j = 0; j < NCL; ++j)
+        if (lane + j * NL < NC) cbf[slot * NCB1 + lane + j * NL] = cidx[j] >= 0 ? __ldg(xc + cidx[j]) : T(0);
+    }
+    __syncthreads();
+    // separable: x pass over the parent's (y, z) lines, y pass over (x, z), z pass
+    // on this thread's z line -- each an fma chain over ascending coarse index, as
+    // warp_prolongate (x, then y, then z), so the bits are the same
+    T* const cbs = cbf + (act ? slot : 0) * NCB1;
+    T* const bxs = cbs + NC + 1;                  // [c][b][px]
+    T* const bys = bxs + NP1 * N * N;             // [c][py][px]
+    if (act && lane < N * N) {
+      const int b = lane % N, c = lane / N;
+      T v[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) v[a] = cbs[a + N * b + N * N * c];
+#pragma unroll
+      for (int p = 0; p < NP1; ++p) {
+        T sx = T(0);
+#pragma unroll
+        for (int a = 0; a < N; ++a) sx = fma((T)Q<K>::P(p, a), v[a], sx);
+        bxs[p + NP1 * b + NP1 * N * c] = sx;
+      }
+    }
+    __syncthreads();
+    if (act && lane < NP1 * N) {
+      const int qx = lane % NP1, c = lane / NP1;
+      T v[N];
+#pragma unroll
+      for (int b = 0; b < N; ++b) v[b] = bxs[qx + NP1 * b + NP1 * N * c];
+#pragma unroll
+      for (int p = 0; p < NP1; ++p) {
+        T sy = T(0);
+#pragma unroll
+        for (int b = 0; b < N; ++b) sy = fma((T)Q<K>::P(p, b), v[b], sy);
+        bys[qx + NP1 * p + S2 * c] = sy;
       }
     }
     __syncthreads();
     if (act) {
-      const int px = lane % NP1, py = lane / NP1;
-      T wx[N], wy[N];
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        wx[a] = wy[a] = T(0);
-#pragma unroll
-        for (int p = 0; p < NP1; ++p) {
-          if (px == p) wx[a] = (T)Q<K>::P(p, a);
-          if (py == p) wy[a] = (T)Q<K>::P(p, a);
-        }
-      }
       T w[N];
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        w[c] = T(0);
-#pragma unroll
-        for (int b = 0; b < N; ++b) {
-          T sx = T(0);
-#pragma unroll
-          for (int a = 0; a < N; ++a) sx = fma(wx[a], cbf[slot * NCB1 + a + N * b + N * N * c], sx);
-          w[c] = fma(wy[b], sx, w[c]);
-        }
-      }
+      for (int c = 0; c < N; ++c) w[c] = bys[lane + S2 * c];
 #pragma unroll
       for (int z = 0; z < NP1; ++z) {
         T sz = T(0);
@@ -492,8 +517,11 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
   if (act) {
     if constexpr (PRO) {   // the gather above is in flight while P x_{l-1} is formed
 #pragma unroll
-      for (int z = 0; z < NP1; ++z)
+      for (int z = 0; z < NP1; ++z) {
         if (gi[z] >= 0) u[z] = u[z] + inc[z];    // = warp_prolongate's old + fine
+        // P x_{l-1} of a streamed row this family transfer-owns -> dv now (cheb_range<PRO>)
+        if (((own >> z) & 1) && gi[z] >= n_r1) dv[gi[z]] = inc[z];
+      }
     }
 #pragma unroll
     for (int z = 0; z < NP1; ++z) ukeep[z] = u[z];
@@ -603,7 +631,8 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
       }
     }
   }
-  if (RES && act) {   // d on the patch nodes this family restricts (transfer owner, R26)
+  if (RES && act) {   // d on the patch nodes this patch restricts (transfer owner, R26); issued here:
+    // requesting it after the z pass was slower (c5 level 10: 1191-1208 vs 1030-1042 us)
 #pragma unroll
     for (int z = 0; z < NP1; ++z) pg[z] = ((own >> z) & 1) ? __ldg(g + gi[z]) : T(0);
   }
@@ -681,7 +710,6 @@ __device__ __forceinline__ void fam_tensor_body(long vb, T* __restrict__ s0, T* 
         if (WDV) dv[i] = dd;
         xw[i] = ukeep[z] + dd;
       } else {
-        if (PRO && ((own >> z) & 1)) dv[i] = inc[z];  // P x_{l-1} of a streamed row (cheb_range<PRO>)
         if (i < n_r1 || (inner && z > 0 && z < 2 * K)) y[i] = v;   // only this family touches the node
         else atomicAdd(y + i, v);
       }
@@ -877,6 +905,9 @@ template <int K> struct GfShape {
   static constexpr int N1 = 4 * K + 1, NL = N1 * N1, NP = N1 * N1 * N1;
   static constexpr int NCP = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);   // G's family patch one level up
   static constexpr int ROW = NP + NCP;
+  // TA_CHEB_P01 per slot: G's coarse patch (+1 pad), the x pass (4k+1)(2k+1)^2 and the
+  // y pass (4k+1)^2 (2k+1) of the separable prolongation
+  static constexpr int NCB = NCP + 1 + N1 * (2 * K + 1) * (2 * K + 1) + N1 * N1 * (2 * K + 1);
 };
 // Transposition layouts (index = cx x + cy y + cz z, per slot).  fp64 shared
 // memory serves a half-warp per pass over 16 bank pairs, so an access whose 16
@@ -906,7 +937,7 @@ template <int K> struct GfLayout {
 template <int K, typename T, int SLOTS, int TM = TA_CHEB_P01>
 constexpr size_t gf_smem_bytes() {
   return sizeof(T) * 2 * SLOTS * GfLayout<K>::SLOT +
-         (TM == TA_CHEB_P01 ? (size_t)sizeof(T) * SLOTS * (GfShape<K>::NCP + 1) : 0);
+         (TM == TA_CHEB_P01 ? (size_t)sizeof(T) * SLOTS * GfShape<K>::NCB : 0);
 }
 
 // The kernel, register-capped two ways: through the minimum-blocks bound (8 blocks
