@@ -894,6 +894,7 @@ __host__ __device__ __forceinline__ constexpr double Mt4(int i, int j) {
 #define GF_LOAD_AT_DEFAULT 2
 #endif
 constexpr int GF_LOAD_AT = GF_LOAD_AT_DEFAULT;   // fused epilogue loads: 1 after the z pass, 2 after the x pass, 3 per row in the scatter
+static_assert(GF_LOAD_AT >= 1 && GF_LOAD_AT <= 3, "gfam_tensor_apply has no epilogue-load placement 0");
 #ifndef GF_REG_CAP
 #define GF_REG_CAP 80
 #endif
