@@ -24,6 +24,9 @@ ap.add_argument("--n", type=int, default=1, help="c5: GPUs the forest is sized f
 ap.add_argument("--passes", type=int, default=-1)
 ap.add_argument("--mixed", action="store_true")
 ap.add_argument("--eager", action="store_true", help="no CUDA graph")
+ap.add_argument("--apply", action="store_true",
+                help="profile one plain level operator y = K_L x on the finest level (gmg_level_apply_kernel) "
+                     "instead of a V-cycle (the V-cycle runs its residual fused with the restriction)")
 args = ap.parse_args()
 cfg = config_c5(args.n) if args.config == "c5" else config(args.config)
 _, _, h = G.build_config(cfg, passes=args.passes, mixed=args.mixed, graph=not args.eager)
@@ -33,8 +36,21 @@ x = torch.zeros_like(b)
 for _ in range(3):
     h.vcycle(b, x)
 torch.cuda.synchronize()
-torch.cuda.profiler.start()
-h.vcycle(b, x)
-torch.cuda.synchronize()
-torch.cuda.profiler.stop()
+if args.apply:
+    info = h.info()
+    L = info["n_levels"] - 1
+    xl = torch.rand(info["level_dofs"][L], device="cuda", dtype=torch.float64)
+    yl = torch.zeros_like(xl)
+    h.level_apply_kernel(L, xl, yl)
+    yl.zero_()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    h.level_apply_kernel(L, xl, yl)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+else:
+    torch.cuda.profiler.start()
+    h.vcycle(b, x)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 print("levels", h.info()["n_levels"], "gf", h.info()["level_gf"], "r1", h.info()["level_r1"])
