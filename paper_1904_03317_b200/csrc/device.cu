@@ -673,7 +673,7 @@ static bool prolong_fusable(DeviceHierarchy* d, int l) {
 
 // The V-cycle's residual and restriction as one operator pass (kernels.cuh TA_RES):
 // d_{l-1} += P^T (d_l - K_l x_l) with every family / grandfamily patch restricting
-// its own contribution, on the levels the 3D tensor kernels run (GMG_FUSE_RES=0:
+// its own contribution, on the levels the tensor kernels run, 3D and 2D (GMG_FUSE_RES=0:
 // plain operator + export-add of t + warp_restrict).  The decision is collective
 // (fuse_res, set at setup): the level's t is neither written nor export-added,
 // so ranks choosing differently would mismatch their exchanges; d_{l-1} is
@@ -693,10 +693,24 @@ static void res_restrict(DeviceHierarchy* d, int l, T* x, const T* g, T* gc, cud
   const double vb = sizeof(T), coarse = 2.0 * vb * (double)d->lv[l - 1].n + 4.0 * nn_of(d) * (double)v.n_fam;
   Prof pr(d, s, GMG_K_RES_RESTRICT, l, 2.0 * vb * (double)v.n + 4.0 * nn_of(d) * (double)v.n_cells + coarse,
           2.0 * vb * (double)v.n + 4.0 * np_of(d) * (double)v.n_fam + coarse);
-  if (d->k == 2)
+  if (d->dim == 2) {           // warp-packed families (fam_res2d)
+    import_ghosts(d, l, x, s);
+    if (v.n_fam == 0) return;
+    const int np = (2 * d->k + 1) * (2 * d->k + 1), nn = (d->k + 1) * (d->k + 1);
+    const int fpw = 32 / (2 * d->k + 1), per_block = fpw * dev::TENSOR_WARPS;
+    const int grid = (int)((v.n_fam + per_block - 1) / per_block);
+    if (d->k == 2)
+      dev::fam_res2d<2, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>((int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale,
+                                                                    x, g, gc);
+    else
+      dev::fam_res2d<1, T><<<grid, 32 * dev::TENSOR_WARPS, 0, s>>>((int)v.n_fam, v.xfer, np + nn, v.fcoef, v.scale,
+                                                                    x, g, gc);
+    d->launches++;
+  } else if (d->k == 2) {
     import_and_tensor<2, T, dev::TA_RES>(d, l, x, gc, g, nullptr, nullptr, 0.0, 0.0, nullptr, s);
-  else
+  } else {
     import_and_tensor<1, T, dev::TA_RES>(d, l, x, gc, g, nullptr, nullptr, 0.0, 0.0, nullptr, s);
+  }
 }
 
 // V(slk_ls) in one cooperative kernel (kernels.cuh small_vcycle)
@@ -1281,8 +1295,7 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       // level's export-add of t, so either every rank runs it or none
       for (int l = 0; l < nl; ++l) {
         const DevLevel& v = d->lv[l];
-        miss[l] = l > 0 && Tp.dim == 3 && d->tensor_apply && !v.elem && (v.coef == nullptr || v.fcoef != nullptr)
-                      ? 0.0 : 1.0;
+        miss[l] = l > 0 && d->tensor_apply && !v.elem && (v.coef == nullptr || v.fcoef != nullptr) ? 0.0 : 1.0;
       }
       CK(cudaMemcpyAsync(d->partial, miss.data(), nl * sizeof(double), cudaMemcpyHostToDevice, s));
       allreduce(d, d->partial, nl, s);

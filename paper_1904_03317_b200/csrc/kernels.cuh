@@ -1031,6 +1031,95 @@ fam_tensor_apply2d(int nfam, const int* __restrict__ xfer, int row, const double
                    y);
 }
 
+// TA_RES in 2D: the V-cycle's residual and restriction d_{l-1} += P^T (d_l - K_l x_l)
+// on family patches, warp-packed like fam_tensor_apply2d (x lines gathered, one
+// transposition, y lines): r = d|_own - K_f x on each y line, P^T along y in
+// registers, one more transposition, P^T along x, (k+1)^2 coarse values added at
+// L2 (the same linearity argument as the 3D TA_RES; g is d_l, dc is d_{l-1})
+template <int K, typename T>
+__global__ void __launch_bounds__(32 * TENSOR_WARPS)
+fam_res2d(int nfam, const int* __restrict__ xfer, int row, const double* __restrict__ fcoef, double scale_,
+          const T* __restrict__ x, const T* __restrict__ g, T* __restrict__ dc) {
+  constexpr int NP1 = 2 * K + 1, NP = NP1 * NP1, FPW = 32 / NP1, N = K + 1;
+  __shared__ T s0[TENSOR_WARPS][FPW][NP], s1[TENSOR_WARPS][FPW][NP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = lane / NP1, line = lane % NP1;
+  const long f = ((long)blockIdx.x * TENSOR_WARPS + w) * FPW + j;
+  T* const s0j = &s0[w][j < FPW ? j : 0][0];
+  T* const s1j = &s1[w][j < FPW ? j : 0][0];
+  const bool active = j < FPW && f < nfam;
+  const int* rp = xfer + (active ? f : 0) * (long)row;
+  const T scale = (T)(active && fcoef ? scale_ * __ldg(fcoef + f) : scale_);
+  if (active) {        // x lines: line = py
+    const int b = line * NP1;
+    T u[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) {
+      const int gi = decode_dof(__ldg(rp + b + q));
+      u[q] = gi >= 0 ? __ldg(x + gi) : T(0);
+    }
+#pragma unroll
+    for (int xx = 0; xx < NP1; ++xx) {
+      T a = 0, bb = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Kt<K>(xx, q) != 0.0) a = fma((T)Kt<K>(xx, q), u[q], a);
+        if (Mt<K>(xx, q) != 0.0) bb = fma((T)Mt<K>(xx, q), u[q], bb);
+      }
+      s0j[b + xx] = a;
+      s1j[b + xx] = bb;
+    }
+  }
+  __syncwarp();
+  T rc[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) rc[c] = T(0);
+  if (active) {        // y lines: line = px; r and P^T along y
+    T a[NP1], bb[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) {
+      a[q] = s0j[line + q * NP1];
+      bb[q] = s1j[line + q * NP1];
+    }
+#pragma unroll
+    for (int yy = 0; yy < NP1; ++yy) {
+      T o = 0;
+#pragma unroll
+      for (int q = 0; q < NP1; ++q) {
+        if (Mt<K>(yy, q) != 0.0) o = fma((T)Mt<K>(yy, q), a[q], o);
+        if (Kt<K>(yy, q) != 0.0) o = fma((T)Kt<K>(yy, q), bb[q], o);
+      }
+      const int e = __ldg(rp + line + yy * NP1);
+      const int i = decode_dof(e);
+      if (i < 0) continue;
+      const T r = (e >= 0 ? __ldg(g + i) : T(0)) - scale * o;
+#pragma unroll
+      for (int c = 0; c < N; ++c)
+        if (Q<K>::P(yy, c) != 0.0) rc[c] = fma((T)Q<K>::P(yy, c), r, rc[c]);
+    }
+  }
+  __syncwarp();        // every lane has read the y-line inputs
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) s0j[line + NP1 * c] = rc[c];
+  }
+  __syncwarp();
+  if (active && line < N) {   // x lines of the coarse rows: jy = line
+    T v[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) v[q] = s0j[q + NP1 * line];
+#pragma unroll
+    for (int jx = 0; jx < N; ++jx) {
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < NP1; ++q)
+        if (Q<K>::P(q, jx) != 0.0) acc = fma((T)Q<K>::P(q, jx), v[q], acc);
+      const int ci = __ldg(rp + NP + jx + N * line);
+      if (ci >= 0) atomicAdd(dc + ci, acc);
+    }
+  }
+}
+
 // cell_dofs is SoA: dof of local node b of cell c at cell_dofs[b * ldc + c]
 template <int D, int K, typename T>
 __global__ void __launch_bounds__(128) cell_apply(int n, const int* __restrict__ list,

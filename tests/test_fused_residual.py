@@ -38,10 +38,11 @@ print("KINDS", ",".join(kinds))
 """
 
 CASES = [("c3", 4, {}, False), ("c3", 4, {}, True), ("c4", -1, {"s": 2, "lmax": 7}, False),
-         ("c3", 4, {"k": 1}, False), ("c5", 2, {"shell": (96, 1024)}, False)]
+         ("c3", 4, {"k": 1}, False), ("c5", 2, {"shell": (96, 1024)}, False), ("c2", -1, {}, False),
+         ("c1", -1, {}, False)]
 
 
-@pytest.mark.parametrize("name,passes,over,mixed", CASES, ids=["c3p4", "c3p4-mixed", "c4s", "c3p4-k1", "c5-thick-p2"])
+@pytest.mark.parametrize("name,passes,over,mixed", CASES, ids=["c3p4", "c3p4-mixed", "c4s", "c3p4-k1", "c5-thick-p2", "c2-2d-q2", "c1-2d-q1"])
 def test_fused_residual_matches_separate(tmp_path, name, passes, over, mixed):
     outs, kinds = [], []
     for fuse in ("1", "0"):
