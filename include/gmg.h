@@ -376,7 +376,11 @@ gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_ce
 /* One V-cycle (P:318-327 with local smoothing P:413-469), x = V(b), x0 = 0:
  * Chebyshev-Jacobi pre/post smoothing of degree m on S rows, residual with the
  * edge matrices (E rows), restriction R = P^T, recursion, dense coarse solve,
- * prolongation.  b and x must not alias. */
+ * prolongation.  On the levels the family-patch kernels run, the residual and
+ * the restriction are one pass (each patch restricts d|_own - K_patch x; by
+ * linearity the same d_{l-1} += P^T (d_l - K_l x_l) up to the order of the
+ * additions), and the prolongation rides on the first post-smoothing step.
+ * b and x must not alias. */
 gmg_status gmg_vcycle(gmg_hierarchy *h, const double *b_dev, double *x_dev, void *cuda_stream);
 
 /* Preconditioned CG on the leaf system (hanging nodes condensed, Dirichlet

@@ -17,14 +17,14 @@ ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control no
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_c3.csv python bench.py --profile --config c3 --secondary none --no-cpu-baseline --steps 2 --warmup 3 \
     > $OUT/ncu_launch_c3.log 2>&1
-# tensor launches of a V-cycle start on the finest level: pre-smoothing X1, 11, 11, 10, then the
+# tensor launches of a V-cycle start on the finest level: pre-smoothing X1, 11, 10 (degree 4), then the
 # residual + restriction TA_RES (c5: each a grandfamily + a family kernel; c3's finest level: family only)
 NCU="ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:tensor_apply"
 $NCU --launch-skip 2 --launch-count 2 -o $OUT/ncu_c5_cheb11 -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full.log 2>&1
-$NCU --launch-skip 8 --launch-count 2 -o $OUT/ncu_c5_res -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full_c5r.log 2>&1
+$NCU --launch-skip 6 --launch-count 2 -o $OUT/ncu_c5_res -f python tools/ncu_vcycle.py --config c5 > $OUT/ncu_full_c5r.log 2>&1
 $NCU --launch-count 2 -o $OUT/ncu_c5_apply -f python tools/ncu_vcycle.py --config c5 --apply > $OUT/ncu_full_c5a.log 2>&1
 $NCU --launch-skip 1 --launch-count 1 -o $OUT/ncu_c3_cheb11 -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3b.log 2>&1
-$NCU --launch-skip 4 --launch-count 1 -o $OUT/ncu_c3_res -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3r.log 2>&1
+$NCU --launch-skip 3 --launch-count 1 -o $OUT/ncu_c3_res -f python tools/ncu_vcycle.py --config c3 > $OUT/ncu_full_c3r.log 2>&1
 $NCU --launch-count 1 -o $OUT/ncu_c3_apply -f python tools/ncu_vcycle.py --config c3 --apply > $OUT/ncu_full_c3.log 2>&1
 
 # the reports themselves stay on the box (gpurun copies back <= 64 MiB): raw metrics
