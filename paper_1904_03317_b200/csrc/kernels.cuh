@@ -269,7 +269,10 @@ __host__ __device__ __forceinline__ constexpr double Mt(int i, int j) {
   return s;
 }
 
-constexpr int TENSOR_WARPS = 8;
+#ifndef TENSOR_WARPS_DEFAULT
+#define TENSOR_WARPS_DEFAULT 4   // 2D kernels: warps per block (4: c2 V-cycle 0.634 -> 0.601 ms against 8; 2: 0.604)
+#endif
+constexpr int TENSOR_WARPS = TENSOR_WARPS_DEFAULT;
 
 // one 1-D pass over `lines` lines of a 3-index array: in(i, q, o) -> out(i, p, o),
 // out = sum_q M(p, q) in, with M = P (UP: q < N, p < NP1) or P^T (!UP)
