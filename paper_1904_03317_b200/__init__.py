@@ -257,7 +257,7 @@ class Forest:
         self.h = handle
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:   # _lib is None at interpreter shutdown
             _lib.gmg_forest_destroy(self.h)
             self.h = None
 
@@ -315,7 +315,7 @@ class Partitioning:
         self.n_ranks = n_ranks
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:   # _lib is None at interpreter shutdown
             _lib.gmg_partition_destroy(self.h)
             self.h = None
 
@@ -380,7 +380,7 @@ class Hierarchy:
         self._n_ranks = i["n_ranks"]
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:   # _lib is None at interpreter shutdown
             _lib.gmg_hierarchy_destroy(self.h)
             self.h = None
 
@@ -585,7 +585,7 @@ class LocalWorld:
         self.n = n
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:   # _lib is None at interpreter shutdown
             _lib.gmg_local_world_destroy(self.h)
             self.h = None
 
@@ -644,7 +644,7 @@ class NcclComm:
         _check(_lib.gmg_nccl_comm_init(C.create_string_buffer(uid, 128), n_ranks, rank, C.byref(self.h)))
 
     def destroy(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:   # _lib is None at interpreter shutdown
             _lib.gmg_nccl_comm_destroy(self.h)
             self.h = None
 

@@ -538,7 +538,7 @@ static void k_cheb(DeviceHierarchy* d, DevLevel& v, const T* g, T* t, T* dv, T* 
   const int nvec = 3 + (RT ? 2 : 0) + (RDV && !DVX ? 1 : 0) + (!XZ ? 1 : 0) + (WDV ? 1 : 0);
   Prof pr(d, s, GMG_K_CHEB_STREAM_FULL, (int)(&v - d->lv.data()), (double)nvec * sizeof(T) * (double)v.n_pad);
   // n_pad is a multiple of VEC_PAD: the grid covers the padded segment exactly
-  dev::cheb_step<T, RT, RDV, WDV, XZ, DVX><<<(int)(v.n_pad / dev::VEC_PAD), dev::VEC_NT, 0, s>>>(
+  dev::cheb_step<T, RT, RDV, WDV, XZ, DVX><<<(int)(v.n_pad / (2 * dev::CHEB_NT)), dev::CHEB_NT, 0, s>>>(
       (const V2*)g, (const V2*)MG<T>::Dinv(v), (V2*)t, (V2*)dv, (V2*)x, c1, c2);
   d->launches++;
 }
@@ -585,7 +585,7 @@ static void cheb_step_fused(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T
     if (n > 0) {
       const int nvec = 6 + (RDV && !DVX ? 1 : 0) + (WDV ? 1 : 0) + (PRO ? 1 : 0);   // g D t x (+dv) | t x (+dv)
       Prof pr2(d, s, GMG_K_CHEB_STREAM, l, (double)nvec * sizeof(T) * (double)n);
-      dev::cheb_range<T, RDV, WDV, DVX, PRO, Z1><<<(int)((n + dev::VEC_NT - 1) / dev::VEC_NT), dev::VEC_NT, 0, s>>>(
+      dev::cheb_range<T, RDV, WDV, DVX, PRO, Z1><<<(int)((n + dev::CHEB_NT - 1) / dev::CHEB_NT), dev::CHEB_NT, 0, s>>>(
           v.n_r1, v.n_pad, g, MG<T>::Dinv(v), t, dv, x, c1, c2, v.n_owned, c0);
       d->launches++;
     }
@@ -1163,6 +1163,8 @@ DeviceHierarchy* device_create(LocalTopo& Tp, const gmg_params& prm, std::unique
       int bps = 2;
       if (const char* e = std::getenv("GMG_SLK_BPS")) bps = std::max(1, std::atoi(e));
       d->slk_grid = std::max(1, std::min(per_sm, bps)) * d->sms;
+      if (const char* e = std::getenv("GMG_SLK_GRID"))   // a fixed number of CTAs (few CTAs: cheaper barriers)
+        d->slk_grid = std::max(1, std::min(std::atoi(e), per_sm * d->sms));
       if (per_sm < 1) d->slk_ls = 0;
     }
     for (double** p : {&d->D, &d->X, &d->T, &d->DV, &d->W, &d->Y, &d->cx, &d->cr, &d->cp, &d->cq, &d->cz}) {

@@ -1214,6 +1214,13 @@ __global__ void cell_load(int n, const int* __restrict__ list, const int* __rest
 // padding, so the grid covers the segment exactly (no bounds branch).
 constexpr int VEC_NT = 256;
 constexpr int VEC_PAD = 2 * VEC_NT;
+// block size of the launches of cheb_step / cheb_range (<= VEC_NT, so that a
+// padded segment is a whole number of cheb_step blocks)
+#ifndef CHEB_NT_DEFAULT
+#define CHEB_NT_DEFAULT 256
+#endif
+constexpr int CHEB_NT = CHEB_NT_DEFAULT;
+static_assert(VEC_PAD % (2 * CHEB_NT) == 0, "cheb_step covers a padded segment exactly");
 template <typename T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
@@ -1226,7 +1233,7 @@ __global__ void __launch_bounds__(VEC_NT) cheb_step(const typename Vec2<S>::type
                                                     typename Vec2<S>::type* __restrict__ x, double c1_, double c2_) {
   using V2 = typename Vec2<S>::type;
   const S c1 = (S)c1_, c2 = (S)c2_;
-  const long i = (long)blockIdx.x * VEC_NT + threadIdx.x;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const V2 G = g[i];
   V2 T = {S(0), S(0)}, V = T, X = T;
   if (READ_T) T = t[i];
@@ -1270,7 +1277,7 @@ __global__ void __launch_bounds__(VEC_NT) cheb_range(long a, long n, const T* __
                                                      const T* __restrict__ Dinv, T* __restrict__ t,
                                                      T* __restrict__ dv, T* __restrict__ x, double c1_, double c2_,
                                                      long n_own = 0, double c0_ = 0) {
-  const long i = a + (long)blockIdx.x * VEC_NT + threadIdx.x;
+  const long i = a + (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const T G = g[i], Tv = t[i], Di = Dinv[i];
   T X = Z1 ? (T)c0_ * Di * G : x[i];   // Z1: x_1 = c2_0 D^-1 g (see TA_CHEB_Z1)
