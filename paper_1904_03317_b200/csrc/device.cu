@@ -106,8 +106,12 @@ struct DeviceHierarchy {
   dev::SlkLevel* slk_dev = nullptr;
   cudaStream_t cstream = nullptr;   // the import's side stream
   cudaGraphExec_t vgraph = nullptr;
+  // gmg_vcycle's variant: copy_to_mg has already formed the finest level's x_1 =
+  // c2_0 D^-1 g (gather_to_mg's x1 arguments), so that level's first pass is skipped
+  cudaGraphExec_t vgraph_x1 = nullptr;
+  bool skip_x1 = false;             // set while such a V-cycle is launched / captured
   cudaStream_t cap = nullptr;
-  long long launches = 0, per_vcycle = 0, per_leaf_apply = 0;
+  long long launches = 0, per_vcycle = 0, per_vcycle_x1 = 0, per_leaf_apply = 0;
   std::vector<std::pair<void*, size_t>> allocs;
   // caller's allocator hooks (gmg_params.dev_alloc / dev_free), else cudaMalloc / cudaFree
   void* (*dev_alloc)(size_t, void*, void*) = nullptr;
@@ -629,7 +633,7 @@ static void smooth(DeviceHierarchy* d, int l, const T* g, T* x, T* t, T* dv, boo
     j0 = 2;
   } else if (x_zero && m > 1) {
     // x_1 = dv_0 = c2_0 D^-1 g: only x is stored, the next step reads dv_0 from x
-    k_cheb<T, false, false, false, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
+    if (!(d->skip_x1 && l == d->L)) k_cheb<T, false, false, false, true>(d, v, g, t, dv, x, 0.0, v.c2[0], s);
     cheb_step_fused<T, dev::TA_CHEB_X1, true, true, true>(d, l, g, x, t, dv, v.c1[1], v.c2[1], s);
     j0 = 2;
   } else if (x_zero) {
@@ -796,14 +800,18 @@ static void upload_slk(DeviceHierarchy* d, cudaStream_t s) {
   CK(cudaStreamSynchronize(s));
 }
 
-static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s) {
+// x1_done: the caller has formed the finest level's x_1 (fuse_x1)
+static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s, bool x1_done = false) {
+  d->skip_x1 = x1_done;
   if (!d->use_graph) {
     upload_slk(d, s);
     if (d->mixed) vcycle_levels<float>(d, s);
     else vcycle_levels<double>(d, s);
+    d->skip_x1 = false;
     return;
   }
-  if (!d->vgraph) {
+  cudaGraphExec_t& ge = x1_done ? d->vgraph_x1 : d->vgraph;
+  if (!ge) {
     upload_slk(d, s);
     long long before = d->launches;
     cudaGraph_t g;
@@ -811,13 +819,27 @@ static void run_vcycle_mg(DeviceHierarchy* d, cudaStream_t s) {
     if (d->mixed) vcycle_levels<float>(d, d->cap);
     else vcycle_levels<double>(d, d->cap);
     CK(cudaStreamEndCapture(d->cap, &g));
-    CK(cudaGraphInstantiate(&d->vgraph, g, 0));
+    CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphDestroy(g));
-    d->per_vcycle = d->launches - before;
+    (x1_done ? d->per_vcycle_x1 : d->per_vcycle) = d->launches - before;
     d->launches = before;
   }
-  CK(cudaGraphLaunch(d->vgraph, s));
-  d->launches += d->per_vcycle;
+  d->skip_x1 = false;
+  CK(cudaGraphLaunch(ge, s));
+  d->launches += x1_done ? d->per_vcycle_x1 : d->per_vcycle;
+}
+
+// The finest level's first pre-smoothing pass x_1 = c2_0 D^-1 g can ride on
+// copy_to_mg (gmg_vcycle only; GMG_FUSE_X1=0 restores the pass): that level's
+// defect is complete once gathered (no restriction adds into it), the pass is a
+// pure row-wise map of it, and the smoother takes the separate-pass branch there.
+static bool fuse_x1(const DeviceHierarchy* d) {
+  static const bool on = [] {
+    const char* e = std::getenv("GMG_FUSE_X1");
+    return !(e && e[0] == '0');
+  }();
+  const DevLevel& v = d->lv[d->L];
+  return on && d->L >= 1 && d->L > d->slk_ls && v.c1.size() > 1 && v.n_pad > 0 && !(z1_enabled() && v.n_r1 > 0);
 }
 
 // leaf operator in MG layout: q = lam * Y, Y = A_leaf p (hanging nodes via E rows)
@@ -1369,6 +1391,7 @@ void device_destroy(DeviceHierarchy* d) {
   if (!d) return;
   cudaDeviceSynchronize();
   if (d->vgraph) cudaGraphExecDestroy(d->vgraph);
+  if (d->vgraph_x1) cudaGraphExecDestroy(d->vgraph_x1);
   for (cudaEvent_t e : d->evpool) cudaEventDestroy(e);
   for (auto& v : d->lv) {
     if (v.ev_pack) cudaEventDestroy(v.ev_pack);
@@ -1387,14 +1410,21 @@ void device_destroy(DeviceHierarchy* d) {
 // ---------------------------------------------------------------- API ops
 void device_vcycle(DeviceHierarchy* d, const double* b, double* x, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  const bool fx1 = fuse_x1(d);
   {
   const size_t vb = d->mixed ? 4 : 8;
-  Prof pr(d, s, GMG_K_COPY_MG, -1, 8.0 * (double)d->n_leaf + (4.0 + vb) * (double)d->N);
-  if (d->mixed) dev::gather_to_mg<float><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32);   // copy_to_mg
-  else dev::gather_to_mg<double><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D);
+  Prof pr(d, s, GMG_K_COPY_MG, -1, 8.0 * (double)d->n_leaf + (4.0 + vb) * (double)d->N +
+                                      (fx1 ? 2.0 * vb * (double)d->lv[d->L].n_pad : 0.0));
+  const DevLevel& vL = d->lv[d->L];
+  const i64 lo = fx1 ? vL.off : 0, hi = fx1 ? vL.off + vL.n_pad : 0;
+  const double c20 = fx1 ? vL.c2[0] : 0.0;
+  if (d->mixed)                                                                                 // copy_to_mg
+    dev::gather_to_mg<float><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D32, lo, hi, vL.Dinv32, d->X32, c20);
+  else
+    dev::gather_to_mg<double><<<grid4(d->N), 256, 0, s>>>(d->N, d->mg_to_leaf, b, d->D, lo, hi, vL.Dinv, d->X, c20);
   d->launches++;
   }
-  run_vcycle_mg(d, s);
+  run_vcycle_mg(d, s, fx1);
   if (d->n_leaf) {                                                                              // copy_from_mg
     Prof pr(d, s, GMG_K_COPY_MG, -1, (4.0 + 8.0 + (d->mixed ? 4 : 8)) * (double)d->n_leaf);
     if (d->mixed) dev::gather_from_mg<float><<<grid4(d->n_leaf), 256, 0, s>>>(d->n_leaf, d->leaf_to_mg, d->X32, x);
@@ -1629,6 +1659,10 @@ void device_set_eigen(DeviceHierarchy* d, int l, double lam) {
     cudaGraphExecDestroy(d->vgraph);
     d->vgraph = nullptr;
   }
+  if (d->vgraph_x1) {
+    cudaGraphExecDestroy(d->vgraph_x1);
+    d->vgraph_x1 = nullptr;
+  }
 }
 
 // gmg_profile_vcycle: n_rep eager V-cycles (no graph) with every launch bracketed
@@ -1673,7 +1707,8 @@ int device_profile_vcycle(DeviceHierarchy* d, const double* b, double* x, int n_
 
 long long device_launches(const DeviceHierarchy* d) { return d->launches; }
 void device_launch_profile(const DeviceHierarchy* d, long long* pv, long long* pl) {
-  *pv = d->per_vcycle;
+  // the graph gmg_vcycle launches (its x_1 variant when that is in use), else the CG's
+  *pv = d->per_vcycle_x1 ? d->per_vcycle_x1 : d->per_vcycle;
   *pl = d->per_leaf_apply;
 }
 

@@ -1754,19 +1754,35 @@ __device__ __forceinline__ void store4(T* p, T a, T b, T c, T d, bool vec) {
   }
 }
 
+// x1 (optional, [x1_lo, x1_hi) a whole padded level segment, both multiples of 4):
+// the first pre-smoothing step from x = 0 on that level, x_1 = c2_0 D^-1 g
+// (cheb_step<..., X_ZERO>'s expression), formed here from the values just
+// gathered instead of by a pass that re-reads g (the finest level of gmg_vcycle)
 template <typename T>
 __global__ void __launch_bounds__(256) gather_to_mg(long n, const int* __restrict__ inv, const double* __restrict__ in,
-                                                    T* __restrict__ out) {
+                                                    T* __restrict__ out, long x1_lo = 0, long x1_hi = 0,
+                                                    const T* __restrict__ Dinv = nullptr, T* __restrict__ x1 = nullptr,
+                                                    double c2_ = 0) {
   const long i0 = ((long)blockIdx.x * 256 + threadIdx.x) * 4;
+  const T c2 = (T)c2_;
   if (i0 + 3 < n) {
     const int4 s = *reinterpret_cast<const int4*>(inv + i0);   // inv: device allocation, i0 % 4 == 0
+    const bool fx = i0 >= x1_lo && i0 < x1_hi;
+    T d0 = T(0), d1 = T(0), d2 = T(0), d3 = T(0);
+    if (fx) {
+      const T* dp = Dinv + (i0 - x1_lo);
+      d0 = __ldg(dp); d1 = __ldg(dp + 1); d2 = __ldg(dp + 2); d3 = __ldg(dp + 3);
+    }
     const T a = s.x >= 0 ? (T)__ldg(in + s.x) : T(0), b = s.y >= 0 ? (T)__ldg(in + s.y) : T(0);
     const T c = s.z >= 0 ? (T)__ldg(in + s.z) : T(0), d = s.w >= 0 ? (T)__ldg(in + s.w) : T(0);
     store4(out + i0, a, b, c, d, true);                        // MG layout: device allocation
+    if (fx) store4(x1 + i0, c2 * d0 * a, c2 * d1 * b, c2 * d2 * c, c2 * d3 * d, true);
   } else {
     for (long i = i0; i < n; ++i) {
       const int s = inv[i];
-      out[i] = s >= 0 ? (T)in[s] : T(0);
+      const T a = s >= 0 ? (T)in[s] : T(0);
+      out[i] = a;
+      if (i >= x1_lo && i < x1_hi) x1[i] = c2 * Dinv[i - x1_lo] * a;
     }
   }
 }
