@@ -380,6 +380,9 @@ gmg_status gmg_export_cell_dofs(const gmg_hierarchy *h, int level, int64_t *n_ce
  * the restriction are one pass (each patch restricts d|_own - K_patch x; by
  * linearity the same d_{l-1} += P^T (d_l - K_l x_l) up to the order of the
  * additions), and the prolongation rides on the first post-smoothing step.
+ * The copy of b into the level vectors (copy_to_mg) also forms the
+ * finest level's first smoothing iterate x_1 = c2_0 D^-1 d (P:882-887 from
+ * x_0 = 0): the same expression on the same values as the separate pass.
  * b and x must not alias. */
 gmg_status gmg_vcycle(gmg_hierarchy *h, const double *b_dev, double *x_dev, void *cuda_stream);
 
